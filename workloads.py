@@ -1,0 +1,114 @@
+"""Seeded synthetic workloads (BASELINE.json configs) -- harness, not product.
+
+The paper's evaluation graphs are not available offline; these seeded
+synthetic graphs with the BASELINE.json shapes stand in for them (SURVEY.md
+§8(d)).  Each generator restates the construction the survey specifies so
+the reference and the GPU consume the identical CSR; the committed golden
+fixtures carry a digest of every generated CSR so a drift is caught.
+
+All generators return a ``paper_2301_01356_b200.graphs.Graph``
+(int64 offsets, uint32 targets -- the reference layout, graphs.py:43-58).
+"""
+
+import hashlib
+
+import numpy as np
+
+from paper_2301_01356_b200.graphs import Graph, symmetrize
+
+
+def csr_digest(g: Graph) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(g.offsets, np.int64).tobytes())
+    h.update(np.ascontiguousarray(g.edges, np.uint32).tobytes())
+    return h.hexdigest()
+
+
+def chain(n: int) -> Graph:
+    """Path 0-1-...-(n-1) (same graph as reference gen_chain, graphs.py:236-241)."""
+    i = np.arange(max(n - 1, 0), dtype=np.int64)
+    return symmetrize(np.column_stack([i, i + 1]), n)
+
+
+def grid(rows: int, cols: int, circular: bool = False, keep_prob: float = 1.0,
+         seed: int = 0) -> Graph:
+    """rows x cols lattice, optional wraparound, edges kept i.i.d. with
+    ``keep_prob`` from PCG64(seed).  Candidate order (all horizontal, then all
+    vertical, row-major) matches reference gen_grid (graphs.py:244-268) so the
+    same seed keeps the same edges."""
+    n = rows * cols
+    ids = np.arange(n, dtype=np.int64).reshape(rows, cols)
+    if circular:
+        hs, hd = ids, np.roll(ids, -1, axis=1)
+        vs, vd = ids, np.roll(ids, -1, axis=0)
+    else:
+        hs, hd = ids[:, :-1], ids[:, 1:]
+        vs, vd = ids[:-1, :], ids[1:, :]
+    u = np.concatenate([hs.ravel(), vs.ravel()])
+    v = np.concatenate([hd.ravel(), vd.ravel()])
+    if keep_prob < 1.0:
+        keep = np.random.Generator(np.random.PCG64(seed)).random(u.size) < keep_prob
+        u, v = u[keep], v[keep]
+    return symmetrize(np.column_stack([u, v]), n)
+
+
+def uniform(n: int = 1 << 20, avg: int = 8, seed: int = 0) -> Graph:
+    """Config 2: avg*n endpoint pairs drawn uniformly from PCG64(seed)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    pairs = rng.integers(0, n, size=(avg * n, 2), dtype=np.int64)
+    return symmetrize(pairs, n)
+
+
+def knn2d(npts: int = 10**6, k: int = 5, seed: int = 0) -> Graph:
+    """Config 3: k nearest neighbours of uniform float32 points in the unit
+    square (float64 KD-tree query with k+1, self dropped)."""
+    from scipy.spatial import cKDTree
+
+    pts = np.random.Generator(np.random.PCG64(seed)).random((npts, 2), dtype=np.float32)
+    p64 = pts.astype(np.float64)
+    _, idx = cKDTree(p64).query(p64, k=k + 1)
+    src = np.repeat(np.arange(npts, dtype=np.int64), k + 1)
+    dst = idx.reshape(-1).astype(np.int64)
+    keep = src != dst
+    return symmetrize(np.column_stack([src[keep], dst[keep]]), npts)
+
+
+def rmat(scale: int = 25, edge_factor: int = 16, seed: int = 0,
+         chunk: int = 1 << 24) -> Graph:
+    """Config 5: RMAT with (a, b, c, d) quadrant probabilities, MSB first,
+    chunks of 2^24 edges from one PCG64(seed) stream, no permutation."""
+    n = 1 << scale
+    total = edge_factor * n
+    rng = np.random.Generator(np.random.PCG64(seed))
+    parts = []
+    done = 0
+    while done < total:
+        k = min(chunk, total - done)
+        u = np.zeros(k, np.int64)
+        v = np.zeros(k, np.int64)
+        for lvl in range(scale):
+            r = rng.random(k)
+            bit = np.int64(1) << np.int64(scale - 1 - lvl)
+            # (a, b, c, d) = (0.57, 0.19, 0.19, 0.05): cumulative 0.57/0.76/0.95
+            row = r >= 0.76                                 # quadrant c or d
+            col = ((r >= 0.57) & (r < 0.76)) | (r >= 0.95)  # quadrant b or d
+            u |= np.where(row, bit, 0)
+            v |= np.where(col, bit, 0)
+        parts.append(np.column_stack([u, v]))
+        done += k
+    return symmetrize(np.concatenate(parts), n)
+
+
+CONFIGS = {
+    "1": ("torus 300x300 p=0.6", lambda: grid(300, 300, circular=True, keep_prob=0.6, seed=0)),
+    "2": ("uniform n=2^20 m=8n", lambda: uniform()),
+    "3": ("2-D kNN 10^6 k=5", lambda: knn2d()),
+    "4a": ("torus 10^4x10^4", lambda: grid(10**4, 10**4, circular=True)),
+    "4b": ("torus 10^3x10^5 p=0.6", lambda: grid(10**3, 10**5, circular=True, keep_prob=0.6, seed=0)),
+    "4c": ("chain 10^8", lambda: chain(10**8)),
+    "5": ("RMAT scale 25 ef 16", lambda: rmat()),
+}
+
+
+def make(name: str) -> Graph:
+    return CONFIGS[name][1]()
