@@ -1,0 +1,329 @@
+"""Benchmark: FAST-BCC on one B200 (or N independent replicas under torchrun).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One step = the whole six-stage hot path (forest, rooting, tags, fence,
+skeleton connectivity, labelling incl. per-edge labels and articulation
+flags) over the BASELINE.json headline workload, config 2 (uniform random
+graph, n = 2^20, m = 8n, seed 0; synthetic -- the paper's graphs are not
+available offline).  ``value`` = undirected edges/s with the CSR resident in
+HBM; ``e2e`` = the same metric through the public API ``fast_bcc(g)`` with
+the CSR in pinned host memory and the results copied back every step.
+L2 (126 MB) is flushed by a 256 MiB device write before every timed step
+(the config-2 CSR, 71 MB, would otherwise stay L2-resident).
+
+``--impl reference`` times the reference algorithm's CPU implementation
+(the golden-pinned C port in oracle/, all host threads) on the same
+workload -- the reference itself is Python/numba and cannot travel to the
+GPU box.
+
+Multi-GPU: the path does not shard; N ranks run N
+replicas, value = N * E * K / max-over-ranks time.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "undirected edges/sec (full BCC, 1 B200)"
+UNIT = "edges/s"
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# Algorithmic bytes per launch of the main kernels: each
+# kernel reads its contract inputs once and writes its outputs once, 4-byte
+# ids, gathers counted at element size (no sector amplification).
+def alg_bytes(kind, n, m, T, E, K1=0):
+    csr = 8 * (n + 1) + 4 * m
+    return {
+        "link_rest": csr + 4 * n + 8 * T,           # one full connectivity pass over the CSR
+        "sample_link": 16 * n + 4 * n + 8 * n,
+        "compress": 8 * n,
+        "walk0": 2 * n * (4 + 8),                    # read succ, write (segment, offset)
+        "positions": n * (16 + 16 + 8 + 4) + 2 * n * 8 * 2,
+        "w_gather": csr + 8 * m + 16 * n + 8 * n,    # (parent, first) per arc + row record + A
+        "tile": 2 * n * 16 + 16 * n,                 # A + P in, partials out
+        "fence": n * (16 + 16 + 16 + 4),
+        "edge_blocks": csr + E * (4 + 4 + 4) + 12 * n,
+        "tree_scatter": n * (16 + 8 + 16) + 4 * 2 * (n - 1) * 2,
+        "link_slots": 2 * n * (4 + 4 + 8 + 4),
+    }.get(kind)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, p in zip(names, parts[2:]):
+                if p.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(g, runs=3):
+    """The reference algorithm on the host cores (golden-pinned C port)."""
+    import oracle
+
+    oracle.build()
+    E = g.m // 2
+    oracle.fast_bcc(g.offsets, g.edges)  # warm-up
+    secs = []
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        oracle.fast_bcc(g.offsets, g.edges)
+        secs.append(time.perf_counter() - t0)
+    s = statistics.median(secs)
+    return {"value": E / s, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port",
+            "sample": f"full config-2 graph ({E} edges), median of {runs} runs after 1 warm-up, "
+                      f"{s:.3f} s/run", "seconds_per_run": s}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import workloads
+
+    g = workloads.make(args.config)
+    E = g.m // 2
+    import oracle
+
+    oracle.build()
+    for _ in range(args.warmup):
+        oracle.fast_bcc(g.offsets, g.edges)
+    secs = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.fast_bcc(g.offsets, g.edges)
+        secs.append(time.perf_counter() - t0)
+    tot = sum(secs)
+    value = E * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": _config(args, g),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port",
+                         "sample": f"full config-{args.config} graph per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(args, g):
+    import workloads
+
+    return {"workload": f"config {args.config}: {workloads.CONFIGS[args.config][0]} (seed 0)",
+            "n": g.n, "undirected_edges": g.m // 2, "directed_slots": g.m,
+            "l2": "flushed between timed steps (256 MiB device write)", "parallelism": "replicas"}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import workloads
+    from paper_2301_01356_b200 import Graph, fast_bcc
+    from paper_2301_01356_b200 import _lib
+    from paper_2301_01356_b200.bcc import run_device
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    g = workloads.make(args.config)
+    n, m = g.n, g.m
+    E = m // 2
+    off = torch.from_numpy(g.offsets).to(dev)
+    adj = torch.from_numpy(g.edges.view(np.int32)).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(profile=False):
+        return run_device(off, adj, profile=profile)
+
+    for _ in range(max(args.warmup, 1)):
+        res, stats = step()
+    torch.cuda.synchronize()
+    T = n - int(stats.num_components)
+
+    # ---- timed region: device-resident CSR -------------------------------
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    per_kernel = {}
+    stage_ms = np.zeros(6)
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record()
+            res, stats = step(profile=True)
+            ends[k].record()
+            launches += int(stats.launches)
+            stage_ms += np.array(list(stats.stage_ms))
+            for i in range(stats.nprof):
+                name = _lib.kernel_name(stats.prof_kind[i])
+                tot, cnt = per_kernel.get(name, (0.0, 0))
+                per_kernel[name] = (tot + float(stats.prof_ms[i]), cnt + 1)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * E * args.steps / (total_ms / 1e3)
+
+    # ---- e2e: public API, pinned host CSR in, results out -----------------
+    gp = Graph(g.offsets, g.edges)
+    gp._pinned = (torch.from_numpy(g.offsets).pin_memory(), torch.from_numpy(g.edges.view(np.int32)).pin_memory())
+    fast_bcc(gp, device=dev)
+    torch.cuda.synchronize()
+    e2e_s = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        lab = fast_bcc(gp, device=dev)
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_total = sum(e2e_s)
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    h2d = 8 * (n + 1) + 4 * m
+    d2h = 4 * n + 4 * n + 4 * E + n + 64
+
+    if rank == 0:
+        peaks, src = _peaks()
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        # dominant kernel = the kernel kind with the largest device time per step
+        kern = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                    "ms_per_launch": v[0] / v[1]} for k, v in per_kernel.items()}
+        dom = max((k for k in kern if alg_bytes(k, n, m, T, E) is not None), key=lambda k: kern[k]["ms_per_step"])
+        b = alg_bytes(dom, n, m, T, E)
+        ach = b / (kern[dom]["ms_per_launch"] / 1e3) / 1e9
+        traffic = None
+        prof = ROOT / "profiles" / "ncu_traffic.json"
+        if prof.exists():
+            try:
+                traffic = json.loads(prof.read_text()).get(f"config{args.config}", {}).get(dom)
+            except Exception:
+                traffic = None
+        sum_alg = 46 * m + 165 * n + 48 * T + 16  # SURVEY §8(d) end-to-end algorithmic bytes
+        ms = total_ms / args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": _config(args, g),
+            "e2e": {"value": world * E * args.steps / e2e_total, "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": 1e3 * e2e_total / args.steps},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                         "frac": ach / hbm, "traffic": traffic, "peak_source": src,
+                         "alg_bytes_per_launch": b},
+            "pipeline_roofline": {"alg_bytes": sum_alg, "achieved_gbs": sum_alg / (ms / 1e3) / 1e9,
+                                  "frac": sum_alg / (ms / 1e3) / 1e9 / hbm},
+            "stage_ms": dict(zip(["forest", "rooting", "tags", "fence", "skeleton_cc", "labelling"],
+                                 [float(x) for x in stage_ms / args.steps])),
+            "kernels": kern,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "num_bccs": int(stats.num_bccs), "num_components": int(stats.num_components),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(g)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,114 @@
+/*
+ * fastbcc_b200.h -- C ABI of the B200-native FAST-BCC hot path.
+ *
+ * Library: paper_2301_01356_b200/libfastbcc_b200.so (sm_100a, built by
+ * paper_2301_01356_b200/build.py).  Plain pointers and sizes only; every
+ * array argument is a DEVICE pointer owned by the caller, and ``stream`` is a
+ * cudaStream_t passed as void*.  The library never allocates device memory
+ * inside a run: the caller provides one workspace of fbcc_workspace_bytes().
+ *
+ * Reference interface replaced (all under /root/reference/pkg/src/fastbcc):
+ *   fbcc_run            fast_bcc(g, *, beta, seed, block) -> BccLabeling
+ *                       bcc.py:147-196, plus articulation_points
+ *                       bcc.py:222-235 and the per-edge labels derived by the
+ *                       rule of bcc.py:24-27 (canonical: min edge id per block,
+ *                       edge ids in tv_skeleton order, baselines.py:251-257)
+ *   fbcc_workspace_bytes  (no reference counterpart: scratch is allocated by
+ *                       _meter inside each step, _meter.py:30-74)
+ *   fbcc_strerror       the reference's ValueError messages
+ *                       (euler_tour.py:349-357, 402-403; graphs.py:126-130)
+ * Input layout is the reference Graph unchanged (graphs.py:43-58): int64
+ * offsets[n+1], uint32 targets[m], symmetric, sorted rows, no self-loops or
+ * duplicates (not validated, exactly like the reference, graphs.py:53).
+ */
+#ifndef FASTBCC_B200_H
+#define FASTBCC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define FBCC_OK 0
+#define FBCC_ERR_ARG 1        /* null pointer / negative size / bad flag     */
+#define FBCC_ERR_TOO_LARGE 2  /* n > 2^30 (euler_tour.py:402-403) or m >= 2^31 */
+#define FBCC_ERR_WORKSPACE 3  /* workspace_bytes smaller than required        */
+#define FBCC_ERR_CUDA 4       /* a CUDA runtime error (see fbcc_last_cuda_error) */
+#define FBCC_ERR_CYCLE 5      /* list ranking: cycle (euler_tour.py:349-351)  */
+#define FBCC_ERR_COVER 6      /* list ranking: not a disjoint cover (:353-355) */
+
+/* run flags */
+#define FBCC_FLAG_TIMING 1u   /* record per-stage CUDA-event times in stats   */
+#define FBCC_FLAG_PROFILE 2u  /* also bracket every launch with CUDA events   */
+#define FBCC_MAX_PROFILE 512
+
+/* Outputs of one run; all DEVICE pointers.  label/head are required. */
+typedef struct {
+  int32_t *label;      /* [n] BccLabeling.label: min id of v's skeleton component */
+  int32_t *head;       /* [n] BccLabeling.head: -1 for root singletons and non-labels */
+  int32_t *edge_label; /* [E] or NULL: min edge id of the edge's block;
+                          edge e = e-th arc (u -> v, u < v) in CSR order */
+  uint8_t *is_ap;      /* [n] or NULL: articulation-point flags */
+  int32_t *comp;       /* [n] or NULL: first-pass component labels (min id) */
+} fbcc_outputs;
+
+/* Optional intermediate exports for stage-level parity (DEVICE pointers,
+   each may be NULL).  Written after the run, outside the per-stage timers. */
+typedef struct {
+  int32_t *forest;  /* [2n] (u, v) of the forest edge that hooked vertex x, at
+                       [2x, 2x+1]; meaningful where comp[x] != x            */
+  int32_t *parent;  /* [n] rooted forest (RootedForest, euler_tour.py:38-54) */
+  int32_t *first;   /* [n] */
+  int32_t *last;    /* [n] */
+  int32_t *w1;      /* [n] VertexTags (tagging.py:42-49)                     */
+  int32_t *w2;      /* [n] */
+  int32_t *low;     /* [n] */
+  int32_t *high;    /* [n] */
+  uint8_t *fence;   /* [n] skeleton_record fence bit (connectivity.py:94-96) */
+} fbcc_debug;
+
+/* Host-side statistics of one run. stage_ms: S1 forest, S2 rooting,
+   S3 tags, S4 fence, S5 skeleton CC, S6 labelling (CUDA events; only with
+   FBCC_FLAG_TIMING, else zeros). */
+typedef struct {
+  int64_t num_bccs;
+  int64_t num_components;
+  int64_t num_edges;
+  float stage_ms[6];
+  float total_ms;
+  int32_t launches;                       /* kernels launched by this run    */
+  int32_t nprof;                          /* FBCC_FLAG_PROFILE: entries below */
+  int32_t prof_kind[FBCC_MAX_PROFILE];    /* kernel kind (fbcc_kernel_name)  */
+  float prof_ms[FBCC_MAX_PROFILE];        /* device time between its events   */
+} fbcc_stats;
+
+/* Required workspace bytes for a graph of n vertices and m directed slots. */
+int fbcc_workspace_bytes(int64_t n, int64_t m, size_t *bytes_out);
+
+/* The whole pipeline on a device-resident CSR.  Asynchronous on ``stream``
+   except for one final synchronisation that reads back the three counts. */
+int fbcc_run(const int64_t *offsets, const uint32_t *edges, int64_t n,
+             int64_t m, void *workspace, size_t workspace_bytes,
+             fbcc_outputs *out, fbcc_debug *debug, fbcc_stats *stats,
+             void *stream, uint32_t flags);
+
+/* Name of a kernel kind reported in fbcc_stats.prof_kind. */
+const char *fbcc_kernel_name(int kind);
+
+/* Human-readable message for a status code (reference wording). */
+const char *fbcc_strerror(int code);
+
+/* Last CUDA error string recorded by this thread (for FBCC_ERR_CUDA). */
+const char *fbcc_last_cuda_error(void);
+
+/* ABI version (major * 100 + minor). */
+int fbcc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTBCC_B200_H */

@@ -1,0 +1,98 @@
+"""ctypes binding of ``libfastbcc_b200.so`` (the C ABI in include/fastbcc_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every entry point raises.
+"""
+
+import ctypes
+import threading
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libfastbcc_b200.so"
+
+FBCC_OK = 0
+FBCC_ERR_ARG = 1
+FBCC_ERR_TOO_LARGE = 2
+FBCC_ERR_WORKSPACE = 3
+FBCC_ERR_CUDA = 4
+FBCC_ERR_CYCLE = 5
+FBCC_ERR_COVER = 6
+FBCC_FLAG_TIMING = 1
+FBCC_FLAG_PROFILE = 2
+FBCC_MAX_PROFILE = 512
+
+# every symbol the header declares (checked by tests/test_abi.py)
+EXPORTS = ("fbcc_workspace_bytes", "fbcc_run", "fbcc_strerror", "fbcc_last_cuda_error", "fbcc_version",
+           "fbcc_kernel_name")
+
+
+class FbccOutputs(ctypes.Structure):
+    _fields_ = [("label", ctypes.c_void_p), ("head", ctypes.c_void_p), ("edge_label", ctypes.c_void_p),
+                ("is_ap", ctypes.c_void_p), ("comp", ctypes.c_void_p)]
+
+
+class FbccDebug(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_void_p) for k in
+                ("forest", "parent", "first", "last", "w1", "w2", "low", "high", "fence")]
+
+
+class FbccStats(ctypes.Structure):
+    _fields_ = [("num_bccs", ctypes.c_int64), ("num_components", ctypes.c_int64),
+                ("num_edges", ctypes.c_int64), ("stage_ms", ctypes.c_float * 6), ("total_ms", ctypes.c_float),
+                ("launches", ctypes.c_int32), ("nprof", ctypes.c_int32),
+                ("prof_kind", ctypes.c_int32 * 512), ("prof_ms", ctypes.c_float * 512)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load the extension (building it first if the .so is missing)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            from . import build
+
+            build.build()
+        L = ctypes.CDLL(str(LIB_PATH))
+        P = ctypes.c_void_p
+        L.fbcc_workspace_bytes.restype = ctypes.c_int
+        L.fbcc_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t)]
+        L.fbcc_run.restype = ctypes.c_int
+        L.fbcc_run.argtypes = [P, P, ctypes.c_int64, ctypes.c_int64, P, ctypes.c_size_t,
+                               ctypes.POINTER(FbccOutputs), ctypes.POINTER(FbccDebug),
+                               ctypes.POINTER(FbccStats), P, ctypes.c_uint32]
+        L.fbcc_strerror.restype = ctypes.c_char_p
+        L.fbcc_strerror.argtypes = [ctypes.c_int]
+        L.fbcc_last_cuda_error.restype = ctypes.c_char_p
+        L.fbcc_version.restype = ctypes.c_int
+        L.fbcc_kernel_name.restype = ctypes.c_char_p
+        L.fbcc_kernel_name.argtypes = [ctypes.c_int]
+        _lib = L
+        return L
+
+
+def check(rc: int) -> None:
+    if rc == FBCC_OK:
+        return
+    L = load()
+    msg = L.fbcc_strerror(rc).decode()
+    if rc == FBCC_ERR_CUDA:
+        raise RuntimeError(f"{msg}: {L.fbcc_last_cuda_error().decode()}")
+    if rc == FBCC_ERR_WORKSPACE:
+        raise MemoryError(msg)
+    raise ValueError(msg)
+
+
+def workspace_bytes(n: int, m: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(load().fbcc_workspace_bytes(n, m, ctypes.byref(out)))
+    return int(out.value)
+
+
+def kernel_name(kind: int) -> str:
+    return load().fbcc_kernel_name(int(kind)).decode()

@@ -1,0 +1,183 @@
+// common.cuh -- shared device helpers for the FAST-BCC sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fbcc {
+
+constexpr int kNumSMs = 148;   // B200
+constexpr int kINF = 0x7FFFFFFF;
+
+// Device-side scalars shared by the stages (lives at the head of the
+// workspace).  Counts that only the device knows stay here so that no stage
+// needs a host round trip (the whole run is one asynchronous stream).
+struct Scalars {
+  int ncomp;       // c: number of components of the first pass (roots)
+  int giant;       // sampled most-frequent root (Afforest skip)
+  int nbccs;       // number of blocks
+  int err;         // error bits
+  int num_edges;   // E
+  int pad[59];
+};
+
+// ---------------------------------------------------------------------------
+// launch log: counts every launch of ours and, in profile mode, brackets
+// each with CUDA events on the launching stream (per-kernel device time)
+// ---------------------------------------------------------------------------
+enum KernelKind : int {
+  K_IOTA = 0, K_SAMPLE_LINK, K_COMPRESS, K_FIND_GIANT, K_LINK_REST, K_ROOT_FLAGS, K_SCAN, K_TREE_DEGREE,
+  K_TREE_SCATTER, K_LINK_SLOTS, K_LINK_ROOTS, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_POSITIONS,
+  K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_AP, K_UPPER_DEGREE, K_SET_EDGES, K_EDGE_BLOCKS,
+  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_NUM_KINDS
+};
+
+struct LaunchLog {
+  static constexpr int kMax = 512;
+  bool profile = false;
+  int count = 0;        // our kernels (memsets excluded)
+  int nrec = 0;
+  int kind[kMax];
+  cudaEvent_t ev[kMax + 1];
+  cudaStream_t st = nullptr;
+};
+
+extern thread_local LaunchLog* g_log;
+
+inline void note(KernelKind k) {
+  LaunchLog* L = g_log;
+  if (!L) return;
+  if (k != K_MEMSET) L->count += (k == K_SCAN) ? 2 : 1;  // a CUB scan is init + scan kernels
+  if (L->profile && L->nrec < LaunchLog::kMax) {
+    cudaEventCreate(&L->ev[L->nrec + 1]);
+    cudaEventRecord(L->ev[L->nrec + 1], L->st);
+    L->kind[L->nrec++] = k;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// memory-order helpers
+// ---------------------------------------------------------------------------
+// Union-find parents are written concurrently by CAS; reads must not be
+// served from a stale L1 line (relaxed, gpu scope -> L2).
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ int4 ld_nc4(const int4* p) { return __ldg(p); }
+
+// streaming (read-once) 128-bit load that does not allocate in L1
+__device__ __forceinline__ int4 ld_stream4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// hashing (splitter choice, sampling)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352dU;
+  x ^= x >> 15; x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+// ---------------------------------------------------------------------------
+// launch geometry: grid-stride loops over a grid sized to the machine
+// ---------------------------------------------------------------------------
+inline int grid_for(int64_t items, int block, int max_waves = 16) {
+  int64_t g = (items + block - 1) / block;
+  int64_t cap = (int64_t)kNumSMs * max_waves;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// CSR row search: largest v in [lo, hi] with off[v] <= a (off[lo] <= a).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int row_of(const int64_t* __restrict__ off, int lo, int hi, int64_t a) {
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (__ldg(off + mid) <= a) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// Arc-balanced CSR traversal.  Every thread owns kItems consecutive arcs
+// (one 32-byte sector of targets, loaded as two 128-bit vectors); a warp
+// finds its row window with two full binary searches and each lane then
+// searches inside the window.  The visitor sees rows in order:
+//   begin(v, row_start, row_end)  arc(v, a, w)  end(v, whole)
+// where ``whole`` says the row lies entirely inside this thread's chunk (no
+// other thread touches it -- plain stores are safe; otherwise combine with
+// atomics).  Hub rows with 600k arcs are spread over 75k threads.
+// ---------------------------------------------------------------------------
+constexpr int kItems = 8;
+
+template <class Visitor>
+__device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off,
+                                                 const uint32_t* __restrict__ adj,
+                                                 int n, int64_t m, Visitor& vis) {
+  const int64_t nchunks = (m + kItems - 1) / kItems;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t warp_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
+  for (int64_t wbase = warp_id * 32; wbase < nchunks; wbase += warps_total * 32) {
+    // warp window [vlo, vhi]
+    int64_t first_a = wbase * kItems;
+    int64_t last_chunk = wbase + 31 < nchunks ? wbase + 31 : nchunks - 1;
+    int64_t last_a = last_chunk * kItems;
+    int s = 0;
+    if (lane == 0) s = row_of(off, 0, n - 1, first_a);
+    if (lane == 1) s = row_of(off, 0, n - 1, last_a);
+    int vlo = __shfl_sync(0xffffffffu, s, 0);
+    int vhi = __shfl_sync(0xffffffffu, s, 1);
+    int64_t q = wbase + lane;
+    if (q >= nchunks) continue;
+    int64_t a0 = q * kItems;
+    int64_t a1 = a0 + kItems < m ? a0 + kItems : m;
+    uint32_t w[kItems];
+    if (vec_ok && a1 - a0 == kItems) {
+      int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
+      int4 y = ld_stream4(reinterpret_cast<const int4*>(adj + a0 + 4));
+      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+      w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;
+    }
+    int v = row_of(off, vlo, vhi, a0);
+    int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+    vis.begin(v, rs, re);
+#pragma unroll
+    for (int i = 0; i < kItems; i++) {
+      int64_t a = a0 + i;
+      if (a < a1) {
+        if (a >= re) {
+          vis.end(v, rs >= a0);
+          v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, vhi, a);
+          rs = __ldg(off + v);
+          re = __ldg(off + v + 1);
+          vis.begin(v, rs, re);
+        }
+        vis.arc(v, a, (int)w[i]);
+      }
+    }
+    vis.end(v, rs >= a0 && re <= a1);
+  }
+}
+
+// warp-aggregated increment of a global counter
+__device__ __forceinline__ void warp_count_add(int* ctr, bool pred) {
+  unsigned b = __ballot_sync(__activemask(), pred);
+  if (b && (threadIdx.x & 31) == (__ffs(b) - 1)) atomicAdd(ctr, __popc(b));
+}
+
+}  // namespace fbcc

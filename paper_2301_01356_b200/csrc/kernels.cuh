@@ -1,0 +1,70 @@
+// kernels.cuh -- stage entry points shared between the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace fbcc {
+
+struct Graph {
+  const int64_t* off;    // [n+1] reference layout (graphs.py:43-58)
+  const uint32_t* adj;   // [m]
+  int n;
+  int64_t m;
+};
+
+// Device arrays for the rooting / tags stages (see api.cu for the layout).
+struct Rooting {
+  int* rootidx;    // [n+1] exclusive scan of (comp[v] == v)
+  int* tdeg;       // [n+1] tree degree, scanned in place into toff
+  int4* ex;        // [n]   forest edge of hooked vertex x: {u, v, slot_u, slot_v}
+  int* tedges;     // [2n]  tree CSR targets
+  int* twin;       // [2n]  reverse slot
+  int* nxt;        // [2n]  unified tour list successor
+  int2* own0;      // [2n]  (segment, offset) per list element
+  // ruling-set levels 1..nlev: element counts and arrays
+  int nlev;
+  int64_t K[8];
+  int S[8];        // splitter spacing used to build level l+1 from level l
+  int* succ[8];
+  int* wgt[8];
+  int2* own[8];
+  int* offs[8];
+  int4* rec;       // [n] {first, last, parent, fence}
+  void* cub_tmp;
+  size_t cub_bytes;
+};
+
+struct Tags {
+  int2* A;         // [ntile*TILE] (w1, w2) at first[v], filler at last[v]
+  int2* P;         // [ntile*TILE] {v or ~v, partner position}
+  int2* lh1;       // [n] in-tile result / suffix partial
+  int2* lh2;       // [n] prefix partial
+  int2* table;     // [tlev * ntile] sparse table over tile extremes
+  int ntile;
+  int tlev;
+};
+
+constexpr int kTile = 4096;      // tour positions per tile in the low/high pass
+
+void stage1_forest(const Graph& g, int* comp, int2* fe, Scalars* sc, cudaStream_t st);
+void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int2* A, int2* P,
+                    Scalars* sc, cudaStream_t st);
+void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st);
+void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out,
+                  cudaStream_t st);
+void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, Scalars* sc, cudaStream_t st);
+void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
+                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
+                      size_t cub_bytes, Scalars* sc, cudaStream_t st);
+void export_debug(const Graph& g, const int2* fe, const int4* rec, const int2* A, int* forest,
+                  int* parent, int* first, int* last, int* w1, int* w2, uint8_t* fence,
+                  cudaStream_t st);
+
+size_t scan_temp_bytes(int64_t items);
+void exclusive_scan(const int* in, int* out, int64_t items, void* tmp, size_t tmp_bytes,
+                    cudaStream_t st);
+
+}  // namespace fbcc

@@ -1,0 +1,189 @@
+// labelling.cu -- Stage 6: block heads, BCC count, articulation flags and
+// canonical per-edge labels.
+//
+// Replaces _component_heads (bcc.py:129-144, sequential packed-min over all
+// vertices), num_bccs (bcc.py:192), articulation_points (bcc.py:222-235,
+// numpy bincount) and adds the per-edge labelling the reference leaves
+// implicit (rule: bcc.py:24-27; canonical numbering: tv_skeleton,
+// baselines.py:251-257, 297-303).
+//
+// B200 design:
+//  * heads without a min pass: by the BCC tree-connectivity lemma
+//     a skeleton component minus nothing is a subtree
+//    whose only member with a parent outside the component is its shallowest
+//    vertex, so `label[v] != label[parent[v]]` identifies exactly one writer
+//    per block; that thread also counts the block and bumps the (saturating)
+//    headed-count of the parent -- one pass, no contended atomics beyond
+//    the count.
+//  * edge ids: upper-degree via binary search in the sorted row + CUB scan.
+//  * per-block minimum edge id: arc-balanced pass, run-length aggregated per
+//    thread, and an L2 read before each atomicMin (ids only decrease, so a
+//    stale read can only cause a redundant atomic) -- config 2 has one block
+//    with 8.4 M edges that would otherwise serialise on one address.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fbcc {
+
+__global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restrict__ label, int* head,
+                        int* cnt, Scalars* sc) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int p = __ldg(&rec[v].z);
+    bool top = false;
+    if (p >= 0) {
+      int l = __ldg(label + v);
+      if (l != __ldg(label + p)) {
+        top = true;
+        head[l] = p;
+        if (ld_relaxed(cnt + p) < 2) atomicAdd(cnt + p, 1);
+      }
+    }
+    warp_count_add(&sc->nbccs, top);
+  }
+}
+
+__global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict__ head,
+                     const int* __restrict__ cnt, uint8_t* __restrict__ is_ap) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    bool root = (__ldg(label + v) == v) && (__ldg(head + v) == -1);
+    int c = __ldg(cnt + v);
+    is_ap[v] = root ? (c >= 2) : (c >= 1);
+  }
+}
+
+// upper degree (neighbours > v) of each row; rows are sorted (graphs.py:36-41)
+__global__ void k_upper_degree(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
+                               int* __restrict__ ud, int* __restrict__ nlow) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
+    if (v == n) { ud[n] = 0; continue; }
+    int64_t lo = __ldg(off + v), hi = __ldg(off + v + 1);
+    int64_t a = lo, b = hi;  // first slot with target > v
+    while (a < b) {
+      int64_t mid = (a + b) >> 1;
+      if ((int)__ldg(adj + mid) < v) a = mid + 1; else b = mid;
+    }
+    nlow[v] = (int)(a - lo);
+    ud[v] = (int)(hi - a);
+  }
+}
+
+struct EdgeBlockVisitor {
+  const int64_t* off;
+  const int* label;
+  const int* head;
+  const int* uoff;
+  const int* nlow;
+  int* eblk;
+  int* bmin;
+  int lu, ebase;
+  int run_blk, run_min;
+  __device__ __forceinline__ void flush() {
+    if (run_blk >= 0 && run_min < ld_relaxed(bmin + run_blk)) atomicMin(bmin + run_blk, run_min);
+    run_blk = -1;
+  }
+  __device__ __forceinline__ void begin(int v, int64_t rs, int64_t) {
+    lu = __ldg(label + v);
+    ebase = __ldg(uoff + v) - (int)(rs + __ldg(nlow + v));  // e = ebase + a for upper arcs
+  }
+  __device__ __forceinline__ void arc(int v, int64_t a, int w) {
+    if (w <= v) return;
+    int e = ebase + (int)a;
+    int lw = __ldg(label + w);
+    int blk = (lu == lw) ? lu : (__ldg(head + lw) == v ? lw : lu);
+    eblk[e] = blk;
+    if (blk != run_blk) {
+      flush();
+      run_blk = blk;
+      run_min = e;
+    }
+  }
+  __device__ __forceinline__ void end(int, bool) {}
+};
+
+__global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                     int n, int64_t m, const int* __restrict__ label,
+                                                     const int* __restrict__ head, const int* __restrict__ uoff,
+                                                     const int* __restrict__ nlow, int* eblk, int* bmin) {
+  EdgeBlockVisitor vis;
+  vis.off = off;
+  vis.label = label;
+  vis.head = head;
+  vis.uoff = uoff;
+  vis.nlow = nlow;
+  vis.eblk = eblk;
+  vis.bmin = bmin;
+  vis.run_blk = -1;
+  visit_arc_chunks(off, adj, n, m, vis);
+  vis.flush();
+}
+
+__global__ void k_edge_final(int* eblk, const int* __restrict__ bmin, const int* __restrict__ uoff, int n) {
+  const int E = uoff[n];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x)
+    eblk[e] = __ldg(bmin + eblk[e]);
+}
+
+__global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) { sc->num_edges = uoff[n]; }
+
+void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
+                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
+                      size_t cub_bytes, Scalars* sc, cudaStream_t st) {
+  const int n = g.n;
+  const int B = 256;
+  const int gv = grid_for(n + 1, B);
+  cudaMemsetAsync(head, 0xFF, sizeof(int) * n, st);
+  cudaMemsetAsync(cnt, 0, sizeof(int) * n, st);
+  note(K_MEMSET);
+  k_heads<<<gv, B, 0, st>>>(n, rec, label, head, cnt, sc);
+  note(K_HEADS);
+  if (is_ap) {
+    k_ap<<<gv, B, 0, st>>>(n, label, head, cnt, is_ap);
+    note(K_AP);
+  }
+  // edge ids: ud -> exclusive scan -> uoff (uoff[n] = E)
+  int* ud = uoff + (n + 1);
+  k_upper_degree<<<gv, B, 0, st>>>(g.off, g.adj, n, ud, nlow);
+  note(K_UPPER_DEGREE);
+  exclusive_scan(ud, uoff, n + 1, cub_tmp, cub_bytes, st);
+  note(K_SCAN);
+  k_set_edges<<<1, 1, 0, st>>>(uoff, n, sc);
+  note(K_SET_EDGES);
+  if (edge_label && g.m > 0) {
+    cudaMemsetAsync(bmin, 0x7F, sizeof(int) * n, st);
+    note(K_MEMSET);
+    int64_t nchunks = (g.m + kItems - 1) / kItems;
+    k_edge_blocks<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, n, g.m, label, head, uoff, nlow,
+                                                          edge_label, bmin);
+    note(K_EDGE_BLOCKS);
+    k_edge_final<<<grid_for(g.m / 2, B), B, 0, st>>>(edge_label, bmin, uoff, n);
+    note(K_EDGE_FINAL);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// intermediate exports (parity rungs 1-4)
+// ---------------------------------------------------------------------------
+__global__ void k_export(int n, const int4* __restrict__ rec, const int2* __restrict__ A, int* parent, int* first,
+                         int* last, int* w1, int* w2, uint8_t* fence) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int4 r = rec[v];
+    if (parent) parent[v] = r.z;
+    if (first) first[v] = r.x;
+    if (last) last[v] = r.y;
+    if (fence) fence[v] = (uint8_t)r.w;
+    if (w1 || w2) {
+      int2 a = A[r.x];
+      if (w1) w1[v] = a.x;
+      if (w2) w2[v] = a.y;
+    }
+  }
+}
+
+void export_debug(const Graph& g, const int2* fe, const int4* rec, const int2* A, int* forest, int* parent,
+                  int* first, int* last, int* w1, int* w2, uint8_t* fence, cudaStream_t st) {
+  if (forest) cudaMemcpyAsync(forest, fe, sizeof(int2) * g.n, cudaMemcpyDeviceToDevice, st);
+  if (parent || first || last || w1 || w2 || fence)
+    k_export<<<grid_for(g.n, 256), 256, 0, st>>>(g.n, rec, A, parent, first, last, w1, w2, fence);
+}
+
+}  // namespace fbcc

@@ -1,0 +1,238 @@
+// tags.cu -- Stage 3 (subtree tags low/high) and Stage 4 (fence bits).
+//
+// Replaces compute_tags (tagging.py:300-304): _w_gather 101-119 (per-vertex
+// gather over non-tree edges, 128 static vertex chunks), _scatter_at_first
+// 122-135, _block_extremes 138-159, _doubling_tables 162-184 ((K+1) x 2n/16
+// int64 words -- ~2.4 GB at n = 1e8) and _range_queries 187-242; then the
+// fence bit of _pack_skeleton (connectivity.py:84-96).
+//
+// B200 design:
+//  * w gather: arc-balanced (kItems arcs per thread, hub rows spread over
+//    many threads), one 16-byte record gather per arc, and the result goes
+//    straight into the tour-indexed array A at first[v] (fusing
+//    _scatter_at_first).  Rows wholly inside a thread's chunk are stored
+//    plainly; rows split across chunks combine with 32-bit atomicMin/Max.
+//  * low/high = min/max of A over [first[v], last[v]] -- a segmented reduction
+//    over Euler-tour order.  Each CTA stages one 4096-position tile of A in
+//    shared memory (coalesced 256-byte warp loads), builds warp-level
+//    prefix/suffix extremes per 32-position sub-block plus a 128-entry sparse
+//    table over sub-blocks, and answers every query whose interval starts or
+//    ends in the tile while the tile is resident: whole queries inside the
+//    tile directly, spanning queries as a suffix partial (at first) and a
+//    prefix partial (at last).  Only a sparse table over TILE EXTREMES stays
+//    in global memory (8 B x 2n/4096 x log2 -- 6 MB at n = 1e8, L2-resident)
+//    instead of the reference's (K+1) x 2n/16 doubling table.
+//  * Stage 4 is the epilogue: combine partials + one table probe, compare
+//    with the parent's interval, set the fence bit in the 16-byte record that
+//    Stage 5's predicate gathers.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fbcc {
+
+__device__ __forceinline__ int2 comb(int2 a, int2 b) { return make_int2(min(a.x, b.x), max(a.y, b.y)); }
+__device__ __forceinline__ int2 filler() { return make_int2(kINF, -1); }
+
+// ---------------------------------------------------------------------------
+// w1/w2 gather into A[first[v]]
+// ---------------------------------------------------------------------------
+struct WGatherVisitor {
+  const int4* rec;
+  int2* A;
+  int fv, pv, m1, m2;
+  __device__ __forceinline__ void begin(int v, int64_t, int64_t) {
+    int4 r = __ldg(rec + v);
+    fv = r.x;
+    pv = r.z;
+    m1 = kINF;
+    m2 = -1;
+  }
+  __device__ __forceinline__ void arc(int v, int64_t, int w) {
+    if (pv == w) return;  // tree edge to the parent
+    int4 r = __ldg(rec + w);
+    if (r.z == v) return;  // tree edge to a child
+    m1 = min(m1, r.x);
+    m2 = max(m2, r.x);
+  }
+  __device__ __forceinline__ void end(int, bool whole) {
+    if (whole) {
+      A[fv] = make_int2(min(fv, m1), max(fv, m2));
+    } else if (m2 >= 0) {
+      atomicMin(&A[fv].x, m1);
+      atomicMax(&A[fv].y, m2);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                  int n, int64_t m, const int4* __restrict__ rec, int2* A) {
+  WGatherVisitor vis;
+  vis.rec = rec;
+  vis.A = A;
+  visit_arc_chunks(off, adj, n, m, vis);
+}
+
+// ---------------------------------------------------------------------------
+// tile pass
+// ---------------------------------------------------------------------------
+constexpr int kTileThreads = 512;
+constexpr int kSub = 32;
+constexpr int kNSub = kTile / kSub;  // 128
+constexpr int kSubLev = 8;           // levels 0..7 over 128 sub-blocks
+constexpr size_t kTileSmem = sizeof(int2) * (3 * kTile + kSubLev * kNSub);
+
+struct TileSmem {
+  int2* raw;
+  int2* pre;
+  int2* suf;
+  int2* st;  // [kSubLev][kNSub]
+  __device__ __forceinline__ int2 st_query(int i, int j) const {  // sub-blocks i..j, i <= j
+    int k = 31 - __clz(j - i + 1);
+    return comb(st[k * kNSub + i], st[k * kNSub + j - (1 << k) + 1]);
+  }
+  __device__ __forceinline__ int2 range(int a, int b) const {  // positions a..b in tile
+    int sa = a >> 5, sb = b >> 5;
+    if (sa == sb) {
+      int2 r = raw[a];
+      for (int i = a + 1; i <= b; i++) r = comb(r, raw[i]);
+      return r;
+    }
+    int2 r = comb(suf[a], pre[b]);
+    if (sb - sa > 1) r = comb(r, st_query(sa + 1, sb - 1));
+    return r;
+  }
+  __device__ __forceinline__ int2 to_end(int p) const {
+    int sp = p >> 5;
+    int2 r = suf[p];
+    if (sp < kNSub - 1) r = comb(r, st_query(sp + 1, kNSub - 1));
+    return r;
+  }
+  __device__ __forceinline__ int2 from_start(int p) const {
+    int sp = p >> 5;
+    int2 r = pre[p];
+    if (sp > 0) r = comb(r, st_query(0, sp - 1));
+    return r;
+  }
+};
+
+__global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int2* __restrict__ A, const int2* __restrict__ P,
+                                                          int64_t N, int ntile, int2* __restrict__ lh1,
+                                                          int2* __restrict__ lh2, int2* __restrict__ table0) {
+  extern __shared__ int2 smem[];
+  TileSmem S;
+  S.raw = smem;
+  S.pre = smem + kTile;
+  S.suf = smem + 2 * kTile;
+  S.st = smem + 3 * kTile;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const int64_t base = (int64_t)tile * kTile;
+    // 1. stage the tile; warp scans per 32-position sub-block
+    for (int sb = warp; sb < kNSub; sb += kTileThreads / 32) {
+      int p = sb * kSub + lane;
+      int2 x = (base + p < N) ? __ldg(A + base + p) : filler();
+      S.raw[p] = x;
+      int2 pr = x, su = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int px = __shfl_up_sync(0xffffffffu, pr.x, o), py = __shfl_up_sync(0xffffffffu, pr.y, o);
+        int sx = __shfl_down_sync(0xffffffffu, su.x, o), sy = __shfl_down_sync(0xffffffffu, su.y, o);
+        if (lane >= o) pr = comb(pr, make_int2(px, py));
+        if (lane + o < 32) su = comb(su, make_int2(sx, sy));
+      }
+      S.pre[p] = pr;
+      S.suf[p] = su;
+      if (lane == 31) S.st[sb] = pr;
+    }
+    __syncthreads();
+    // 2. sparse table over the 128 sub-block extremes
+    for (int k = 1; k < kSubLev; k++) {
+      if (threadIdx.x < kNSub) {
+        int i = threadIdx.x, j = i + (1 << (k - 1));
+        int2 a = S.st[(k - 1) * kNSub + i];
+        S.st[k * kNSub + i] = (j < kNSub) ? comb(a, S.st[(k - 1) * kNSub + j]) : a;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) table0[tile] = S.st[(kSubLev - 1) * kNSub];
+    // 3. answer the queries that start or end here
+    for (int p = threadIdx.x; p < kTile; p += kTileThreads) {
+      int64_t gp = base + p;
+      if (gp >= N) break;
+      int2 q = __ldg(P + gp);
+      if (q.x >= 0) {  // entry position of v = q.x; partner = last[v]
+        int64_t rel = (int64_t)q.y - base;
+        lh1[q.x] = (rel < kTile) ? S.range(p, (int)rel) : S.to_end(p);
+      } else if ((int64_t)q.y < base) {  // exit position of ~q.x, entry in an earlier tile
+        lh2[~q.x] = S.from_start(p);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_table_level(int2* table, int ntile, int k) {
+  const int2* prev = table + (int64_t)(k - 1) * ntile;
+  int2* cur = table + (int64_t)k * ntile;
+  const int half = 1 << (k - 1);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ntile; i += gridDim.x * blockDim.x) {
+    int2 a = prev[i];
+    cur[i] = (i + half < ntile) ? comb(a, prev[i + half]) : a;
+  }
+}
+
+void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st) {
+  const int B = 256;
+  int64_t nchunks = (g.m + kItems - 1) / kItems;
+  if (g.m > 0) {
+    k_w_gather<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.n, g.m, R.rec, T.A);
+    note(K_W_GATHER);
+  }
+  cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+  k_tile<<<grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st>>>(T.A, T.P, 2 * (int64_t)g.n, T.ntile, T.lh1,
+                                                                  T.lh2, T.table);
+  note(K_TILE);
+  for (int k = 1; k < T.tlev; k++) {
+    k_table_level<<<grid_for(T.ntile, B), B, 0, st>>>(T.table, T.ntile, k);
+    note(K_TABLE);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 4: combine, fence bit
+// ---------------------------------------------------------------------------
+__global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const int2* __restrict__ lh2,
+                        const int2* __restrict__ table, int ntile, int* low_out, int* high_out) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int4 r = rec[v];
+    int ta = r.x / kTile, tb = r.y / kTile;
+    int2 res = lh1[v];
+    if (ta != tb) {
+      res = comb(res, lh2[v]);
+      if (tb - ta > 1) {
+        int i = ta + 1, j = tb - 1;
+        int k = 31 - __clz(j - i + 1);
+        res = comb(res, comb(table[(int64_t)k * ntile + i], table[(int64_t)k * ntile + j - (1 << k) + 1]));
+      }
+    }
+    int fence = 0;
+    if (r.z >= 0) {
+      int4 pr = rec[r.z];
+      fence = (res.x >= pr.x && res.y <= pr.y) ? 1 : 0;
+    }
+    reinterpret_cast<int*>(rec + v)[3] = fence;
+    if (low_out) {
+      low_out[v] = res.x;
+      high_out[v] = res.y;
+    }
+  }
+}
+
+void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, cudaStream_t st) {
+  const int B = 256;
+  k_fence<<<grid_for(g.n, B), B, 0, st>>>(g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out);
+  note(K_FENCE);
+}
+
+}  // namespace fbcc
