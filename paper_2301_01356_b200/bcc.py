@@ -121,7 +121,7 @@ def _device_csr(g: Graph, device):
         if adj.dtype == torch.uint32:
             adj = adj.view(torch.int32)
         return off, adj, 0
-    pinned = getattr(g, "_pinned", None)
+    pinned = g._pinned
     if pinned is not None:
         off_h, adj_h = pinned
     else:

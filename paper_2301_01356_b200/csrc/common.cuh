@@ -133,7 +133,7 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
     // warp window [vlo, vhi]
     int64_t first_a = wbase * kItems;
     int64_t last_chunk = wbase + 31 < nchunks ? wbase + 31 : nchunks - 1;
-    int64_t last_a = last_chunk * kItems;
+    int64_t last_a = (last_chunk + 1) * kItems < m ? (last_chunk + 1) * kItems - 1 : m - 1;  // warp's last arc
     int s = 0;
     if (lane == 0) s = row_of(off, 0, n - 1, first_a);
     if (lane == 1) s = row_of(off, 0, n - 1, last_a);

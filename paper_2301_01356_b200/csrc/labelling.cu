@@ -9,12 +9,11 @@
 //
 // B200 design:
 //  * heads without a min pass: by the BCC tree-connectivity lemma
-//     a skeleton component minus nothing is a subtree
-//    whose only member with a parent outside the component is its shallowest
-//    vertex, so `label[v] != label[parent[v]]` identifies exactly one writer
-//    per block; that thread also counts the block and bumps the (saturating)
-//    headed-count of the parent -- one pass, no contended atomics beyond
-//    the count.
+//     a block is tree-connected through its head, so
+//    every member v of skeleton component l with label[parent[v]] != l is a
+//    tree child of the head: `head[l] = parent[v]` is an idempotent store
+//    (no packed-min over first[] like the reference).  A second per-label
+//    pass counts blocks and bumps the heads' saturating headed-counts.
 //  * edge ids: upper-degree via binary search in the sorted row + CUB scan.
 //  * per-block minimum edge id: arc-balanced pass, run-length aggregated per
 //    thread, and an L2 read before each atomicMin (ids only decrease, so a
@@ -25,20 +24,28 @@
 
 namespace fbcc {
 
-__global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restrict__ label, int* head,
-                        int* cnt, Scalars* sc) {
+// Every member of component l whose tree parent lies outside l has that
+// parent equal to the block's head (all such members are children of the
+// head: the block is tree-connected through its head),
+// so the concurrent stores are idempotent.
+__global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restrict__ label, int* head) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int p = __ldg(&rec[v].z);
-    bool top = false;
     if (p >= 0) {
       int l = __ldg(label + v);
-      if (l != __ldg(label + p)) {
-        top = true;
-        head[l] = p;
-        if (ld_relaxed(cnt + p) < 2) atomicAdd(cnt + p, 1);
-      }
+      if (l != __ldg(label + p)) head[l] = p;
     }
-    warp_count_add(&sc->nbccs, top);
+  }
+}
+
+// one thread per label: count the block and bump its head's (saturating)
+// headed-count for the articulation rule of bcc.py:229-234
+__global__ void k_count_blocks(int n, const int* __restrict__ head, int* cnt, Scalars* sc) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
+    int h = __ldg(head + l);
+    bool blk = h >= 0;
+    if (blk && ld_relaxed(cnt + h) < 2) atomicAdd(cnt + h, 1);
+    warp_count_add(&sc->nbccs, blk);
   }
 }
 
@@ -134,7 +141,9 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   cudaMemsetAsync(head, 0xFF, sizeof(int) * n, st);
   cudaMemsetAsync(cnt, 0, sizeof(int) * n, st);
   note(K_MEMSET);
-  k_heads<<<gv, B, 0, st>>>(n, rec, label, head, cnt, sc);
+  k_heads<<<gv, B, 0, st>>>(n, rec, label, head);
+  note(K_HEADS);
+  k_count_blocks<<<gv, B, 0, st>>>(n, head, cnt, sc);
   note(K_HEADS);
   if (is_ap) {
     k_ap<<<gv, B, 0, st>>>(n, label, head, cnt, is_ap);

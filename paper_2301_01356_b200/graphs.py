@@ -21,12 +21,13 @@ class Graph:
     :param edges: uint32[m] neighbour ids
     """
 
-    __slots__ = ("offsets", "edges", "_dev")
+    __slots__ = ("offsets", "edges", "_dev", "_pinned")
 
     def __init__(self, offsets, edges, validate: bool = False):
         self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         self.edges = np.ascontiguousarray(edges, dtype=np.uint32)
         self._dev = None
+        self._pinned = None
         if self.offsets.ndim != 1 or self.offsets.size == 0:
             raise ValueError("offsets must be a 1-d array of length n+1")
         if validate:
@@ -46,6 +47,7 @@ class Graph:
         g.offsets = None
         g.edges = None
         g._dev = (offsets_t.contiguous(), edges_t.contiguous())
+        g._pinned = None
         return g
 
     @property
