@@ -95,6 +95,27 @@ int fbcc_run(const int64_t *offsets, const uint32_t *edges, int64_t n,
              fbcc_outputs *out, fbcc_debug *debug, fbcc_stats *stats,
              void *stream, uint32_t flags);
 
+/* CUDA-graph plan: the whole launch sequence for one (graph, workspace,
+   outputs) binding, captured once and replayed by fbcc_plan_run (same
+   results as fbcc_run).  The graph records the six stage boundaries as event
+   nodes (stats.stage_ms after each run); with FBCC_FLAG_PROFILE it also
+   records one event node after every kernel (stats.prof_*).  The bound
+   buffers must stay valid until fbcc_plan_destroy. */
+typedef struct fbcc_plan_s *fbcc_plan;
+int fbcc_plan_create(const int64_t *offsets, const uint32_t *edges, int64_t n,
+                     int64_t m, void *workspace, size_t workspace_bytes,
+                     const fbcc_outputs *out, uint32_t flags,
+                     fbcc_plan *plan_out);
+int fbcc_plan_run(fbcc_plan plan, fbcc_stats *stats, void *stream);
+int fbcc_plan_destroy(fbcc_plan plan);
+
+/* Process-wide tuning knobs (result-neutral, like the reference's beta /
+   block / seed, bcc.py:147-155).  Keys: 0 Afforest sampling rounds (0..8),
+   1 giant-component skip (0/1), 2 path halving (0/1), 3 level-0 splitter
+   spacing, 4 higher-level splitter spacing (powers of two >= 2). */
+int fbcc_set_option(int key, int value);
+int fbcc_get_option(int key);
+
 /* Name of a kernel kind reported in fbcc_stats.prof_kind. */
 const char *fbcc_kernel_name(int kind);
 

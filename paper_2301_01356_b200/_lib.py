@@ -24,7 +24,18 @@ FBCC_MAX_PROFILE = 512
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = ("fbcc_workspace_bytes", "fbcc_run", "fbcc_strerror", "fbcc_last_cuda_error", "fbcc_version",
-           "fbcc_kernel_name")
+           "fbcc_kernel_name", "fbcc_plan_create", "fbcc_plan_run", "fbcc_plan_destroy",
+           "fbcc_set_option", "fbcc_get_option")
+
+OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "find_halving": 2, "s0": 3, "sl": 4, "sample_full": 5, "sample_mode": 6}
+
+
+def set_option(name: str, value: int) -> None:
+    check(load().fbcc_set_option(OPTIONS[name], int(value)))
+
+
+def get_option(name: str) -> int:
+    return int(load().fbcc_get_option(OPTIONS[name]))
 
 
 class FbccOutputs(ctypes.Structure):
@@ -72,6 +83,7 @@ def load():
         L.fbcc_version.restype = ctypes.c_int
         L.fbcc_kernel_name.restype = ctypes.c_char_p
         L.fbcc_kernel_name.argtypes = [ctypes.c_int]
+        _bind_plan(L)
         _lib = L
         return L
 
@@ -96,3 +108,14 @@ def workspace_bytes(n: int, m: int) -> int:
 
 def kernel_name(kind: int) -> str:
     return load().fbcc_kernel_name(int(kind)).decode()
+
+
+def _bind_plan(L):
+    P = ctypes.c_void_p
+    L.fbcc_plan_create.restype = ctypes.c_int
+    L.fbcc_plan_create.argtypes = [P, P, ctypes.c_int64, ctypes.c_int64, P, ctypes.c_size_t,
+                                   ctypes.POINTER(FbccOutputs), ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p)]
+    L.fbcc_plan_run.restype = ctypes.c_int
+    L.fbcc_plan_run.argtypes = [P, ctypes.POINTER(FbccStats), P]
+    L.fbcc_plan_destroy.restype = ctypes.c_int
+    L.fbcc_plan_destroy.argtypes = [P]

@@ -178,6 +178,111 @@ def run_device(off, adj, *, edge_labels=True, articulation=True, timing=True, de
     return res, stats
 
 
+class Plan:
+    """A CUDA-graph replay of the six stages bound to device tensors
+    (``fbcc_plan_*`` in the C ABI).  ``run()`` launches the graph, waits and
+    returns the counts; outputs land in ``self.label`` etc."""
+
+    def __init__(self, off, adj, *, edge_labels=True, articulation=True, profile=False):
+        import torch
+
+        self.L = _lib.load()
+        n = off.numel() - 1
+        m = adj.numel()
+        dev = off.device
+        self.n, self.m, self.off, self.adj = n, m, off, adj
+        self.ws = torch.empty(max(_lib.workspace_bytes(n, m), 256), dtype=torch.uint8, device=dev)
+        self.label = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.head = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.comp = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.is_ap = torch.empty(max(n, 1), dtype=torch.uint8, device=dev) if articulation else None
+        self.edge_label = torch.empty(max(m // 2, 1), dtype=torch.int32, device=dev) if edge_labels else None
+        outs = _lib.FbccOutputs(self.label.data_ptr(), self.head.data_ptr(),
+                                self.edge_label.data_ptr() if edge_labels else None,
+                                self.is_ap.data_ptr() if articulation else None, self.comp.data_ptr())
+        h = ctypes.c_void_p()
+        _lib.check(self.L.fbcc_plan_create(off.data_ptr(), adj.data_ptr() if m else None, n, m,
+                                           self.ws.data_ptr(), self.ws.numel(), ctypes.byref(outs),
+                                           _lib.FBCC_FLAG_PROFILE if profile else 0, ctypes.byref(h)))
+        self._h = h
+        self.stats = _lib.FbccStats()
+
+    def run(self, stream=None):
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.off.device)
+        _lib.check(self.L.fbcc_plan_run(self._h, ctypes.byref(self.stats), ctypes.c_void_p(s.cuda_stream)))
+        return self.stats
+
+    def outputs(self):
+        E = int(self.stats.num_edges)
+        n = self.n
+        return {"label": self.label[:n], "head": self.head[:n], "comp": self.comp[:n],
+                "is_ap": self.is_ap[:n] if self.is_ap is not None else None,
+                "edge_label": self.edge_label[:E] if self.edge_label is not None else None}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self.L.fbcc_plan_destroy(h)
+            self._h = None
+
+
+_SESSIONS = {}
+
+
+def _session(g: Graph, dev) -> Plan:
+    """A graph-replay plan bound to device buffers for this input.
+
+    Device-resident inputs bind their own tensors (keyed by pointer); host
+    inputs are copied (from pinned memory when ``g._pinned`` is set) into
+    persistent device buffers of the right size, reused across calls."""
+    import torch
+
+    if g._dev is not None:
+        off, adj, _ = _device_csr(g, dev)
+        key = ("dev", off.data_ptr(), adj.data_ptr(), g.n, g.m)
+        plan = _SESSIONS.get(key)
+        if plan is None:
+            _SESSIONS.clear()
+            plan = _SESSIONS[key] = Plan(off, adj)
+        return plan
+    key = ("host", str(dev), g.n, g.m)
+    plan = _SESSIONS.get(key)
+    if plan is None:
+        _SESSIONS.clear()
+        off = torch.empty(g.n + 1, dtype=torch.int64, device=dev)
+        adj = torch.empty(max(g.m, 1), dtype=torch.int32, device=dev)[: g.m]
+        plan = _SESSIONS[key] = Plan(off, adj)
+    if g._pinned is not None:
+        off_h, adj_h = g._pinned
+    else:
+        off_h = torch.from_numpy(g.offsets)
+        adj_h = torch.from_numpy(g.edges.view(np.int32))
+    plan.off.copy_(off_h, non_blocking=True)
+    if g.m:
+        plan.adj.copy_(adj_h, non_blocking=True)
+    return plan
+
+
+def _to_host(res, keys):
+    """D2H into pinned buffers (full link speed), returned as numpy views that
+    own their buffer (freed back to torch's pinned cache when dropped)."""
+    import torch
+
+    host = {}
+    for k in keys:
+        t = res[k]
+        if t is None:
+            host[k] = None
+            continue
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        host[k] = h
+    torch.cuda.current_stream(next(v for v in res.values() if v is not None).device).synchronize()
+    return {k: (None if v is None else v.numpy()) for k, v in host.items()}
+
+
 def fast_bcc(g: Graph, *, beta: float | None = None, seed: int = 0, block: int = 16,
              device=None, device_outputs: bool = False, validate: bool = False) -> BccLabeling:
     """Biconnected components of ``g`` (bcc.py:147-196) on a CUDA device.
@@ -206,16 +311,20 @@ def fast_bcc(g: Graph, *, beta: float | None = None, seed: int = 0, block: int =
         raise RuntimeError("fast_bcc needs a CUDA device (no CPU fallback)")
     dev = torch.device(device) if device is not None else (
         g._dev[0].device if g._dev is not None else torch.device("cuda", torch.cuda.current_device()))
-    off, adj, _ = _device_csr(g, dev)
-    res, stats = run_device(off, adj)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    plan = _session(g, dev)
+    stats = plan.run()
+    res = plan.outputs()
     ms = [float(x) for x in stats.stage_ms]
     tim = StepTimings(first_cc=ms[0] / 1e3, rooting=ms[1] / 1e3, tagging=ms[2] / 1e3,
                       last_cc=(ms[3] + ms[4]) / 1e3, labelling=ms[5] / 1e3,
                       total=float(stats.total_ms) / 1e3, stage_ms=tuple(ms))
-    if device_outputs:
+    if device_outputs:  # plan buffers are reused by the next call: hand out copies
+        res = {k: (None if v is None else v.clone()) for k, v in res.items()}
         return BccLabeling(res["label"], res["head"], int(stats.num_bccs), int(stats.num_components), tim,
                            res["edge_label"], res["is_ap"])
-    out = {k: res[k].cpu().numpy() for k in ("label", "head", "edge_label", "is_ap")}
+    out = _to_host(res, ("label", "head", "edge_label", "is_ap"))
     return BccLabeling(out["label"], out["head"], int(stats.num_bccs), int(stats.num_components), tim,
                        out["edge_label"], out["is_ap"].astype(bool))
 

@@ -1,5 +1,6 @@
-// api.cu -- the C ABI (include/fastbcc_b200.h): workspace layout and the
-// six-stage orchestration of fast_bcc (bcc.py:147-196) on one stream.
+// api.cu -- the C ABI (include/fastbcc_b200.h): workspace layout, the
+// six-stage orchestration of fast_bcc (bcc.py:147-196) on one stream, and
+// CUDA-graph plans that replay the whole launch sequence.
 #include <cstdio>
 #include <cstring>
 
@@ -16,20 +17,20 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "iota", "sample_link", "compress", "find_giant", "link_rest", "root_flags", "scan", "tree_degree",
     "tree_scatter", "link_slots", "link_roots", "walk0", "walk_level", "final_rank", "expand", "positions",
     "w_gather", "tile", "table", "fence", "heads", "ap", "upper_degree", "set_edges", "edge_blocks",
-    "edge_final", "memset", "export"};
+    "edge_final", "memset", "export", "accept"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
   return FBCC_ERR_CUDA;
 }
 
-constexpr int kS0 = 16;   // level-0 splitter spacing (mean segment length)
-constexpr int kSl = 32;   // spacing on the weighted splitter levels
+int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*halving*/ 1, /*S0*/ 16, /*SL*/ 32,
+                      /*full-link rounds mask*/ 0, /*sample mode: propose/accept*/ 0};
 constexpr int kFinalMaxHost = 4096;
 
 struct Layout {
   size_t total = 0;
-  size_t sc, comp, fe, rootidx, tdeg, ex, tedges, twin, nxt, own0, rec, A, P, lh1, lh2, table, cnt, uoff,
+  size_t sc, comp, fe, prop, rootidx, tdeg, ex, tedges, twin, nxt, own0, rec, A, P, lh1, lh2, table, cnt, uoff,
       nlow, bmin, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
@@ -46,6 +47,7 @@ struct Layout {
 
   explicit Layout(int64_t n) {
     const int64_t N0 = 2 * n;
+    const int kS0 = g_opt[OPT_S0], kSl = g_opt[OPT_SL];
     S[0] = kS0;
     K[1] = (N0 + kS0 - 1) / kS0;
     nlev = 1;
@@ -63,6 +65,7 @@ struct Layout {
     sc = take(sizeof(Scalars));
     comp = take(4 * n);
     fe = take(8 * n);
+    prop = take(8 * n);
     rootidx = take(4 * 2 * (n + 1));
     tdeg = take(4 * 2 * (n + 1));
     ex = take(16 * n);
@@ -90,19 +93,127 @@ struct Layout {
   }
 };
 
+// One bound instance of the pipeline: graph, workspace carve-up, outputs.
+struct Pipeline {
+  Graph g;
+  Layout lay;
+  Scalars* sc;
+  int* comp;
+  int2* fe;
+  unsigned long long* prop;
+  Rooting R;
+  Tags T;
+  fbcc_outputs out;
+  int* cnt;
+  int* uoff;
+  int* nlow;
+  int* bmin;
+
+  Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
+           const fbcc_outputs* o)
+      : lay(n) {
+    g = Graph{offsets, edges, (int)n, m};
+    out = *o;
+    char* ws = (char*)workspace;
+    auto at = [&](size_t off) { return (void*)(ws + off); };
+    sc = (Scalars*)at(lay.sc);
+    comp = out.comp ? out.comp : (int*)at(lay.comp);
+    fe = (int2*)at(lay.fe);
+    prop = (unsigned long long*)at(lay.prop);
+    R.rootidx = (int*)at(lay.rootidx);
+    R.tdeg = (int*)at(lay.tdeg);
+    R.ex = (int4*)at(lay.ex);
+    R.tedges = (int*)at(lay.tedges);
+    R.twin = (int*)at(lay.twin);
+    R.nxt = (int*)at(lay.nxt);
+    R.own0 = (int2*)at(lay.own0);
+    R.nlev = lay.nlev;
+    for (int l = 0; l < 8; l++) {
+      R.K[l] = lay.K[l];
+      R.S[l] = lay.S[l];
+      R.succ[l] = nullptr;
+      R.wgt[l] = nullptr;
+      R.own[l] = nullptr;
+      R.offs[l] = nullptr;
+    }
+    for (int l = 1; l <= lay.nlev; l++) {
+      R.succ[l] = (int*)at(lay.lsucc[l]);
+      R.wgt[l] = (int*)at(lay.lwgt[l]);
+      R.own[l] = (int2*)at(lay.lown[l]);
+      R.offs[l] = (int*)at(lay.loffs[l]);
+    }
+    R.rec = (int4*)at(lay.rec);
+    R.cub_tmp = at(lay.cub);
+    R.cub_bytes = lay.cub_bytes;
+    T.A = (int2*)at(lay.A);
+    T.P = (int2*)at(lay.P);
+    T.lh1 = (int2*)at(lay.lh1);
+    T.lh2 = (int2*)at(lay.lh2);
+    T.table = (int2*)at(lay.table);
+    T.ntile = lay.ntile;
+    T.tlev = lay.tlev;
+    cnt = (int*)at(lay.cnt);
+    uoff = (int*)at(lay.uoff);
+    nlow = (int*)at(lay.nlow);
+    bmin = (int*)at(lay.bmin);
+  }
+
+  // Enqueue all six stages.  ev (7 events) brackets the stages when given.
+  void enqueue(cudaStream_t st, cudaEvent_t* ev, int* low_out, int* high_out, bool capturing = false) {
+    auto mark = [&](int i) {
+      if (!ev) return;
+      // inside a graph capture the record must become an event-record node
+      if (capturing) cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal);
+      else cudaEventRecord(ev[i], st);
+    };
+    cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
+    note(K_MEMSET);
+    mark(0);
+    stage1_forest(g, comp, fe, prop, sc, st);
+    mark(1);
+    stage2_rooting(g, comp, fe, R, T.A, T.P, sc, st);
+    mark(2);
+    stage3_tags(g, R, T, st);
+    mark(3);
+    stage4_fence(g, R, T, low_out, high_out, st);
+    mark(4);
+    stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st);
+    mark(5);
+    stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, R.cub_tmp,
+                     R.cub_bytes, sc, st);
+    mark(6);
+  }
+};
+
 }  // namespace fbcc
 
 using namespace fbcc;
 
+struct fbcc_plan_s {
+  Pipeline* pipe = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  Scalars* host = nullptr;  // pinned
+  LaunchLog* log = nullptr;  // launch count (+ event nodes when profiled)
+  cudaEvent_t ev[7] = {};    // stage boundaries, recorded by the graph itself
+};
+
 extern "C" {
 
-int fbcc_version(void) { return 100; }
+int fbcc_version(void) { return 101; }
 
-const char* fbcc_kernel_name(int kind) {
-  return (kind >= 0 && kind < K_NUM_KINDS) ? kKernelNames[kind] : "?";
+int fbcc_set_option(int key, int value) {
+  if (key < 0 || key >= OPT_NUM) return FBCC_ERR_ARG;
+  if ((key == OPT_S0 || key == OPT_SL) && (value < 2 || (value & (value - 1)))) return FBCC_ERR_ARG;
+  if (key == OPT_SAMPLE_ROUNDS && (value < 0 || value > 8)) return FBCC_ERR_ARG;
+  g_opt[key] = value;
+  return FBCC_OK;
 }
 
+int fbcc_get_option(int key) { return (key >= 0 && key < OPT_NUM) ? g_opt[key] : -1; }
+
 const char* fbcc_last_cuda_error(void) { return g_cuda_err; }
+
+const char* fbcc_kernel_name(int kind) { return (kind >= 0 && kind < K_NUM_KINDS) ? kKernelNames[kind] : "?"; }
 
 const char* fbcc_strerror(int code) {
   switch (code) {
@@ -125,6 +236,18 @@ static int check_sizes(int64_t n, int64_t m) {
   return FBCC_OK;
 }
 
+static int check_args(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
+                      size_t workspace_bytes, const fbcc_outputs* out) {
+  int rc = check_sizes(n, m);
+  if (rc) return rc;
+  if (!out || !offsets || (m > 0 && !edges)) return FBCC_ERR_ARG;
+  if (n == 0) return FBCC_OK;
+  if (!out->label || !out->head || !workspace) return FBCC_ERR_ARG;
+  Layout lay(n);
+  if (workspace_bytes < lay.total) return FBCC_ERR_WORKSPACE;
+  return FBCC_OK;
+}
+
 int fbcc_workspace_bytes(int64_t n, int64_t m, size_t* bytes_out) {
   if (!bytes_out) return FBCC_ERR_ARG;
   int rc = check_sizes(n, m);
@@ -134,125 +257,136 @@ int fbcc_workspace_bytes(int64_t n, int64_t m, size_t* bytes_out) {
   return FBCC_OK;
 }
 
+static void fill_counts(fbcc_stats* stats, const Scalars& host) {
+  stats->num_bccs = host.nbccs;
+  stats->num_components = host.ncomp;
+  stats->num_edges = host.num_edges;
+}
+
+static void fill_profile(fbcc_stats* stats, const LaunchLog& log) {
+  if (!log.profile) return;
+  stats->nprof = log.nrec;
+  for (int i = 0; i < log.nrec; i++) {
+    stats->prof_kind[i] = log.kind[i];
+    cudaEventElapsedTime(&stats->prof_ms[i], log.ev[i], log.ev[i + 1]);
+  }
+}
+
 int fbcc_run(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
              size_t workspace_bytes, fbcc_outputs* out, fbcc_debug* dbg, fbcc_stats* stats, void* stream,
              uint32_t flags) {
-  int rc = check_sizes(n, m);
+  int rc = check_args(offsets, edges, n, m, workspace, workspace_bytes, out);
   if (rc) return rc;
-  if (!out || !offsets || (m > 0 && !edges)) return FBCC_ERR_ARG;
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n == 0) return FBCC_OK;
-  if (!out->label || !out->head || !workspace) return FBCC_ERR_ARG;
-  Layout lay(n);
-  if (workspace_bytes < lay.total) return FBCC_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  char* ws = (char*)workspace;
-  auto at = [&](size_t o) { return (void*)(ws + o); };
-
-  Graph g{offsets, edges, (int)n, m};
-  Scalars* sc = (Scalars*)at(lay.sc);
-  int* comp = out->comp ? out->comp : (int*)at(lay.comp);
-  int2* fe = (int2*)at(lay.fe);
-  Rooting R;
-  R.rootidx = (int*)at(lay.rootidx);
-  R.tdeg = (int*)at(lay.tdeg);
-  R.ex = (int4*)at(lay.ex);
-  R.tedges = (int*)at(lay.tedges);
-  R.twin = (int*)at(lay.twin);
-  R.nxt = (int*)at(lay.nxt);
-  R.own0 = (int2*)at(lay.own0);
-  R.nlev = lay.nlev;
-  for (int l = 0; l < 8; l++) {
-    R.K[l] = lay.K[l];
-    R.S[l] = lay.S[l];
-    R.succ[l] = nullptr; R.wgt[l] = nullptr; R.own[l] = nullptr; R.offs[l] = nullptr;
-  }
-  for (int l = 1; l <= lay.nlev; l++) {
-    R.succ[l] = (int*)at(lay.lsucc[l]);
-    R.wgt[l] = (int*)at(lay.lwgt[l]);
-    R.own[l] = (int2*)at(lay.lown[l]);
-    R.offs[l] = (int*)at(lay.loffs[l]);
-  }
-  R.rec = (int4*)at(lay.rec);
-  R.cub_tmp = at(lay.cub);
-  R.cub_bytes = lay.cub_bytes;
-  Tags T;
-  T.A = (int2*)at(lay.A);
-  T.P = (int2*)at(lay.P);
-  T.lh1 = (int2*)at(lay.lh1);
-  T.lh2 = (int2*)at(lay.lh2);
-  T.table = (int2*)at(lay.table);
-  T.ntile = lay.ntile;
-  T.tlev = lay.tlev;
+  Pipeline P(offsets, edges, n, m, workspace, out);
 
   const bool timing = (flags & FBCC_FLAG_TIMING) && stats;
   cudaEvent_t ev[7];
   if (timing)
     for (int i = 0; i < 7; i++) cudaEventCreate(&ev[i]);
-  auto mark = [&](int i) {
-    if (timing) cudaEventRecord(ev[i], st);
-  };
-
   LaunchLog* log = new LaunchLog();
   log->st = st;
   log->profile = (flags & FBCC_FLAG_PROFILE) && stats;
-  if (log->profile) {
-    cudaEventCreate(&log->ev[0]);
-    cudaEventRecord(log->ev[0], st);
-  }
+  log->start();
   g_log = log;
-  cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
-  note(K_MEMSET);
-  mark(0);
-  stage1_forest(g, comp, fe, sc, st);
-  mark(1);
-  stage2_rooting(g, comp, fe, R, T.A, T.P, sc, st);
-  mark(2);
-  stage3_tags(g, R, T, st);
-  mark(3);
-  stage4_fence(g, R, T, dbg ? dbg->low : nullptr, dbg ? dbg->high : nullptr, st);
-  mark(4);
-  stage5_skeleton_cc(g, R.rec, out->label, sc, st);
-  mark(5);
-  stage6_labelling(g, R.rec, out->label, out->head, out->is_ap, out->edge_label, (int*)at(lay.cnt),
-                   (int*)at(lay.uoff), (int*)at(lay.nlow), (int*)at(lay.bmin), R.cub_tmp, R.cub_bytes, sc, st);
-  mark(6);
+  P.enqueue(st, timing ? ev : nullptr, dbg ? dbg->low : nullptr, dbg ? dbg->high : nullptr);
   g_log = nullptr;
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    delete log;
-    return cuda_fail(e, "launch");
-  }
-  if (dbg)
-    export_debug(g, fe, R.rec, T.A, dbg->forest, dbg->parent, dbg->first, dbg->last, dbg->w1, dbg->w2, dbg->fence,
-                 st);
+  if (e == cudaSuccess && dbg)
+    export_debug(P.g, P.fe, P.R.rec, P.T.A, dbg->forest, dbg->parent, dbg->first, dbg->last, dbg->w1, dbg->w2,
+                 dbg->fence, st);
   Scalars host;
-  e = cudaMemcpyAsync(&host, sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&host, P.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) {
-    delete log;
-    return cuda_fail(e, "run");
-  }
-  if (stats) {
+  if (e == cudaSuccess && stats) {
+    fill_counts(stats, host);
     stats->launches = log->count;
-    if (log->profile) {
-      stats->nprof = log->nrec;
-      for (int i = 0; i < log->nrec; i++) {
-        stats->prof_kind[i] = log->kind[i];
-        cudaEventElapsedTime(&stats->prof_ms[i], log->ev[i], log->ev[i + 1]);
-      }
-      for (int i = 0; i <= log->nrec; i++) cudaEventDestroy(log->ev[i]);
-    }
-    stats->num_bccs = host.nbccs;
-    stats->num_components = host.ncomp;
-    stats->num_edges = host.num_edges;
+    fill_profile(stats, *log);
     if (timing) {
       for (int i = 0; i < 6; i++) cudaEventElapsedTime(&stats->stage_ms[i], ev[i], ev[i + 1]);
       cudaEventElapsedTime(&stats->total_ms, ev[0], ev[6]);
-      for (int i = 0; i < 7; i++) cudaEventDestroy(ev[i]);
     }
   }
+  log->destroy();
+  if (timing)
+    for (int i = 0; i < 7; i++) cudaEventDestroy(ev[i]);
   delete log;
+  if (e != cudaSuccess) return cuda_fail(e, "run");
+  return FBCC_OK;
+}
+
+int fbcc_plan_create(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
+                     size_t workspace_bytes, const fbcc_outputs* out, uint32_t flags, fbcc_plan* plan_out) {
+  if (!plan_out) return FBCC_ERR_ARG;
+  *plan_out = nullptr;
+  int rc = check_args(offsets, edges, n, m, workspace, workspace_bytes, out);
+  if (rc) return rc;
+  fbcc_plan p = new fbcc_plan_s();
+  if (n > 0) {
+    p->pipe = new Pipeline(offsets, edges, n, m, workspace, out);
+    cudaStream_t cap;
+    cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+    cudaGraph_t graph = nullptr;
+    p->log = new LaunchLog();
+    p->log->st = cap;
+    p->log->capturing = true;
+    p->log->profile = (flags & FBCC_FLAG_PROFILE) != 0;
+    for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreate(&p->ev[i]);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      g_log = p->log;
+      p->log->start();
+      p->pipe->enqueue(cap, p->ev, nullptr, nullptr, true);
+      g_log = nullptr;
+      e = cudaStreamEndCapture(cap, &graph);
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&p->exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+    if (e == cudaSuccess) e = cudaMallocHost((void**)&p->host, sizeof(Scalars));
+    if (e != cudaSuccess) {
+      fbcc_plan_destroy(p);
+      return cuda_fail(e, "plan_create");
+    }
+  }
+  *plan_out = p;
+  return FBCC_OK;
+}
+
+int fbcc_plan_run(fbcc_plan plan, fbcc_stats* stats, void* stream) {
+  if (!plan) return FBCC_ERR_ARG;
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (!plan->pipe) return FBCC_OK;  // n == 0
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaGraphLaunch(plan->exec, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(plan->host, plan->pipe->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "plan_run");
+  if (stats) {
+    fill_counts(stats, *plan->host);
+    stats->launches = plan->log->count;
+    fill_profile(stats, *plan->log);
+    for (int i = 0; i < 6; i++) cudaEventElapsedTime(&stats->stage_ms[i], plan->ev[i], plan->ev[i + 1]);
+    cudaEventElapsedTime(&stats->total_ms, plan->ev[0], plan->ev[6]);
+  }
+  return FBCC_OK;
+}
+
+int fbcc_plan_destroy(fbcc_plan plan) {
+  if (!plan) return FBCC_OK;
+  if (plan->exec) cudaGraphExecDestroy(plan->exec);
+  if (plan->host) cudaFreeHost(plan->host);
+  for (int i = 0; i < 7; i++)
+    if (plan->ev[i]) cudaEventDestroy(plan->ev[i]);
+  if (plan->log) {
+    plan->log->destroy();
+    delete plan->log;
+  }
+  delete plan->pipe;
+  delete plan;
   return FBCC_OK;
 }
 

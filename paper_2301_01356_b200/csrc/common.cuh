@@ -18,7 +18,8 @@ struct Scalars {
   int nbccs;       // number of blocks
   int err;         // error bits
   int num_edges;   // E
-  int pad[59];
+  int nroots[16];  // roots after each sampling round's compress (stage 1: 0..7, stage 5: 8..15)
+  int pad[43];
 };
 
 // ---------------------------------------------------------------------------
@@ -29,28 +30,55 @@ enum KernelKind : int {
   K_IOTA = 0, K_SAMPLE_LINK, K_COMPRESS, K_FIND_GIANT, K_LINK_REST, K_ROOT_FLAGS, K_SCAN, K_TREE_DEGREE,
   K_TREE_SCATTER, K_LINK_SLOTS, K_LINK_ROOTS, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_POSITIONS,
   K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_AP, K_UPPER_DEGREE, K_SET_EDGES, K_EDGE_BLOCKS,
-  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_NUM_KINDS
+  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_ACCEPT, K_NUM_KINDS
 };
 
 struct LaunchLog {
   static constexpr int kMax = 512;
   bool profile = false;
-  int count = 0;        // our kernels (memsets excluded)
+  bool capturing = false;  // inside a CUDA-graph capture: records become event nodes
+  int count = 0;           // our kernels (memsets excluded)
   int nrec = 0;
   int kind[kMax];
   cudaEvent_t ev[kMax + 1];
   cudaStream_t st = nullptr;
+
+  void record(int i) {
+    cudaEventCreate(&ev[i]);
+    if (capturing) cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal);
+    else cudaEventRecord(ev[i], st);
+  }
+  void start() {
+    if (profile) record(0);
+  }
+  void destroy() {
+    if (profile)
+      for (int i = 0; i <= nrec; i++) cudaEventDestroy(ev[i]);
+    nrec = 0;
+  }
 };
 
 extern thread_local LaunchLog* g_log;
+
+// process-wide tunables (fbcc_set_option); defaults are the tuned values
+enum Option : int {
+  OPT_SAMPLE_ROUNDS = 0,  // Afforest neighbour-sampling rounds
+  OPT_GIANT_SKIP = 1,     // skip rows already in the sampled giant component
+  OPT_FIND_HALVING = 2,   // path halving during finds
+  OPT_S0 = 3,             // level-0 splitter spacing (power of two)
+  OPT_SL = 4,             // spacing on higher ranking levels (power of two)
+  OPT_SAMPLE_FULL = 5,    // CAS mode: bitmask of sampling rounds that climb (exact Afforest link)
+  OPT_SAMPLE_MODE = 6,    // 0: propose/accept rounds, 1: CAS rounds
+  OPT_NUM = 16
+};
+extern int g_opt[OPT_NUM];
 
 inline void note(KernelKind k) {
   LaunchLog* L = g_log;
   if (!L) return;
   if (k != K_MEMSET) L->count += (k == K_SCAN) ? 2 : 1;  // a CUB scan is init + scan kernels
   if (L->profile && L->nrec < LaunchLog::kMax) {
-    cudaEventCreate(&L->ev[L->nrec + 1]);
-    cudaEventRecord(L->ev[L->nrec + 1], L->st);
+    L->record(L->nrec + 1);
     L->kind[L->nrec++] = k;
   }
 }

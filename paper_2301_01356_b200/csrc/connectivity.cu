@@ -37,28 +37,49 @@ __device__ __forceinline__ bool skel_keep(int u, const int4& ru, int w, const in
   return true;                                      // cross edge
 }
 
-// Afforest link with forest recording.  p1/p2 are always ancestors of the
-// two endpoints; a successful CAS hooks root `hi` under `lo`, which lies in
-// the other endpoint's set (roots are set minima, lo < hi), so (u, w) is a
-// spanning-forest edge joining two distinct sets.
+// Root of x with path halving.  Only non-roots are rewritten, always to an
+// ancestor (ancestors stay ancestors: sets only merge), and roots change only
+// through the hooking CAS -- so the concurrent plain stores are benign.
+//
+// Parent reads are L1-cacheable (ld.global.ca).  Every value comp[x] ever
+// held is an ancestor of x, so a stale line can only (a) make two endpoints
+// look joined when they truly are, or (b) offer a "root" that is no longer
+// one -- the CAS then fails and returns the fresh parent, so every retry
+// climbs.  What the L1 buys: once most vertices share one giant root, every
+// find ends at the same word; served from L2 (ld.relaxed.gpu) those ~1M
+// requests serialise on a single L2 slice.
+__device__ __forceinline__ int ldp(const int* p) { return __ldca(p); }
+
+__device__ __forceinline__ int find_halve(int* comp, int x, bool halve) {
+  int p = ldp(comp + x);
+  while (p != x) {
+    int gp = ldp(comp + p);
+    if (gp == p) return p;
+    if (halve) comp[x] = gp;
+    x = gp;
+    p = ldp(comp + x);
+  }
+  return x;
+}
+
+// Hook the larger root under the smaller.  ru/rw are roots of the sets
+// holding u and w when found; a successful CAS hooks root `hi` under `lo`,
+// whose set holds the other endpoint (roots are set minima, root(lo) <= lo <
+// hi), so (u, w) is a spanning-forest edge joining two distinct sets.
 template <bool kRecord>
-__device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
-  int p1 = ld_relaxed(comp + u);
-  int p2 = ld_relaxed(comp + w);
-  while (p1 != p2) {
-    int hi = p1 > p2 ? p1 : p2;
-    int lo = p1 + p2 - hi;
-    int phi = ld_relaxed(comp + hi);
-    if (phi == lo) break;  // already hooked together
-    if (phi == hi) {
-      int prev = atomicCAS(comp + hi, hi, lo);
-      if (prev == hi) {
-        if (kRecord) fe[hi] = make_int2(u, w);
-        break;
-      }
+__device__ __forceinline__ void link(int u, int w, int* comp, int2* fe, bool halve) {
+  int ru = find_halve(comp, u, halve);
+  int rw = find_halve(comp, w, halve);
+  while (ru != rw) {
+    int hi = ru > rw ? ru : rw;
+    int lo = ru + rw - hi;
+    int prev = atomicCAS(comp + hi, hi, lo);
+    if (prev == hi) {
+      if (kRecord) fe[hi] = make_int2(u, w);
+      return;
     }
-    p1 = ld_relaxed(comp + ld_relaxed(comp + hi));
-    p2 = ld_relaxed(comp + lo);
+    ru = find_halve(comp, prev, halve);  // hi was hooked meanwhile: climb on
+    rw = find_halve(comp, lo, halve);
   }
 }
 
@@ -66,9 +87,18 @@ __global__ void k_iota(int* __restrict__ comp, int n) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) comp[v] = v;
 }
 
+// Best-effort sampling round: one CAS attempt on the (post-compress, hence
+// depth-1) parents of v and of its round-th neighbour, no climbing.  A win is
+// still a valid forest edge (hi was a root; lo is an ancestor of the other
+// endpoint, root(lo) <= lo < hi); a loss is simply left to k_link_rest, which
+// re-covers every arc of every row outside the giant component.  Climbing
+// here is what made round 1 contention-bound: after round 0 the ~n/17
+// local-minimum roots all merge into one giant and every failed CAS then
+// chases the same few hot roots.
 template <bool kSkel, bool kRecord>
 __global__ void k_sample_link(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
-                              int round, int* comp, int2* fe, const int4* __restrict__ rec) {
+                              int round, int* comp, int2* fe, const int4* __restrict__ rec, bool full,
+                              bool halve) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t s = __ldg(off + v) + round;
     if (s >= __ldg(off + v + 1)) continue;
@@ -76,14 +106,92 @@ __global__ void k_sample_link(const int64_t* __restrict__ off, const uint32_t* _
     if (kSkel) {
       if (!skel_keep(v, __ldg(rec + v), w, __ldg(rec + w))) continue;
     }
-    link<kRecord>(v, w, comp, fe);
+    if (full) {  // exact Afforest sampling: climb until joined
+      link<kRecord>(v, w, comp, fe, halve);
+      continue;
+    }
+    int ru = ldp(comp + v), rw = ldp(comp + w);
+    if (ru == rw) continue;
+    int hi = ru > rw ? ru : rw;
+    int lo = ru + rw - hi;
+    // one CAS per distinct target root per warp (later rounds have few roots)
+    unsigned peers = __match_any_sync(__activemask(), hi);
+    if ((threadIdx.x & 31) != __ffs(peers) - 1) continue;
+    if (atomicCAS(comp + hi, hi, lo) == hi && kRecord) fe[hi] = make_int2(v, w);
+  }
+}
+
+// Propose/accept sampling round (the default).  Against the round-start
+// components (comp is flat after the previous compress and is not written
+// during the propose kernel), every vertex proposes its round-th arc to the
+// HIGHER of the two component roots with one fire-and-forget 64-bit
+// atomicMin of (lower root << 32 | arc slot).  Same-address REDs pipeline in
+// the L2 atomic unit instead of serialising retry loops, so the many-to-few
+// merges of later rounds are cheap.  k_accept then hooks every proposed-to
+// root under its minimum proposal: hooks always point to a smaller
+// round-start root, so they form a forest over the components (no cycles),
+// and each accepted hook records its arc -- one forest edge per merge.
+//
+// Proposers are thinned to ~kPerRoot per surviving root: on config 2 the
+// rounds go 1M -> 65k -> 565 -> 1 components, and round 2 would otherwise
+// aim 941k proposals at 565 roots (up to 18k REDs on one word).  A root that
+// draws no proposer simply stays for the next round / k_link_rest.
+constexpr int kPerRoot = 32;
+
+template <bool kSkel>
+__global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round,
+                          const int* __restrict__ comp, unsigned long long* prop, const int4* __restrict__ rec,
+                          const int* __restrict__ nroots_prev) {
+  // participate iff hash < thr / 2^24, thr = min(1, kPerRoot * roots / n)
+  uint32_t thr = 1u << 24;
+  if (nroots_prev) {
+    uint64_t t = ((uint64_t)kPerRoot * (uint64_t)(*nroots_prev) << 24) / (uint64_t)n;
+    if (t < thr) thr = (uint32_t)t;
+  }
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (thr < (1u << 24) && (hash32((uint32_t)v * 0x9E3779B1u + (uint32_t)round) >> 8) >= thr) continue;
+    int ru = __ldg(comp + v);
+    int64_t s = __ldg(off + v) + round;
+    if (s >= __ldg(off + v + 1)) continue;
+    int w = (int)__ldg(adj + s);
+    if (kSkel) {
+      if (!skel_keep(v, __ldg(rec + v), w, __ldg(rec + w))) continue;
+    }
+    int rw = __ldg(comp + w);
+    if (ru == rw) continue;
+    int hi = ru > rw ? ru : rw;
+    int lo = ru + rw - hi;
+    // any proposal is a valid hook, so lanes aiming at the same root send one
+    // (small components below the giant's root all aim at it in round 2)
+    unsigned peers = __match_any_sync(__activemask(), hi);
+    if ((threadIdx.x & 31) != __ffs(peers) - 1) continue;
+    atomicMin(prop + hi, ((unsigned long long)(unsigned)lo << 32) | (unsigned long long)(uint32_t)s);
+  }
+}
+
+template <bool kRecord>
+__global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int* comp,
+                         unsigned long long* prop, int2* fe) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    unsigned long long key = prop[v];
+    if (key == ~0ull) continue;
+    prop[v] = ~0ull;  // ready for the next round
+    int lo = (int)(key >> 32);
+    comp[v] = lo;     // v is a round-start root (only roots receive proposals)
+    if (kRecord) {
+      int64_t s = (int64_t)(key & 0xffffffffull);
+      int u = row_of(off, 0, n - 1, s);
+      fe[v] = make_int2(u, (int)__ldg(adj + s));
+    }
   }
 }
 
 // pointer jumping to the root (the root is the component minimum)
-__global__ void k_compress(int* comp, int n) {
+// (optionally counting the roots into *nroots)
+__global__ void k_compress(int* comp, int n, int* nroots) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int c = comp[v];
+    if (nroots) warp_count_add(nroots, c == v);
     int cc = comp[c];
     if (c == cc) continue;
     while (c != cc) { c = cc; cc = comp[c]; }
@@ -91,17 +199,26 @@ __global__ void k_compress(int* comp, int n) {
   }
 }
 
-// Most frequent root among 1024 sampled vertices (one block of 1024).
-__global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc) {
-  __shared__ int val[1024];
+// Most frequent root among 1024 sampled vertices (one block of 1024):
+// shared-memory open-addressing histogram, then a block argmax.
+__global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, bool enable) {
+  constexpr int H = 2048;
+  __shared__ int key[H], num[H];
   __shared__ int bestc[32], bestv[32];
   int t = threadIdx.x;
+  for (int i = t; i < H; i += 1024) { key[i] = -1; num[i] = 0; }
+  __syncthreads();
   int v = (int)(hash32(0x9E3779B9u * (uint32_t)(t + 1)) % (uint32_t)n);
   int mine = comp[v];
-  val[t] = mine;
+  int slot = hash32((uint32_t)mine) & (H - 1);
+  while (true) {
+    int k = atomicCAS(&key[slot], -1, mine);
+    if (k == -1 || k == mine) break;
+    slot = (slot + 1) & (H - 1);
+  }
+  int cnt = atomicAdd(&num[slot], 1) + 1;  // any member's final count works below
   __syncthreads();
-  int cnt = 0;
-  for (int i = 0; i < 1024; i++) cnt += (val[i] == mine);
+  cnt = num[slot];
   // argmax (ties -> smaller root id, deterministic)
   for (int o = 16; o > 0; o >>= 1) {
     int oc = __shfl_down_sync(0xffffffffu, cnt, o);
@@ -117,7 +234,7 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc) {
       int ov = __shfl_down_sync(0xffffffffu, mine, o);
       if (oc > cnt || (oc == cnt && ov < mine)) { cnt = oc; mine = ov; }
     }
-    if (t == 0) sc->giant = mine;
+    if (t == 0) sc->giant = enable ? mine : -1;
   }
 }
 
@@ -128,12 +245,13 @@ struct LinkRestVisitor {
   const int4* rec;
   int giant;
   int rounds;
+  bool halve;
   int64_t rs;
   bool skip;
   int4 rv;
   __device__ __forceinline__ void begin(int v, int64_t s, int64_t e) {
     rs = s;
-    skip = ld_relaxed(comp + v) == giant;
+    skip = ldp(comp + v) == giant;
     if (kSkel && !skip) rv = __ldg(rec + v);
   }
   __device__ __forceinline__ void arc(int v, int64_t a, int w) {
@@ -141,7 +259,7 @@ struct LinkRestVisitor {
     if (kSkel) {
       if (!skel_keep(v, rv, w, __ldg(rec + w))) return;
     }
-    link<kRecord>(v, w, comp, fe);
+    link<kRecord>(v, w, comp, fe, halve);
   }
   __device__ __forceinline__ void end(int, bool) {}
 };
@@ -150,49 +268,68 @@ template <bool kSkel, bool kRecord>
 __global__ void __launch_bounds__(256) k_link_rest(const int64_t* __restrict__ off,
                                                    const uint32_t* __restrict__ adj, int n, int64_t m,
                                                    int rounds, int* comp, int2* fe,
-                                                   const int4* __restrict__ rec, const Scalars* sc) {
+                                                   const int4* __restrict__ rec, const Scalars* sc, bool halve) {
   LinkRestVisitor<kSkel, kRecord> vis;
   vis.comp = comp;
   vis.fe = fe;
   vis.rec = rec;
   vis.giant = sc->giant;
   vis.rounds = rounds;
+  vis.halve = halve;
   visit_arc_chunks(off, adj, n, m, vis);
 }
 
 // Afforest schedule shared by Stage 1 (kSkel=false, record forest) and
 // Stage 5 (kSkel=true, no forest).
 template <bool kSkel, bool kRecord>
-static void run_cc(const Graph& g, int* comp, int2* fe, const int4* rec, Scalars* sc, cudaStream_t st) {
+static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop, const int4* rec, Scalars* sc,
+                   cudaStream_t st) {
   const int B = 256;
-  const int kRounds = 2;
+  const int kRounds = g_opt[OPT_SAMPLE_ROUNDS];
+  const bool halve = g_opt[OPT_FIND_HALVING] != 0;
+  const bool propose = g_opt[OPT_SAMPLE_MODE] == 0;
+  int* nroots = sc->nroots + (kSkel ? 8 : 0);  // device addresses (sc is a device pointer)
   int gv = grid_for(g.n, B);
   k_iota<<<gv, B, 0, st>>>(comp, g.n);
   note(K_IOTA);
+  if (propose && kRounds > 0) {
+    cudaMemsetAsync(prop, 0xFF, sizeof(unsigned long long) * g.n, st);
+    note(K_MEMSET);
+  }
   for (int r = 0; r < kRounds; r++) {
-    k_sample_link<kSkel, kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, fe, rec);
-    note(K_SAMPLE_LINK);
-    k_compress<<<gv, B, 0, st>>>(comp, g.n);
+    if (propose) {
+      k_propose<kSkel><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, rec,
+                                          r > 0 ? nroots + r - 1 : nullptr);
+      note(K_SAMPLE_LINK);
+      k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, comp, prop, fe);
+      note(K_ACCEPT);
+    } else {
+      k_sample_link<kSkel, kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, fe, rec,
+                                                      (g_opt[OPT_SAMPLE_FULL] >> r) & 1, halve);
+      note(K_SAMPLE_LINK);
+    }
+    k_compress<<<gv, B, 0, st>>>(comp, g.n, r < 8 ? nroots + r : nullptr);
     note(K_COMPRESS);
   }
-  k_find_giant<<<1, 1024, 0, st>>>(comp, g.n, sc);
+  k_find_giant<<<1, 1024, 0, st>>>(comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
   note(K_FIND_GIANT);
   int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (nchunks > 0) {
     int ga = grid_for(nchunks, B, 32);
-    k_link_rest<kSkel, kRecord><<<ga, B, 0, st>>>(g.off, g.adj, g.n, g.m, kRounds, comp, fe, rec, sc);
+    k_link_rest<kSkel, kRecord><<<ga, B, 0, st>>>(g.off, g.adj, g.n, g.m, /*skip arcs below*/ 0, comp, fe, rec, sc, halve);
     note(K_LINK_REST);
   }
-  k_compress<<<gv, B, 0, st>>>(comp, g.n);
+  k_compress<<<gv, B, 0, st>>>(comp, g.n, nullptr);
   note(K_COMPRESS);
 }
 
-void stage1_forest(const Graph& g, int* comp, int2* fe, Scalars* sc, cudaStream_t st) {
-  run_cc<false, true>(g, comp, fe, nullptr, sc, st);
+void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st) {
+  run_cc<false, true>(g, comp, fe, prop, nullptr, sc, st);
 }
 
-void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, Scalars* sc, cudaStream_t st) {
-  run_cc<true, false>(g, label, nullptr, rec, sc, st);
+void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
+                        cudaStream_t st) {
+  run_cc<true, false>(g, label, nullptr, prop, rec, sc, st);
 }
 
 }  // namespace fbcc

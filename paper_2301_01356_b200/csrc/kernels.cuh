@@ -49,13 +49,14 @@ struct Tags {
 
 constexpr int kTile = 4096;      // tour positions per tile in the low/high pass
 
-void stage1_forest(const Graph& g, int* comp, int2* fe, Scalars* sc, cudaStream_t st);
+void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st);
 void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int2* A, int2* P,
                     Scalars* sc, cudaStream_t st);
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st);
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out,
                   cudaStream_t st);
-void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, Scalars* sc, cudaStream_t st);
+void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
+                        cudaStream_t st);
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
                       size_t cub_bytes, Scalars* sc, cudaStream_t st);

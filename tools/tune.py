@@ -1,0 +1,55 @@
+"""Tuning harness (GPU box): per-launch device times of one profiled run of
+the pipeline under option variants.  Usage:
+    python tools/tune.py --config 2 --variant sample_rounds=2,find_halving=1 ...
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    import torch
+
+    import workloads
+    from paper_2301_01356_b200 import _lib
+    from paper_2301_01356_b200.bcc import run_device
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="2")
+    ap.add_argument("--variant", action="append", default=[])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--raw", action="store_true")
+    a = ap.parse_args()
+    g = workloads.make(a.config)
+    off = torch.from_numpy(g.offsets).cuda()
+    adj = torch.from_numpy(g.edges.view(np.int32)).cuda()
+    defaults = {k: _lib.get_option(k) for k in _lib.OPTIONS}
+    for var in (a.variant or [""]):
+        for k, v in defaults.items():
+            _lib.set_option(k, v)
+        for kv in filter(None, var.split(",")):
+            k, v = kv.split("=")
+            _lib.set_option(k, int(v))
+        run_device(off, adj)  # warm
+        rows = []
+        for _ in range(a.reps):
+            res, st = run_device(off, adj, profile=True)
+            rows.append([(_lib.kernel_name(st.prof_kind[i]), st.prof_ms[i]) for i in range(st.nprof)])
+            tot = st.total_ms
+        seq = [(rows[0][i][0], np.median([r[i][1] for r in rows])) for i in range(len(rows[0]))]
+        print(f"== variant [{var or 'defaults'}] total {tot:.3f} ms  stages {[round(x, 3) for x in st.stage_ms]}"
+              f" bccs {st.num_bccs}")
+        if a.raw:
+            print("  " + "  ".join(f"{k}:{v * 1e3:.0f}" for k, v in seq))
+        agg = {}
+        for k, v in seq:
+            agg[k] = agg.get(k, 0) + v
+        print("  " + "  ".join(f"{k}:{v * 1e3:.0f}" for k, v in sorted(agg.items(), key=lambda x: -x[1])[:12]))
+
+
+if __name__ == "__main__":
+    main()
