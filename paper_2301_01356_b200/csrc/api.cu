@@ -17,7 +17,7 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "iota", "sample_link", "compress", "find_giant", "link_rest", "root_flags", "scan", "tree_degree",
     "tree_scatter", "link_slots", "link_roots", "walk0", "walk_level", "final_rank", "expand", "positions",
     "w_gather", "tile", "table", "fence", "heads", "ap", "upper_degree", "set_edges", "edge_blocks",
-    "edge_final", "memset", "export", "accept"};
+    "edge_final", "memset", "export", "accept", "chunk_rows"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -30,7 +30,7 @@ constexpr int kFinalMaxHost = 4096;
 
 struct Layout {
   size_t total = 0;
-  size_t sc, comp, fe, prop, rootidx, tdeg, ex, tedges, twin, nxt, own0, rec, A, P, lh1, lh2, table, cnt, uoff,
+  size_t sc, crow, comp, fe, prop, rootidx, tdeg, ex, tedges, twin, nxt, own0, rec, A, P, lh1, lh2, table, cnt, uoff,
       nlow, bmin, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
@@ -45,7 +45,7 @@ struct Layout {
     return at;
   }
 
-  explicit Layout(int64_t n) {
+  explicit Layout(int64_t n, int64_t m) {
     const int64_t N0 = 2 * n;
     const int kS0 = g_opt[OPT_S0], kSl = g_opt[OPT_SL];
     S[0] = kS0;
@@ -63,6 +63,7 @@ struct Layout {
     cub_bytes = scan_temp_bytes(n + 1);
 
     sc = take(sizeof(Scalars));
+    crow = take(4 * ((m + kItems - 1) / kItems + 1));
     comp = take(4 * n);
     fe = take(8 * n);
     prop = take(8 * n);
@@ -111,11 +112,11 @@ struct Pipeline {
 
   Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
            const fbcc_outputs* o)
-      : lay(n) {
-    g = Graph{offsets, edges, (int)n, m};
+      : lay(n, m) {
     out = *o;
     char* ws = (char*)workspace;
     auto at = [&](size_t off) { return (void*)(ws + off); };
+    g = Graph{offsets, edges, (int)n, m, (const int*)at(lay.crow)};
     sc = (Scalars*)at(lay.sc);
     comp = out.comp ? out.comp : (int*)at(lay.comp);
     fe = (int2*)at(lay.fe);
@@ -169,6 +170,7 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mark(0);
+    build_chunk_rows(g, const_cast<int*>(g.crow), st);
     stage1_forest(g, comp, fe, prop, sc, st);
     mark(1);
     stage2_rooting(g, comp, fe, R, T.A, T.P, sc, st);
@@ -243,7 +245,7 @@ static int check_args(const int64_t* offsets, const uint32_t* edges, int64_t n, 
   if (!out || !offsets || (m > 0 && !edges)) return FBCC_ERR_ARG;
   if (n == 0) return FBCC_OK;
   if (!out->label || !out->head || !workspace) return FBCC_ERR_ARG;
-  Layout lay(n);
+  Layout lay(n, m);
   if (workspace_bytes < lay.total) return FBCC_ERR_WORKSPACE;
   return FBCC_OK;
 }
@@ -252,7 +254,7 @@ int fbcc_workspace_bytes(int64_t n, int64_t m, size_t* bytes_out) {
   if (!bytes_out) return FBCC_ERR_ARG;
   int rc = check_sizes(n, m);
   if (rc) return rc;
-  Layout lay(n);
+  Layout lay(n, m);
   *bytes_out = lay.total;
   return FBCC_OK;
 }

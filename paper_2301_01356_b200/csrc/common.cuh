@@ -30,7 +30,7 @@ enum KernelKind : int {
   K_IOTA = 0, K_SAMPLE_LINK, K_COMPRESS, K_FIND_GIANT, K_LINK_REST, K_ROOT_FLAGS, K_SCAN, K_TREE_DEGREE,
   K_TREE_SCATTER, K_LINK_SLOTS, K_LINK_ROOTS, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_POSITIONS,
   K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_AP, K_UPPER_DEGREE, K_SET_EDGES, K_EDGE_BLOCKS,
-  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_ACCEPT, K_NUM_KINDS
+  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_ACCEPT, K_CHUNK_ROWS, K_NUM_KINDS
 };
 
 struct LaunchLog {
@@ -138,9 +138,10 @@ __device__ __forceinline__ int row_of(const int64_t* __restrict__ off, int lo, i
 
 // ---------------------------------------------------------------------------
 // Arc-balanced CSR traversal.  Every thread owns kItems consecutive arcs
-// (one 32-byte sector of targets, loaded as two 128-bit vectors); a warp
-// finds its row window with two full binary searches and each lane then
-// searches inside the window.  The visitor sees rows in order:
+// (one 32-byte sector of targets, loaded as two 128-bit vectors) and reads
+// the row of its first arc from the per-run chunk->row table (crow, built by
+// k_chunk_rows; hub rows fall back to a binary search).  The visitor sees
+// rows in order:
 //   begin(v, row_start, row_end)  arc(v, a, w)  end(v, whole)
 // where ``whole`` says the row lies entirely inside this thread's chunk (no
 // other thread touches it -- plain stores are safe; otherwise combine with
@@ -151,24 +152,12 @@ constexpr int kItems = 8;
 template <class Visitor>
 __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off,
                                                  const uint32_t* __restrict__ adj,
+                                                 const int* __restrict__ crow,
                                                  int n, int64_t m, Visitor& vis) {
   const int64_t nchunks = (m + kItems - 1) / kItems;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t warp_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
-  for (int64_t wbase = warp_id * 32; wbase < nchunks; wbase += warps_total * 32) {
-    // warp window [vlo, vhi]
-    int64_t first_a = wbase * kItems;
-    int64_t last_chunk = wbase + 31 < nchunks ? wbase + 31 : nchunks - 1;
-    int64_t last_a = (last_chunk + 1) * kItems < m ? (last_chunk + 1) * kItems - 1 : m - 1;  // warp's last arc
-    int s = 0;
-    if (lane == 0) s = row_of(off, 0, n - 1, first_a);
-    if (lane == 1) s = row_of(off, 0, n - 1, last_a);
-    int vlo = __shfl_sync(0xffffffffu, s, 0);
-    int vhi = __shfl_sync(0xffffffffu, s, 1);
-    int64_t q = wbase + lane;
-    if (q >= nchunks) continue;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nchunks; q += stride) {
     int64_t a0 = q * kItems;
     int64_t a1 = a0 + kItems < m ? a0 + kItems : m;
     uint32_t w[kItems];
@@ -181,7 +170,8 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
 #pragma unroll
       for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;
     }
-    int v = row_of(off, vlo, vhi, a0);
+    int v = __ldg(crow + q);
+    if (v < 0) v = row_of(off, 0, n - 1, a0);  // chunk inside a hub row (see k_chunk_rows)
     int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
     vis.begin(v, rs, re);
 #pragma unroll
@@ -190,7 +180,7 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
       if (a < a1) {
         if (a >= re) {
           vis.end(v, rs >= a0);
-          v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, vhi, a);
+          v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, n - 1, a);
           rs = __ldg(off + v);
           re = __ldg(off + v + 1);
           vis.begin(v, rs, re);
@@ -201,6 +191,13 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
     vis.end(v, rs >= a0 && re <= a1);
   }
 }
+
+// chunk -> row table for visit_arc_chunks: crow[q] = row holding arc q*kItems,
+// written by the row itself (one thread per row) for rows spanning at most
+// kRowChunks chunks; chunks inside longer (hub) rows keep -1 from the memset
+// and fall back to a binary search.  One pass of n threads replaces a binary
+// search per chunk in each of the four arc-balanced kernels of a run.
+constexpr int kRowChunks = 64;
 
 // warp-aggregated increment of a global counter
 __device__ __forceinline__ void warp_count_add(int* ctr, bool pred) {

@@ -83,6 +83,26 @@ __device__ __forceinline__ void link(int u, int w, int* comp, int2* fe, bool hal
   }
 }
 
+// chunk -> row table (see visit_arc_chunks): row v owns the chunks whose
+// first arc lies in it
+__global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int64_t q0 = (__ldg(off + v) + kItems - 1) / kItems;
+    int64_t q1 = (__ldg(off + v + 1) + kItems - 1) / kItems;
+    if (q1 - q0 > kRowChunks) continue;  // hub row: consumers binary-search
+    for (int64_t q = q0; q < q1; q++) crow[q] = v;
+  }
+}
+
+void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st) {
+  int64_t nchunks = (g.m + kItems - 1) / kItems;
+  if (nchunks == 0) return;
+  cudaMemsetAsync(crow, 0xFF, sizeof(int) * nchunks, st);
+  note(K_MEMSET);
+  k_chunk_rows<<<grid_for(g.n, 256), 256, 0, st>>>(g.off, g.n, crow);
+  note(K_CHUNK_ROWS);
+}
+
 __global__ void k_iota(int* __restrict__ comp, int n) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) comp[v] = v;
 }
@@ -266,7 +286,7 @@ struct LinkRestVisitor {
 
 template <bool kSkel, bool kRecord>
 __global__ void __launch_bounds__(256) k_link_rest(const int64_t* __restrict__ off,
-                                                   const uint32_t* __restrict__ adj, int n, int64_t m,
+                                                   const uint32_t* __restrict__ adj, const int* __restrict__ crow, int n, int64_t m,
                                                    int rounds, int* comp, int2* fe,
                                                    const int4* __restrict__ rec, const Scalars* sc, bool halve) {
   LinkRestVisitor<kSkel, kRecord> vis;
@@ -276,7 +296,7 @@ __global__ void __launch_bounds__(256) k_link_rest(const int64_t* __restrict__ o
   vis.giant = sc->giant;
   vis.rounds = rounds;
   vis.halve = halve;
-  visit_arc_chunks(off, adj, n, m, vis);
+  visit_arc_chunks(off, adj, crow, n, m, vis);
 }
 
 // Afforest schedule shared by Stage 1 (kSkel=false, record forest) and
@@ -316,7 +336,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (nchunks > 0) {
     int ga = grid_for(nchunks, B, 32);
-    k_link_rest<kSkel, kRecord><<<ga, B, 0, st>>>(g.off, g.adj, g.n, g.m, /*skip arcs below*/ 0, comp, fe, rec, sc, halve);
+    k_link_rest<kSkel, kRecord><<<ga, B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, /*skip arcs below*/ 0, comp, fe, rec, sc, halve);
     note(K_LINK_REST);
   }
   k_compress<<<gv, B, 0, st>>>(comp, g.n, nullptr);

@@ -13,7 +13,10 @@ struct Graph {
   const uint32_t* adj;   // [m]
   int n;
   int64_t m;
+  const int* crow;       // [ceil(m/kItems)] chunk -> row table (build_chunk_rows)
 };
+
+void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st);
 
 // Device arrays for the rooting / tags stages (see api.cu for the layout).
 struct Rooting {

@@ -107,7 +107,7 @@ struct EdgeBlockVisitor {
   __device__ __forceinline__ void end(int, bool) {}
 };
 
-__global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+__global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
                                                      int n, int64_t m, const int* __restrict__ label,
                                                      const int* __restrict__ head, const int* __restrict__ uoff,
                                                      const int* __restrict__ nlow, int* eblk, int* bmin) {
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__
   vis.eblk = eblk;
   vis.bmin = bmin;
   vis.run_blk = -1;
-  visit_arc_chunks(off, adj, n, m, vis);
+  visit_arc_chunks(off, adj, crow, n, m, vis);
   vis.flush();
 }
 
@@ -161,7 +161,7 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
     cudaMemsetAsync(bmin, 0x7F, sizeof(int) * n, st);
     note(K_MEMSET);
     int64_t nchunks = (g.m + kItems - 1) / kItems;
-    k_edge_blocks<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, n, g.m, label, head, uoff, nlow,
+    k_edge_blocks<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow,
                                                           edge_label, bmin);
     note(K_EDGE_BLOCKS);
     k_edge_final<<<grid_for(g.m / 2, B), B, 0, st>>>(edge_label, bmin, uoff, n);

@@ -64,12 +64,12 @@ struct WGatherVisitor {
   }
 };
 
-__global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+__global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
                                                   int n, int64_t m, const int4* __restrict__ rec, int2* A) {
   WGatherVisitor vis;
   vis.rec = rec;
   vis.A = A;
-  visit_arc_chunks(off, adj, n, m, vis);
+  visit_arc_chunks(off, adj, crow, n, m, vis);
 }
 
 // ---------------------------------------------------------------------------
@@ -186,7 +186,7 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st) {
   const int B = 256;
   int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (g.m > 0) {
-    k_w_gather<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.n, g.m, R.rec, T.A);
+    k_w_gather<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, R.rec, T.A);
     note(K_W_GATHER);
   }
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
