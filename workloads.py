@@ -99,6 +99,85 @@ def rmat(scale: int = 25, edge_factor: int = 16, seed: int = 0,
     return symmetrize(np.concatenate(parts), n)
 
 
+# ---------------------------------------------------------------------------
+# Large configs on the device: the same pairs (same PCG64 draws, same
+# candidate order) are built on the host, then symmetrised on the GPU
+# (sort + unique of packed 64-bit keys) -- the host numpy sort of 4e8-1e9 keys
+# dominates otherwise.  The resulting CSR is identical to symmetrize()'s.
+# ---------------------------------------------------------------------------
+def _pairs(name):
+    if name == "4a":
+        rows, cols, keep_prob = 10**4, 10**4, 1.0
+    elif name == "4b":
+        rows, cols, keep_prob = 10**3, 10**5, 0.6
+    elif name == "4c":
+        i = np.arange(10**8 - 1, dtype=np.int64)
+        return i, i + 1, 10**8
+    elif name == "5":
+        return _rmat_pairs() + (1 << 25,)
+    else:
+        raise KeyError(name)
+    n = rows * cols
+    ids = np.arange(n, dtype=np.int64).reshape(rows, cols)
+    u = np.concatenate([ids.ravel(), ids.ravel()])
+    v = np.concatenate([np.roll(ids, -1, axis=1).ravel(), np.roll(ids, -1, axis=0).ravel()])
+    if keep_prob < 1.0:
+        keep = np.random.Generator(np.random.PCG64(0)).random(u.size) < keep_prob
+        u, v = u[keep], v[keep]
+    return u, v, n
+
+
+def _rmat_pairs(scale=25, edge_factor=16, seed=0, chunk=1 << 24):
+    n = 1 << scale
+    total = edge_factor * n
+    rng = np.random.Generator(np.random.PCG64(seed))
+    us, vs = [], []
+    done = 0
+    while done < total:
+        k = min(chunk, total - done)
+        u = np.zeros(k, np.int64)
+        v = np.zeros(k, np.int64)
+        for lvl in range(scale):
+            r = rng.random(k)
+            bit = np.int64(1) << np.int64(scale - 1 - lvl)
+            u |= np.where(r >= 0.76, bit, 0)
+            v |= np.where(((r >= 0.57) & (r < 0.76)) | (r >= 0.95), bit, 0)
+        us.append(u)
+        vs.append(v)
+        done += k
+    return np.concatenate(us), np.concatenate(vs)
+
+
+def symmetrize_device(u, v, n, device="cuda"):
+    """symmetrize() on the GPU; returns (offsets int64[n+1], edges int32[m]) tensors."""
+    import torch
+
+    u = torch.as_tensor(u).to(device)
+    v = torch.as_tensor(v).to(device)
+    keep = u != v
+    u, v = u[keep], v[keep]
+    keys = torch.cat([(u << 32) | v, (v << 32) | u])
+    del u, v, keep
+    keys = torch.unique(keys, sorted=True)
+    src = keys >> 32
+    dst = (keys & 0xFFFFFFFF).to(torch.int32)
+    del keys
+    off = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    off[1:] = torch.cumsum(torch.bincount(src, minlength=n), 0)
+    return off, dst
+
+
+def make_device(name, device="cuda"):
+    """Config ``name`` as device tensors (offsets int64, edges int32)."""
+    if name in ("1", "2", "3"):
+        import torch
+
+        g = make(name)
+        return (torch.from_numpy(g.offsets).to(device), torch.from_numpy(g.edges.view(np.int32)).to(device))
+    u, v, n = _pairs(name)
+    return symmetrize_device(u, v, n, device)
+
+
 CONFIGS = {
     "1": ("torus 300x300 p=0.6", lambda: grid(300, 300, circular=True, keep_prob=0.6, seed=0)),
     "2": ("uniform n=2^20 m=8n", lambda: uniform()),
