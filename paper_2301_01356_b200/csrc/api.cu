@@ -17,20 +17,20 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "iota", "sample_link", "compress", "find_giant", "link_rest", "root_flags", "scan", "tree_degree",
     "tree_scatter", "link_slots", "link_roots", "walk0", "walk_level", "final_rank", "expand", "positions",
     "w_gather", "tile", "table", "fence", "heads", "ap", "upper_degree", "set_edges", "edge_blocks",
-    "edge_final", "memset", "export", "accept", "chunk_rows"};
+    "edge_final", "memset", "export", "accept", "chunk_rows", "root_list"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
   return FBCC_ERR_CUDA;
 }
 
-int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*halving*/ 1, /*S0*/ 16, /*SL*/ 32,
+int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*halving*/ 1, /*S0*/ 16, /*SL*/ 8,
                       /*full-link rounds mask*/ 0, /*sample mode: propose/accept*/ 0};
-constexpr int kFinalMaxHost = 4096;
+constexpr int kFinalMaxHost = kFinalMax;
 
 struct Layout {
   size_t total = 0;
-  size_t sc, crow, comp, fe, prop, rootidx, tdeg, ex, tedges, twin, nxt, own0, rec, A, P, lh1, lh2, table, cnt, uoff,
+  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, nexto, nxt, own0, rec, A, P, lh1, lh2, table, cnt, uoff,
       nlow, bmin, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
@@ -67,11 +67,11 @@ struct Layout {
     comp = take(4 * n);
     fe = take(8 * n);
     prop = take(8 * n);
-    rootidx = take(4 * 2 * (n + 1));
-    tdeg = take(4 * 2 * (n + 1));
-    ex = take(16 * n);
-    tedges = take(4 * N0);
-    twin = take(4 * N0);
+    flags = take(4 * (n + 1));
+    rootidx = take(4 * (n + 1));
+    rlist = take(4 * n);
+    lhead = take(4 * n);
+    nexto = take(4 * N0);
     nxt = take(4 * N0);
     own0 = take(8 * N0);
     for (int l = 1; l <= nlev; l++) {
@@ -121,11 +121,11 @@ struct Pipeline {
     comp = out.comp ? out.comp : (int*)at(lay.comp);
     fe = (int2*)at(lay.fe);
     prop = (unsigned long long*)at(lay.prop);
+    R.flags = (int*)at(lay.flags);
     R.rootidx = (int*)at(lay.rootidx);
-    R.tdeg = (int*)at(lay.tdeg);
-    R.ex = (int4*)at(lay.ex);
-    R.tedges = (int*)at(lay.tedges);
-    R.twin = (int*)at(lay.twin);
+    R.rlist = (int*)at(lay.rlist);
+    R.lhead = (int*)at(lay.lhead);
+    R.nexto = (int*)at(lay.nexto);
     R.nxt = (int*)at(lay.nxt);
     R.own0 = (int2*)at(lay.own0);
     R.nlev = lay.nlev;

@@ -30,7 +30,7 @@ enum KernelKind : int {
   K_IOTA = 0, K_SAMPLE_LINK, K_COMPRESS, K_FIND_GIANT, K_LINK_REST, K_ROOT_FLAGS, K_SCAN, K_TREE_DEGREE,
   K_TREE_SCATTER, K_LINK_SLOTS, K_LINK_ROOTS, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_POSITIONS,
   K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_AP, K_UPPER_DEGREE, K_SET_EDGES, K_EDGE_BLOCKS,
-  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_ACCEPT, K_CHUNK_ROWS, K_NUM_KINDS
+  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_ACCEPT, K_CHUNK_ROWS, K_ROOT_LIST, K_NUM_KINDS
 };
 
 struct LaunchLog {
@@ -198,6 +198,21 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
 // and fall back to a binary search.  One pass of n threads replaces a binary
 // search per chunk in each of the four arc-balanced kernels of a run.
 constexpr int kRowChunks = 64;
+
+// Block-reduced counter add: every thread of the block must call it (after
+// its grid-stride loop) with its private count; one atomic per block.
+__device__ __forceinline__ void block_count_add(int* ctr, int mine) {
+  __shared__ int warp_sums[32];
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) warp_sums[warp] = mine;
+  __syncthreads();
+  if (warp == 0) {
+    int s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0 && s) atomicAdd(ctr, s);
+  }
+}
 
 // warp-aggregated increment of a global counter
 __device__ __forceinline__ void warp_count_add(int* ctr, bool pred) {

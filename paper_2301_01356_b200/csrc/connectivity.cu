@@ -185,12 +185,13 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
     // (small components below the giant's root all aim at it in round 2)
     unsigned peers = __match_any_sync(__activemask(), hi);
     if ((threadIdx.x & 31) != __ffs(peers) - 1) continue;
-    atomicMin(prop + hi, ((unsigned long long)(unsigned)lo << 32) | (unsigned long long)(uint32_t)s);
+    // low word = the proposer: its arc is off[v] + round, no search on accept
+    atomicMin(prop + hi, ((unsigned long long)(unsigned)lo << 32) | (unsigned long long)(uint32_t)v);
   }
 }
 
 template <bool kRecord>
-__global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int* comp,
+__global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
                          unsigned long long* prop, int2* fe) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     unsigned long long key = prop[v];
@@ -199,24 +200,38 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
     int lo = (int)(key >> 32);
     comp[v] = lo;     // v is a round-start root (only roots receive proposals)
     if (kRecord) {
-      int64_t s = (int64_t)(key & 0xffffffffull);
-      int u = row_of(off, 0, n - 1, s);
-      fe[v] = make_int2(u, (int)__ldg(adj + s));
+      int u = (int)(key & 0xffffffffull);
+      fe[v] = make_int2(u, (int)__ldg(adj + __ldg(off + u) + round));
     }
   }
 }
 
 // pointer jumping to the root (the root is the component minimum)
-// (optionally counting the roots into *nroots)
+// (optionally counting the roots into *nroots).  Every step stores the
+// advanced pointer and reads the parent's CURRENT pointer from L2, so
+// concurrent threads ride each other's progress: pointer doubling, ~log2(depth)
+// steps per thread.  Walking to the root and storing once at the end is
+// O(depth) per thread -- O(n^2) on a 10^8-vertex path whose round-0 hooks
+// form one chain (3.2 s measured on config 4c).
+//
+// No hooks happen during a compress, so a root's entry is stable: the
+// "is c a root" test may use an L1-cached load (the giant root's word is then
+// served per SM instead of hammering one L2 slice), and only non-root
+// pointers -- which other threads are advancing -- are re-read from L2.
 __global__ void k_compress(int* comp, int n, int* nroots) {
+  int roots = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    int c = comp[v];
-    if (nroots) warp_count_add(nroots, c == v);
-    int cc = comp[c];
-    if (c == cc) continue;
-    while (c != cc) { c = cc; cc = comp[c]; }
-    comp[v] = c;
+    int c = __ldcg(comp + v);
+    roots += (c == v);
+    if (c == v) continue;
+    while (true) {
+      if (__ldca(comp + c) == c) break;  // root (stable during compress)
+      int cc = __ldcg(comp + c);           // c's current pointer
+      __stcg(comp + v, cc);
+      c = cc;
+    }
   }
+  if (nroots) block_count_add(nroots, roots);
 }
 
 // Most frequent root among 1024 sampled vertices (one block of 1024):
@@ -310,6 +325,10 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   const bool propose = g_opt[OPT_SAMPLE_MODE] == 0;
   int* nroots = sc->nroots + (kSkel ? 8 : 0);  // device addresses (sc is a device pointer)
   int gv = grid_for(g.n, B);
+  // k_compress relies on concurrent threads advancing each other's pointers:
+  // its grid must be fully resident (2048 threads/SM), or grid-stride
+  // threads chase pointers owned by blocks that cannot be scheduled yet
+  const int gres = grid_for(g.n, B, 2048 / B);
   k_iota<<<gv, B, 0, st>>>(comp, g.n);
   note(K_IOTA);
   if (propose && kRounds > 0) {
@@ -321,14 +340,14 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       k_propose<kSkel><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, rec,
                                           r > 0 ? nroots + r - 1 : nullptr);
       note(K_SAMPLE_LINK);
-      k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, comp, prop, fe);
+      k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, fe);
       note(K_ACCEPT);
     } else {
       k_sample_link<kSkel, kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, fe, rec,
                                                       (g_opt[OPT_SAMPLE_FULL] >> r) & 1, halve);
       note(K_SAMPLE_LINK);
     }
-    k_compress<<<gv, B, 0, st>>>(comp, g.n, r < 8 ? nroots + r : nullptr);
+    k_compress<<<gres, B, 0, st>>>(comp, g.n, r < 8 ? nroots + r : nullptr);
     note(K_COMPRESS);
   }
   k_find_giant<<<1, 1024, 0, st>>>(comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
@@ -339,7 +358,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     k_link_rest<kSkel, kRecord><<<ga, B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, /*skip arcs below*/ 0, comp, fe, rec, sc, halve);
     note(K_LINK_REST);
   }
-  k_compress<<<gv, B, 0, st>>>(comp, g.n, nullptr);
+  k_compress<<<gres, B, 0, st>>>(comp, g.n, nullptr);
   note(K_COMPRESS);
 }
 

@@ -19,12 +19,14 @@ struct Graph {
 void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st);
 
 // Device arrays for the rooting / tags stages (see api.cu for the layout).
+constexpr int kFinalMax = 16384;  // list-ranking level finished in one CTA
+
 struct Rooting {
-  int* rootidx;    // [n+1] exclusive scan of (comp[v] == v)
-  int* tdeg;       // [n+1] tree degree, scanned in place into toff
-  int4* ex;        // [n]   forest edge of hooked vertex x: {u, v, slot_u, slot_v}
-  int* tedges;     // [2n]  tree CSR targets
-  int* twin;       // [2n]  reverse slot
+  int* flags;      // [n+1] comp[v] == v
+  int* rootidx;    // [n+1] exclusive scan of flags (rank among roots)
+  int* rlist;      // [n]   roots in id order
+  int* lhead;      // [n]   first out-arc of each vertex (-1: none)
+  int* nexto;      // [2n]  next out-arc of the same vertex
   int* nxt;        // [2n]  unified tour list successor
   int2* own0;      // [2n]  (segment, offset) per list element
   // ruling-set levels 1..nlev: element counts and arrays

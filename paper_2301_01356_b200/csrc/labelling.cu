@@ -41,12 +41,14 @@ __global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restri
 // one thread per label: count the block and bump its head's (saturating)
 // headed-count for the articulation rule of bcc.py:229-234
 __global__ void k_count_blocks(int n, const int* __restrict__ head, int* cnt, Scalars* sc) {
+  int blocks = 0;
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
     int h = __ldg(head + l);
-    bool blk = h >= 0;
-    if (blk && ld_relaxed(cnt + h) < 2) atomicAdd(cnt + h, 1);
-    warp_count_add(&sc->nbccs, blk);
+    if (h < 0) continue;
+    blocks++;
+    if (ld_relaxed(cnt + h) < 2) atomicAdd(cnt + h, 1);
   }
+  block_count_add(&sc->nbccs, blocks);
 }
 
 __global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict__ head,

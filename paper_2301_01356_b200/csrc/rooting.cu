@@ -9,40 +9,38 @@
 // (_vertex_positions 262-294).
 //
 // B200 design:
-//  * Tree CSR: one atomicAdd per endpoint returns the arc's rank inside its
-//    row, so after a CUB scan the scatter needs no second atomic pass.
-//  * ONE list for the whole forest.  Every root r contributes two virtual
-//    elements, enter(r) = 2*ri and exit(r) = 2*ri+1 (ri = rank of r among
-//    roots); tree arc slot t is element 2c+t.  enter(r) -> r's first out-arc
-//    ... -> the in-arc that closes r's circuit -> exit(r) -> enter(next root).
-//    The list has exactly 2n elements, its head is element 0, and an
-//    element's rank IS its tour position in the reference layout (tree of
-//    root r owns [base_r, base_r + 2 size_r), root at both ends, trees in
-//    root-id order, euler_tour.py:12-17).  No per-tree base scan, no list
-//    heads beyond element 0.
-//  * Ruling-set list ranking: splitters are one hash-chosen element per
-//    window of S consecutive ids (so structured tours, e.g. a chain whose
-//    return path only touches odd ids, are still cut), the splitter index is
-//    the window index (no compaction), each splitter walks to the next one
-//    writing (segment, offset) per element; recurse on the weighted splitter
-//    list until it fits one CTA, which finishes with Wyllie pointer jumping
-//    in shared memory.  Offsets are pushed back down level by level; level 0
-//    ranks are never materialised -- the positions kernel computes
-//    rank(e) = offs1[own0[e].seg] + own0[e].off on the fly.
-//  * Positions: one thread per forest edge compares the ranks of its two
-//    arcs: the earlier one is the down arc, giving parent, first and last of
-//    the child in one shot (no per-vertex loop over tree degree, so hub
-//    vertices cost nothing extra).  It also initialises the tour-indexed
-//    arrays the tag stage reads (A: (first, first) at entry, filler at exit;
-//    P: vertex id + partner position).
+//  * Element numbering without a tree CSR.  Stage 1 records the forest edge
+//    that hooked vertex x at fe[x]; list elements 2x and 2x+1 are that
+//    edge's two arcs (u->v, v->u).  A root r has no such edge, and its pair
+//    2r / 2r+1 becomes the virtual enter(r) / exit(r) of its tree.  So the
+//    whole forest is 2n elements with no holes and no compaction.
+//  * Euler circuit: every vertex's out-arcs form a list built by one
+//    atomicExch per arc (no degree histogram, scan or scatter).  Arriving at
+//    t through arc e, the tour leaves through the out-arc after e^1 in t's
+//    list, wrapping to the first (non-root) or to exit(t) (root).
+//  * ONE list for the forest: enter(r) -> first out-arc of r ... -> exit(r)
+//    -> enter(next root by id).  Its head is element 0 (vertex 0 is always a
+//    root) and each element's rank IS its tour position in the reference
+//    layout (tree of root r owns [base_r, base_r + 2 size_r), root at both
+//    ends, trees in root-id order, euler_tour.py:12-17).
+//  * Ruling-set list ranking: one hash-placed splitter per window of S ids
+//    (splitter index = window index: no compaction; structured tours such as
+//    a chain's return path, which touches every other id, are still cut);
+//    each splitter walks to the next writing (segment, offset) per element;
+//    recurse on the weighted splitter list until it fits one CTA (Wyllie
+//    pointer jumping in shared memory).  Level-0 ranks are never
+//    materialised: rank(e) = offs1[own0[e].seg] + own0[e].off.
+//  * Positions: one thread per vertex x reads own0[2x..2x+1] as ONE 16-byte
+//    load; the earlier of the two arcs is the down arc, giving the child's
+//    parent, first and last.  It also initialises the tour-indexed arrays the
+//    tag stage reads (A: (first, first) at entry, filler at exit; P: vertex
+//    id + partner position).
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace fbcc {
-
-constexpr int kFinalMax = 4096;
 
 // ---------------------------------------------------------------------------
 // scans (CUB)
@@ -59,77 +57,58 @@ void exclusive_scan(const int* in, int* out, int64_t items, void* tmp, size_t tm
 }
 
 // ---------------------------------------------------------------------------
-// tree CSR
+// roots in id order
 // ---------------------------------------------------------------------------
 __global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restrict__ flags) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x)
     flags[v] = (v < n) ? (__ldg(comp + v) == v) : 0;
 }
 
-__global__ void k_tree_degree(const int* __restrict__ comp, const int2* __restrict__ fe, int n, int* tdeg,
-                              int4* __restrict__ ex, const int* __restrict__ rootidx, Scalars* sc) {
+// rlist[rank among roots] = root;  sc->ncomp = c
+__global__ void k_root_list(const int* __restrict__ comp, const int* __restrict__ rootidx, int n,
+                            int* __restrict__ rlist, Scalars* sc) {
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid == 0) sc->ncomp = rootidx[n];
-  for (int x = (int)tid; x < n; x += gridDim.x * blockDim.x) {
-    if (__ldg(comp + x) == x) continue;
-    int2 e = fe[x];
-    int lu = atomicAdd(tdeg + e.x, 1);
-    int lv = atomicAdd(tdeg + e.y, 1);
-    ex[x] = make_int4(e.x, e.y, lu, lv);
-  }
+  for (int r = (int)tid; r < n; r += gridDim.x * blockDim.x)
+    if (__ldg(comp + r) == r) rlist[__ldg(rootidx + r)] = r;
 }
 
-__global__ void k_tree_scatter(const int* __restrict__ comp, int n, const int* __restrict__ toff,
-                               int4* __restrict__ ex, int* __restrict__ tedges, int* __restrict__ twin) {
+// out-arc lists: arc 2x = u->v is an out-arc of u, 2x+1 = v->u of v
+__global__ void k_out_lists(const int* __restrict__ comp, const int2* __restrict__ fe, int n, int* lhead,
+                            int* __restrict__ nexto) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     if (__ldg(comp + x) == x) continue;
-    int4 e = ex[x];
-    int su = __ldg(toff + e.x) + e.z;
-    int sv = __ldg(toff + e.y) + e.w;
-    tedges[su] = e.y;
-    tedges[sv] = e.x;
-    twin[su] = sv;
-    twin[sv] = su;
-    ex[x] = make_int4(e.x, e.y, su, sv);
+    int2 e = __ldg(fe + x);
+    nexto[2 * x] = atomicExch(lhead + e.x, 2 * x);
+    nexto[2 * x + 1] = atomicExch(lhead + e.y, 2 * x + 1);
   }
 }
 
-// Unified tour list.  Arc slot t (element 2c+t) arrives at v = tedges[t];
-// its twin is v's out-slot i; the tour continues with v's out-slot i+1, or,
-// after v's last out-slot, with v's first out-slot (non-root: closes the
-// circuit around v) or exit(v) (root: the tour of v's tree is complete).
-__global__ void k_link_slots(const int* __restrict__ comp, const int* __restrict__ toff,
-                             const int* __restrict__ tedges, const int* __restrict__ twin,
-                             const int* __restrict__ rootidx, int n, int* __restrict__ nxt,
-                             const Scalars* sc) {
+__global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict__ fe,
+                            const int* __restrict__ lhead, const int* __restrict__ nexto,
+                            const int* __restrict__ rootidx, const int* __restrict__ rlist, int n,
+                            int* __restrict__ nxt, const Scalars* sc) {
   const int c = sc->ncomp;
-  const int L = 2 * (n - c);
-  const int c2 = 2 * c;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < L; t += gridDim.x * blockDim.x) {
-    int v = __ldg(tedges + t);
-    int s = __ldg(twin + t);
-    int b = __ldg(toff + v);
-    int k = __ldg(toff + v + 1) - b;
-    int i = s - b;
-    int e;
-    if (i + 1 < k) e = c2 + b + i + 1;
-    else if (__ldg(comp + v) == v) e = 2 * __ldg(rootidx + v) + 1;
-    else e = c2 + b;
-    nxt[c2 + t] = e;
-  }
-}
-
-__global__ void k_link_roots(const int* __restrict__ comp, const int* __restrict__ toff,
-                             const int* __restrict__ rootidx, int n, int* __restrict__ nxt,
-                             const Scalars* sc) {
-  const int c = sc->ncomp;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    if (__ldg(comp + r) != r) continue;
-    int ri = __ldg(rootidx + r);
-    int b = __ldg(toff + r);
-    int k = __ldg(toff + r + 1) - b;
-    nxt[2 * ri] = k > 0 ? 2 * c + b : 2 * ri + 1;
-    nxt[2 * ri + 1] = (ri + 1 < c) ? 2 * ri + 2 : -1;
+  const int64_t N = 2 * (int64_t)n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+    int x = (int)(e >> 1);
+    int out;
+    if (__ldg(comp + x) == x) {  // enter(x) / exit(x)
+      if ((e & 1) == 0) {
+        int h = __ldg(lhead + x);
+        out = h >= 0 ? h : (int)e + 1;
+      } else {
+        int ri = __ldg(rootidx + x);
+        out = (ri + 1 < c) ? 2 * __ldg(rlist + ri + 1) : -1;
+      }
+    } else {  // arc e arrives at t; leave through the out-arc after e^1
+      int2 uv = __ldg(fe + x);
+      int t = (e & 1) ? uv.x : uv.y;
+      int nx = __ldg(nexto + (e ^ 1));
+      if (nx >= 0) out = nx;
+      else out = (__ldg(comp + t) == t) ? 2 * t + 1 : __ldg(lhead + t);
+    }
+    nxt[e] = out;
   }
 }
 
@@ -167,28 +146,32 @@ __global__ void __launch_bounds__(256) k_walk(int64_t K, int S, int64_t N, const
 
 // Final level: <= kFinalMax elements, head = element 0; exclusive weighted
 // prefix along the list by Wyllie pointer jumping over predecessor links,
-// entirely in shared memory (one CTA).
-__global__ void __launch_bounds__(1024) k_final_rank(int K, const int* __restrict__ succ,
-                                                     const int* __restrict__ w, int* __restrict__ offs) {
-  __shared__ int P[kFinalMax];
-  __shared__ int V[kFinalMax];
+// entirely in shared memory (one CTA, 2 x 64 KB).
+constexpr int kFinalThreads = 1024;
+constexpr size_t kFinalSmem = 2 * sizeof(int) * kFinalMax;
+
+__global__ void __launch_bounds__(kFinalThreads) k_final_rank(int K, const int* __restrict__ succ,
+                                                              const int* __restrict__ w, int* __restrict__ offs) {
+  extern __shared__ int fsm[];
+  int* P = fsm;
+  int* V = fsm + kFinalMax;
   const int t = threadIdx.x;
-  for (int j = t; j < K; j += 1024) P[j] = -1;
+  for (int j = t; j < K; j += kFinalThreads) P[j] = -1;
   __syncthreads();
-  for (int j = t; j < K; j += 1024) {
+  for (int j = t; j < K; j += kFinalThreads) {
     int s = succ[j];
     if (s >= 0) P[s] = j;
   }
   __syncthreads();
-  for (int j = t; j < K; j += 1024) V[j] = P[j] >= 0 ? w[P[j]] : 0;
+  for (int j = t; j < K; j += kFinalThreads) V[j] = P[j] >= 0 ? w[P[j]] : 0;
   __syncthreads();
-  constexpr int PER = kFinalMax / 1024;
-  for (int round = 0; round < 13; round++) {
+  constexpr int PER = kFinalMax / kFinalThreads;
+  for (int round = 0; round < 32; round++) {
     int np[PER], nv[PER];
     int active = 0;
 #pragma unroll
     for (int q = 0; q < PER; q++) {
-      int j = t + q * 1024;
+      int j = t + q * kFinalThreads;
       np[q] = -1;
       nv[q] = 0;
       if (j < K) {
@@ -200,12 +183,12 @@ __global__ void __launch_bounds__(1024) k_final_rank(int K, const int* __restric
     if (!__syncthreads_or(active)) break;
 #pragma unroll
     for (int q = 0; q < PER; q++) {
-      int j = t + q * 1024;
+      int j = t + q * kFinalThreads;
       if (j < K) { P[j] = np[q]; V[j] = nv[q]; }
     }
     __syncthreads();
   }
-  for (int j = t; j < K; j += 1024) offs[j] = V[j];
+  for (int j = t; j < K; j += kFinalThreads) offs[j] = V[j];
 }
 
 __global__ void k_expand(int64_t K, const int2* __restrict__ own, const int* __restrict__ offs_up,
@@ -227,23 +210,19 @@ __device__ __forceinline__ void place(int v, int f, int l, int par, int4* rec, i
   P[l] = make_int2(~v, f);
 }
 
-__global__ void k_positions(const int* __restrict__ comp, const int4* __restrict__ ex,
-                            const int* __restrict__ rootidx, const int2* __restrict__ own0,
-                            const int* __restrict__ offs1, int n, int4* __restrict__ rec, int2* __restrict__ A,
-                            int2* __restrict__ P, const Scalars* sc) {
-  const int c2 = 2 * sc->ncomp;
+__global__ void k_positions(const int* __restrict__ comp, const int2* __restrict__ fe,
+                            const int4* __restrict__ own0, const int* __restrict__ offs1, int n,
+                            int4* __restrict__ rec, int2* __restrict__ A, int2* __restrict__ P) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    int4 o = __ldg(own0 + x);  // (seg, off) of elements 2x and 2x+1
+    int r0 = __ldg(offs1 + o.x) + o.y;
+    int r1 = __ldg(offs1 + o.z) + o.w;
     if (__ldg(comp + x) == x) {
-      int ri = __ldg(rootidx + x);
-      int2 o1 = own0[2 * ri], o2 = own0[2 * ri + 1];
-      place(x, __ldg(offs1 + o1.x) + o1.y, __ldg(offs1 + o2.x) + o2.y, -1, rec, A, P);
+      place(x, r0, r1, -1, rec, A, P);  // enter(x), exit(x)
     } else {
-      int4 e = ex[x];
-      int2 ou = own0[c2 + e.z], ov = own0[c2 + e.w];
-      int ru = __ldg(offs1 + ou.x) + ou.y;
-      int rv = __ldg(offs1 + ov.x) + ov.y;
-      if (ru < rv) place(e.y, ru, rv, e.x, rec, A, P);  // u -> v is the down arc
-      else place(e.x, rv, ru, e.y, rec, A, P);
+      int2 uv = __ldg(fe + x);
+      if (r0 < r1) place(uv.y, r0, r1, uv.x, rec, A, P);  // u -> v is the down arc
+      else place(uv.x, r1, r0, uv.y, rec, A, P);
     }
   }
 }
@@ -253,26 +232,21 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
   const int n = g.n;
   const int B = 256;
   const int gv = grid_for(n + 1, B);
-  // roots: rank among roots (ri) and c
-  k_root_flags<<<gv, B, 0, st>>>(comp, n, R.rootidx + (n + 1));  // flags staged after rootidx
+  // roots in id order: rank among roots, and the inverse list
+  k_root_flags<<<gv, B, 0, st>>>(comp, n, R.flags);
   note(K_ROOT_FLAGS);
-  exclusive_scan(R.rootidx + (n + 1), R.rootidx, n + 1, R.cub_tmp, R.cub_bytes, st);
+  exclusive_scan(R.flags, R.rootidx, n + 1, R.cub_tmp, R.cub_bytes, st);
   note(K_SCAN);
-  // tree CSR
-  cudaMemsetAsync(R.tdeg, 0, sizeof(int) * (n + 1), st);
+  k_root_list<<<gv, B, 0, st>>>(comp, R.rootidx, n, R.rlist, sc);
+  note(K_ROOT_LIST);
+  // Euler circuit
+  cudaMemsetAsync(R.lhead, 0xFF, sizeof(int) * n, st);
   note(K_MEMSET);
-  k_tree_degree<<<gv, B, 0, st>>>(comp, fe, n, R.tdeg, R.ex, R.rootidx, sc);
+  k_out_lists<<<gv, B, 0, st>>>(comp, fe, n, R.lhead, R.nexto);
   note(K_TREE_DEGREE);
-  int* toff = R.tdeg + (n + 1);
-  exclusive_scan(R.tdeg, toff, n + 1, R.cub_tmp, R.cub_bytes, st);
-  note(K_SCAN);
-  k_tree_scatter<<<gv, B, 0, st>>>(comp, n, toff, R.ex, R.tedges, R.twin);
-  note(K_TREE_SCATTER);
-  // unified list
-  k_link_slots<<<grid_for(2 * (int64_t)n, B), B, 0, st>>>(comp, toff, R.tedges, R.twin, R.rootidx, n, R.nxt, sc);
+  k_link_tour<<<grid_for(2 * (int64_t)n, B), B, 0, st>>>(comp, fe, R.lhead, R.nexto, R.rootidx, R.rlist, n, R.nxt,
+                                                         sc);
   note(K_LINK_SLOTS);
-  k_link_roots<<<gv, B, 0, st>>>(comp, toff, R.rootidx, n, R.nxt, sc);
-  note(K_LINK_ROOTS);
   // ruling-set levels
   const int64_t N0 = 2 * (int64_t)n;
   k_walk<false><<<grid_for(R.K[1], B, 64), B, 0, st>>>(R.K[1], R.S[0], N0, R.nxt, nullptr, R.own0,
@@ -283,13 +257,15 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
                                                             R.own[l], R.succ[l + 1], R.wgt[l + 1]);
     note(K_WALKL);
   }
-  k_final_rank<<<1, 1024, 0, st>>>((int)R.K[R.nlev], R.succ[R.nlev], R.wgt[R.nlev], R.offs[R.nlev]);
+  cudaFuncSetAttribute(k_final_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinalSmem);
+  k_final_rank<<<1, kFinalThreads, kFinalSmem, st>>>((int)R.K[R.nlev], R.succ[R.nlev], R.wgt[R.nlev],
+                                                      R.offs[R.nlev]);
   note(K_FINAL_RANK);
   for (int l = R.nlev - 1; l >= 1; l--) {
     k_expand<<<grid_for(R.K[l], B), B, 0, st>>>(R.K[l], R.own[l], R.offs[l + 1], R.offs[l]);
     note(K_EXPAND);
   }
-  k_positions<<<gv, B, 0, st>>>(comp, R.ex, R.rootidx, R.own0, R.offs[1], n, R.rec, A, P, sc);
+  k_positions<<<gv, B, 0, st>>>(comp, fe, reinterpret_cast<const int4*>(R.own0), R.offs[1], n, R.rec, A, P);
   note(K_POSITIONS);
 }
 

@@ -42,6 +42,8 @@ def _sha(a):
 
 @pytest.mark.parametrize("name", ["4c", "4a", "4b", "5"])
 def test_large_config(name, oracle_mod):
+    if name not in os.environ.get("FBCC_LARGE_CONFIGS", "4c,4a,4b,5").split(","):
+        pytest.skip("not selected by FBCC_LARGE_CONFIGS")
     import workloads
     from paper_2301_01356_b200.bcc import Plan
 

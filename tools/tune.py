@@ -24,9 +24,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--raw", action="store_true")
     a = ap.parse_args()
-    g = workloads.make(a.config)
-    off = torch.from_numpy(g.offsets).cuda()
-    adj = torch.from_numpy(g.edges.view(np.int32)).cuda()
+    off, adj = workloads.make_device(a.config)
     defaults = {k: _lib.get_option(k) for k in _lib.OPTIONS}
     for var in (a.variant or [""]):
         for k, v in defaults.items():
