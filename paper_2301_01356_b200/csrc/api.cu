@@ -30,7 +30,7 @@ constexpr int kFinalMaxHost = kFinalMax;
 
 struct Layout {
   size_t total = 0;
-  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, nexto, nxt, own0, rec, A, P, lh1, lh2, table, cnt, uoff,
+  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
       nlow, bmin, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
@@ -74,6 +74,7 @@ struct Layout {
     nexto = take(4 * N0);
     nxt = take(4 * N0);
     own0 = take(8 * N0);
+    rank0 = take(4 * N0);
     for (int l = 1; l <= nlev; l++) {
       lsucc[l] = take(4 * K[l]);
       lwgt[l] = take(4 * K[l]);
@@ -81,8 +82,7 @@ struct Layout {
       loffs[l] = take(4 * K[l]);
     }
     rec = take(16 * n);
-    A = take(8 * (size_t)ntile * kTile);
-    P = take(8 * (size_t)ntile * kTile);
+    AP = take(16 * (size_t)ntile * kTile);
     lh1 = take(8 * n);
     lh2 = take(8 * n);
     table = take(8 * (size_t)ntile * tlev);
@@ -128,6 +128,7 @@ struct Pipeline {
     R.nexto = (int*)at(lay.nexto);
     R.nxt = (int*)at(lay.nxt);
     R.own0 = (int2*)at(lay.own0);
+    R.rank0 = (int*)at(lay.rank0);
     R.nlev = lay.nlev;
     for (int l = 0; l < 8; l++) {
       R.K[l] = lay.K[l];
@@ -146,8 +147,7 @@ struct Pipeline {
     R.rec = (int4*)at(lay.rec);
     R.cub_tmp = at(lay.cub);
     R.cub_bytes = lay.cub_bytes;
-    T.A = (int2*)at(lay.A);
-    T.P = (int2*)at(lay.P);
+    T.AP = (int4*)at(lay.AP);
     T.lh1 = (int2*)at(lay.lh1);
     T.lh2 = (int2*)at(lay.lh2);
     T.table = (int2*)at(lay.table);
@@ -173,7 +173,7 @@ struct Pipeline {
     build_chunk_rows(g, const_cast<int*>(g.crow), st);
     stage1_forest(g, comp, fe, prop, sc, st);
     mark(1);
-    stage2_rooting(g, comp, fe, R, T.A, T.P, sc, st);
+    stage2_rooting(g, comp, fe, R, T.AP, sc, st);
     mark(2);
     stage3_tags(g, R, T, st);
     mark(3);
@@ -297,7 +297,7 @@ int fbcc_run(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m
   g_log = nullptr;
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && dbg)
-    export_debug(P.g, P.fe, P.R.rec, P.T.A, dbg->forest, dbg->parent, dbg->first, dbg->last, dbg->w1, dbg->w2,
+    export_debug(P.g, P.fe, P.R.rec, P.T.AP, dbg->forest, dbg->parent, dbg->first, dbg->last, dbg->w1, dbg->w2,
                  dbg->fence, st);
   Scalars host;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&host, P.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st);

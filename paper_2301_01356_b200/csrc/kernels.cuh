@@ -29,6 +29,7 @@ struct Rooting {
   int* nexto;      // [2n]  next out-arc of the same vertex
   int* nxt;        // [2n]  unified tour list successor
   int2* own0;      // [2n]  (segment, offset) per list element
+  int* rank0;      // [2n]  tour position of each list element
   // ruling-set levels 1..nlev: element counts and arrays
   int nlev;
   int64_t K[8];
@@ -43,8 +44,8 @@ struct Rooting {
 };
 
 struct Tags {
-  int2* A;         // [ntile*TILE] (w1, w2) at first[v], filler at last[v]
-  int2* P;         // [ntile*TILE] {v or ~v, partner position}
+  int4* AP;        // [ntile*TILE] per tour position: {w1, w2, v or ~v, partner position};
+                   // (w1, w2) at first[v], filler at last[v]
   int2* lh1;       // [n] in-tile result / suffix partial
   int2* lh2;       // [n] prefix partial
   int2* table;     // [tlev * ntile] sparse table over tile extremes
@@ -55,7 +56,7 @@ struct Tags {
 constexpr int kTile = 4096;      // tour positions per tile in the low/high pass
 
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st);
-void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int2* A, int2* P,
+void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
                     Scalars* sc, cudaStream_t st);
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st);
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out,
@@ -65,7 +66,7 @@ void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned lo
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
                       size_t cub_bytes, Scalars* sc, cudaStream_t st);
-void export_debug(const Graph& g, const int2* fe, const int4* rec, const int2* A, int* forest,
+void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* AP, int* forest,
                   int* parent, int* first, int* last, int* w1, int* w2, uint8_t* fence,
                   cudaStream_t st);
 

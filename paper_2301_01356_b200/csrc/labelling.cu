@@ -174,7 +174,7 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
 // ---------------------------------------------------------------------------
 // intermediate exports (parity rungs 1-4)
 // ---------------------------------------------------------------------------
-__global__ void k_export(int n, const int4* __restrict__ rec, const int2* __restrict__ A, int* parent, int* first,
+__global__ void k_export(int n, const int4* __restrict__ rec, const int4* __restrict__ AP, int* parent, int* first,
                          int* last, int* w1, int* w2, uint8_t* fence) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
@@ -183,18 +183,18 @@ __global__ void k_export(int n, const int4* __restrict__ rec, const int2* __rest
     if (last) last[v] = r.y;
     if (fence) fence[v] = (uint8_t)r.w;
     if (w1 || w2) {
-      int2 a = A[r.x];
+      int4 a = AP[r.x];
       if (w1) w1[v] = a.x;
       if (w2) w2[v] = a.y;
     }
   }
 }
 
-void export_debug(const Graph& g, const int2* fe, const int4* rec, const int2* A, int* forest, int* parent,
+void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* AP, int* forest, int* parent,
                   int* first, int* last, int* w1, int* w2, uint8_t* fence, cudaStream_t st) {
   if (forest) cudaMemcpyAsync(forest, fe, sizeof(int2) * g.n, cudaMemcpyDeviceToDevice, st);
   if (parent || first || last || w1 || w2 || fence)
-    k_export<<<grid_for(g.n, 256), 256, 0, st>>>(g.n, rec, A, parent, first, last, w1, w2, fence);
+    k_export<<<grid_for(g.n, 256), 256, 0, st>>>(g.n, rec, AP, parent, first, last, w1, w2, fence);
 }
 
 }  // namespace fbcc

@@ -28,13 +28,13 @@
 //    a chain's return path, which touches every other id, are still cut);
 //    each splitter walks to the next writing (segment, offset) per element;
 //    recurse on the weighted splitter list until it fits one CTA (Wyllie
-//    pointer jumping in shared memory).  Level-0 ranks are never
-//    materialised: rank(e) = offs1[own0[e].seg] + own0[e].off.
-//  * Positions: one thread per vertex x reads own0[2x..2x+1] as ONE 16-byte
+//    pointer jumping in shared memory).  Level-0 ranks are expanded in one
+//    coalesced pass: rank(e) = offs1[own0[e].seg] + own0[e].off.
+//  * Positions: one thread per vertex x reads rank[2x..2x+1] as ONE 8-byte
 //    load; the earlier of the two arcs is the down arc, giving the child's
-//    parent, first and last.  It also initialises the tour-indexed arrays the
-//    tag stage reads (A: (first, first) at entry, filler at exit; P: vertex
-//    id + partner position).
+//    parent, first and last.  It also initialises the tour-indexed array the
+//    tag stage reads, one 16-byte record per position (AP: (first, first) at
+//    entry, filler at exit; vertex id + partner position).
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
@@ -202,32 +202,40 @@ __global__ void k_expand(int64_t K, const int2* __restrict__ own, const int* __r
 // ---------------------------------------------------------------------------
 // positions: parent / first / last + tour-indexed tag arrays
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void place(int v, int f, int l, int par, int4* rec, int2* A, int2* P) {
+// AP[first] = {first, first (w1 = w2 = own entry, gathered into by stage 3), v, last};
+// AP[last] = {filler (tagging.py:33-39), ~v, first}: two 16 B stores per vertex
+__device__ __forceinline__ void place(int v, int f, int l, int par, int4* rec, int4* AP) {
   rec[v] = make_int4(f, l, par, 0);
-  A[f] = make_int2(f, f);      // w1 = w2 = own entry position, gathered into by stage 3
-  A[l] = make_int2(kINF, -1);  // neutral filler (tagging.py:33-39)
-  P[f] = make_int2(v, l);
-  P[l] = make_int2(~v, f);
+  AP[f] = make_int4(f, f, v, l);
+  AP[l] = make_int4(kINF, -1, ~v, f);
+}
+
+// level-0 ranks, coalesced over elements (the offs1 gathers hit L2 here,
+// instead of competing with the positions kernel's scattered stores)
+__global__ void k_rank0(int64_t N, const int2* __restrict__ own0, const int* __restrict__ offs1,
+                        int* __restrict__ rank0) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+    int2 o = __ldg(own0 + e);
+    rank0[e] = __ldg(offs1 + o.x) + o.y;
+  }
 }
 
 __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict__ fe,
-                            const int4* __restrict__ own0, const int* __restrict__ offs1, int n,
-                            int4* __restrict__ rec, int2* __restrict__ A, int2* __restrict__ P) {
+                            const int2* __restrict__ rank0, int n, int4* __restrict__ rec,
+                            int4* __restrict__ AP) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-    int4 o = __ldg(own0 + x);  // (seg, off) of elements 2x and 2x+1
-    int r0 = __ldg(offs1 + o.x) + o.y;
-    int r1 = __ldg(offs1 + o.z) + o.w;
+    int2 r = __ldg(rank0 + x);  // ranks of elements 2x and 2x+1, one 8-byte load
     if (__ldg(comp + x) == x) {
-      place(x, r0, r1, -1, rec, A, P);  // enter(x), exit(x)
+      place(x, r.x, r.y, -1, rec, AP);  // enter(x), exit(x)
     } else {
       int2 uv = __ldg(fe + x);
-      if (r0 < r1) place(uv.y, r0, r1, uv.x, rec, A, P);  // u -> v is the down arc
-      else place(uv.x, r1, r0, uv.y, rec, A, P);
+      if (r.x < r.y) place(uv.y, r.x, r.y, uv.x, rec, AP);  // u -> v is the down arc
+      else place(uv.x, r.y, r.x, uv.y, rec, AP);
     }
   }
 }
 
-void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int2* A, int2* P,
+void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
                     Scalars* sc, cudaStream_t st) {
   const int n = g.n;
   const int B = 256;
@@ -265,7 +273,9 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
     k_expand<<<grid_for(R.K[l], B), B, 0, st>>>(R.K[l], R.own[l], R.offs[l + 1], R.offs[l]);
     note(K_EXPAND);
   }
-  k_positions<<<gv, B, 0, st>>>(comp, fe, reinterpret_cast<const int4*>(R.own0), R.offs[1], n, R.rec, A, P);
+  k_rank0<<<grid_for(N0, B), B, 0, st>>>(N0, R.own0, R.offs[1], R.rank0);
+  note(K_EXPAND);
+  k_positions<<<gv, B, 0, st>>>(comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP);
   note(K_POSITIONS);
 }
 

@@ -38,7 +38,7 @@ __device__ __forceinline__ int2 filler() { return make_int2(kINF, -1); }
 // ---------------------------------------------------------------------------
 struct WGatherVisitor {
   const int4* rec;
-  int2* A;
+  int4* AP;
   int fv, pv, m1, m2;
   __device__ __forceinline__ void begin(int v, int64_t, int64_t) {
     int4 r = __ldg(rec + v);
@@ -56,19 +56,19 @@ struct WGatherVisitor {
   }
   __device__ __forceinline__ void end(int, bool whole) {
     if (whole) {
-      A[fv] = make_int2(min(fv, m1), max(fv, m2));
+      *reinterpret_cast<int2*>(AP + fv) = make_int2(min(fv, m1), max(fv, m2));
     } else if (m2 >= 0) {
-      atomicMin(&A[fv].x, m1);
-      atomicMax(&A[fv].y, m2);
+      atomicMin(&AP[fv].x, m1);
+      atomicMax(&AP[fv].y, m2);
     }
   }
 };
 
 __global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
-                                                  int n, int64_t m, const int4* __restrict__ rec, int2* A) {
+                                                  int n, int64_t m, const int4* __restrict__ rec, int4* AP) {
   WGatherVisitor vis;
   vis.rec = rec;
-  vis.A = A;
+  vis.AP = AP;
   visit_arc_chunks(off, adj, crow, n, m, vis);
 }
 
@@ -115,7 +115,7 @@ struct TileSmem {
   }
 };
 
-__global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int2* __restrict__ A, const int2* __restrict__ P,
+__global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int4* __restrict__ AP,
                                                           int64_t N, int ntile, int2* __restrict__ lh1,
                                                           int2* __restrict__ lh2, int2* __restrict__ table0) {
   extern __shared__ int2 smem[];
@@ -131,7 +131,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int2* __restrict
     // 1. stage the tile; warp scans per 32-position sub-block
     for (int sb = warp; sb < kNSub; sb += kTileThreads / 32) {
       int p = sb * kSub + lane;
-      int2 x = (base + p < N) ? __ldg(A + base + p) : filler();
+      int2 x = filler();
+      if (base + p < N) {
+        int4 ap = __ldg(AP + base + p);
+        x = make_int2(ap.x, ap.y);
+      }
       S.raw[p] = x;
       int2 pr = x, su = x;
 #pragma unroll
@@ -160,7 +164,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int2* __restrict
     for (int p = threadIdx.x; p < kTile; p += kTileThreads) {
       int64_t gp = base + p;
       if (gp >= N) break;
-      int2 q = __ldg(P + gp);
+      int4 ap = __ldg(AP + gp);  // L1 hit: the tile was just staged
+      int2 q = make_int2(ap.z, ap.w);
       if (q.x >= 0) {  // entry position of v = q.x; partner = last[v]
         int64_t rel = (int64_t)q.y - base;
         lh1[q.x] = (rel < kTile) ? S.range(p, (int)rel) : S.to_end(p);
@@ -186,11 +191,11 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st) {
   const int B = 256;
   int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (g.m > 0) {
-    k_w_gather<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, R.rec, T.A);
+    k_w_gather<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, R.rec, T.AP);
     note(K_W_GATHER);
   }
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-  k_tile<<<grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st>>>(T.A, T.P, 2 * (int64_t)g.n, T.ntile, T.lh1,
+  k_tile<<<grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st>>>(T.AP, 2 * (int64_t)g.n, T.ntile, T.lh1,
                                                                   T.lh2, T.table);
   note(K_TILE);
   for (int k = 1; k < T.tlev; k++) {
