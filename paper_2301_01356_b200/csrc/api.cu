@@ -25,7 +25,8 @@ static int cuda_fail(cudaError_t e, const char* where) {
 }
 
 int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*halving*/ 1, /*S0*/ 16, /*SL*/ 8,
-                      /*full-link rounds mask*/ 0, /*sample mode: propose/accept*/ 0};
+                      /*full-link rounds mask*/ 0, /*sample mode: propose/accept*/ 0,
+                      /*link mode: row-filtered*/ 0, /*compress after rounds mask: 0 = first+last*/ 0};
 constexpr int kFinalMaxHost = kFinalMax;
 
 struct Layout {

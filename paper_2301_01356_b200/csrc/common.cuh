@@ -19,7 +19,8 @@ struct Scalars {
   int err;         // error bits
   int num_edges;   // E
   int nroots[16];  // roots after each sampling round's compress (stage 1: 0..7, stage 5: 8..15)
-  int pad[43];
+  int hooks[16];   // hooks accepted per sampling round (same split)
+  int pad[27];
 };
 
 // ---------------------------------------------------------------------------
@@ -69,6 +70,8 @@ enum Option : int {
   OPT_SL = 4,             // spacing on higher ranking levels (power of two)
   OPT_SAMPLE_FULL = 5,    // CAS mode: bitmask of sampling rounds that climb (exact Afforest link)
   OPT_SAMPLE_MODE = 6,    // 0: propose/accept rounds, 1: CAS rounds
+  OPT_LINK_MODE = 7,      // remaining arcs: 0 row-filtered warps, 1 arc-balanced chunks
+  OPT_COMPRESS_MASK = 8,  // bitmask: sampling rounds followed by a compress (bit 0 always honoured)
   OPT_NUM = 16
 };
 extern int g_opt[OPT_NUM];

@@ -160,24 +160,29 @@ constexpr int kPerRoot = 32;
 
 template <bool kSkel>
 __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round,
-                          const int* __restrict__ comp, unsigned long long* prop, const int4* __restrict__ rec,
-                          const int* __restrict__ nroots_prev) {
-  // participate iff hash < thr / 2^24, thr = min(1, kPerRoot * roots / n)
+                          int* comp, unsigned long long* prop, const int4* __restrict__ rec,
+                          const int* __restrict__ nroots, const int* __restrict__ hooks, bool flat) {
+  // participate iff hash < thr / 2^24, thr = min(1, kPerRoot * roots / n);
+  // roots at round start = roots counted after round 0 minus later hooks
   uint32_t thr = 1u << 24;
-  if (nroots_prev) {
-    uint64_t t = ((uint64_t)kPerRoot * (uint64_t)(*nroots_prev) << 24) / (uint64_t)n;
+  if (round > 0) {
+    int64_t R = nroots[0];
+    for (int i = 1; i < round; i++) R -= hooks[i];
+    uint64_t t = ((uint64_t)kPerRoot * (uint64_t)(R > 0 ? R : 0) << 24) / (uint64_t)n;
     if (t < thr) thr = (uint32_t)t;
   }
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     if (thr < (1u << 24) && (hash32((uint32_t)v * 0x9E3779B1u + (uint32_t)round) >> 8) >= thr) continue;
-    int ru = __ldg(comp + v);
     int64_t s = __ldg(off + v) + round;
     if (s >= __ldg(off + v + 1)) continue;
     int w = (int)__ldg(adj + s);
     if (kSkel) {
       if (!skel_keep(v, __ldg(rec + v), w, __ldg(rec + w))) continue;
     }
-    int rw = __ldg(comp + w);
+    // flat after a compress; otherwise (rounds >= 1 hook root -> root only,
+    // so trees stay shallow) find with halving
+    int ru = flat ? ldp(comp + v) : find_halve(comp, v, true);
+    int rw = flat ? ldp(comp + w) : find_halve(comp, w, true);
     if (ru == rw) continue;
     int hi = ru > rw ? ru : rw;
     int lo = ru + rw - hi;
@@ -192,18 +197,21 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
 
 template <bool kRecord>
 __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
-                         unsigned long long* prop, int2* fe) {
+                         unsigned long long* prop, int2* fe, int* hooks) {
+  int hooked = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     unsigned long long key = prop[v];
     if (key == ~0ull) continue;
     prop[v] = ~0ull;  // ready for the next round
     int lo = (int)(key >> 32);
     comp[v] = lo;     // v is a round-start root (only roots receive proposals)
+    hooked++;
     if (kRecord) {
       int u = (int)(key & 0xffffffffull);
       fe[v] = make_int2(u, (int)__ldg(adj + __ldg(off + u) + round));
     }
   }
+  block_count_add(hooks + round, hooked);
 }
 
 // pointer jumping to the root (the root is the component minimum)
@@ -244,7 +252,8 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, b
   for (int i = t; i < H; i += 1024) { key[i] = -1; num[i] = 0; }
   __syncthreads();
   int v = (int)(hash32(0x9E3779B9u * (uint32_t)(t + 1)) % (uint32_t)n);
-  int mine = comp[v];
+  int mine = comp[v];  // comp may not be flat here: climb to the root
+  for (int up = comp[mine]; up != mine; up = comp[mine]) mine = up;
   int slot = hash32((uint32_t)mine) & (H - 1);
   while (true) {
     int k = atomicCAS(&key[slot], -1, mine);
@@ -286,7 +295,8 @@ struct LinkRestVisitor {
   int4 rv;
   __device__ __forceinline__ void begin(int v, int64_t s, int64_t e) {
     rs = s;
-    skip = ldp(comp + v) == giant;
+    int p = ldp(comp + v);
+    skip = p == giant || ldp(comp + p) == giant;  // sound: giant is an ancestor
     if (kSkel && !skip) rv = __ldg(rec + v);
   }
   __device__ __forceinline__ void arc(int v, int64_t a, int w) {
@@ -314,6 +324,56 @@ __global__ void __launch_bounds__(256) k_link_rest(const int64_t* __restrict__ o
   visit_arc_chunks(off, adj, crow, n, m, vis);
 }
 
+// Remaining arcs, row-filtered: each warp takes 32 consecutive rows and drops
+// the ones already in the sampled giant before touching their adjacency
+// (after the sampling rounds that is almost every row of a low-diameter
+// graph, so the 4m bytes of targets are mostly never read).  Rows of <= 32
+// arcs are linked by their own lane; longer rows are linked by the whole warp
+// striding over the arcs (a non-giant hub cannot serialise one thread).
+template <bool kSkel, bool kRecord>
+__global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                   int n, int* comp, int2* fe, const int4* __restrict__ rec,
+                                                   const Scalars* sc, bool halve) {
+  const int giant = sc->giant;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n; base += warps * 32) {
+    const int v = (int)base + lane;
+    int64_t rs = 0, re = 0;
+    int p = v < n ? ldp(comp + v) : giant;
+    // skip rows whose parent or grandparent is the giant root (sound: an
+    // ancestor; comp need not be flat after the last sampling round)
+    if (p != giant && ldp(comp + p) != giant) {
+      rs = __ldg(off + v);
+      re = __ldg(off + v + 1);
+    }
+    const bool heavy = re - rs > 32;
+    if (!heavy && re > rs) {
+      int4 rv;
+      if (kSkel) rv = __ldg(rec + v);
+      for (int64_t a = rs; a < re; a++) {
+        int w = (int)__ldg(adj + a);
+        if (kSkel && !skel_keep(v, rv, w, __ldg(rec + w))) continue;
+        link<kRecord>(v, w, comp, fe, halve);
+      }
+    }
+    unsigned hb = __ballot_sync(0xffffffffu, heavy);
+    while (hb) {
+      const int src = __ffs(hb) - 1;
+      hb &= hb - 1;
+      const int hv = __shfl_sync(0xffffffffu, v, src);
+      const int64_t hs = __shfl_sync(0xffffffffu, rs, src), he = __shfl_sync(0xffffffffu, re, src);
+      int4 rv;
+      if (kSkel) rv = __ldg(rec + hv);
+      for (int64_t a = hs + lane; a < he; a += 32) {
+        int w = (int)__ldg(adj + a);
+        if (kSkel && !skel_keep(hv, rv, w, __ldg(rec + w))) continue;
+        link<kRecord>(hv, w, comp, fe, halve);
+      }
+    }
+  }
+}
+
 // Afforest schedule shared by Stage 1 (kSkel=false, record forest) and
 // Stage 5 (kSkel=true, no forest).
 template <bool kSkel, bool kRecord>
@@ -324,6 +384,12 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   const bool halve = g_opt[OPT_FIND_HALVING] != 0;
   const bool propose = g_opt[OPT_SAMPLE_MODE] == 0;
   int* nroots = sc->nroots + (kSkel ? 8 : 0);  // device addresses (sc is a device pointer)
+  int* hooks = sc->hooks + (kSkel ? 8 : 0);
+  // compress after round 0 (flattens the deep min-neighbour forest) and after
+  // the last round (k_link_rows' giant test wants a flat array); rounds in
+  // between only hook roots under roots and their proposers find() instead
+  int cmask = g_opt[OPT_COMPRESS_MASK];
+  if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
   int gv = grid_for(g.n, B);
   // k_compress relies on concurrent threads advancing each other's pointers:
   // its grid must be fully resident (2048 threads/SM), or grid-stride
@@ -336,26 +402,36 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     note(K_MEMSET);
   }
   for (int r = 0; r < kRounds; r++) {
+    const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
     if (propose) {
-      k_propose<kSkel><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, rec,
-                                          r > 0 ? nroots + r - 1 : nullptr);
+      k_propose<kSkel><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, rec, nroots, hooks, flat);
       note(K_SAMPLE_LINK);
-      k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, fe);
+      k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, fe, hooks);
       note(K_ACCEPT);
     } else {
       k_sample_link<kSkel, kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, fe, rec,
                                                       (g_opt[OPT_SAMPLE_FULL] >> r) & 1, halve);
       note(K_SAMPLE_LINK);
     }
-    k_compress<<<gres, B, 0, st>>>(comp, g.n, r < 8 ? nroots + r : nullptr);
-    note(K_COMPRESS);
+    // round 0 hooks every vertex to its smallest neighbour (deep trees: a
+    // path becomes one chain) and must be flattened; later rounds hook roots
+    // under roots, and their proposers find() through the shallow result
+    if (((cmask >> r) & 1) || !propose) {
+      k_compress<<<gres, B, 0, st>>>(comp, g.n, r == 0 ? nroots : nullptr);
+      note(K_COMPRESS);
+    }
   }
   k_find_giant<<<1, 1024, 0, st>>>(comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
   note(K_FIND_GIANT);
-  int64_t nchunks = (g.m + kItems - 1) / kItems;
-  if (nchunks > 0) {
-    int ga = grid_for(nchunks, B, 32);
-    k_link_rest<kSkel, kRecord><<<ga, B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, /*skip arcs below*/ 0, comp, fe, rec, sc, halve);
+  if (g.m > 0) {
+    if (g_opt[OPT_LINK_MODE] == 0) {
+      k_link_rows<kSkel, kRecord><<<grid_for(g.n, B, 32), B, 0, st>>>(g.off, g.adj, g.n, comp, fe, rec, sc, halve);
+    } else {
+      int64_t nchunks = (g.m + kItems - 1) / kItems;
+      k_link_rest<kSkel, kRecord><<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m,
+                                                                            /*skip arcs below*/ 0, comp, fe, rec,
+                                                                            sc, halve);
+    }
     note(K_LINK_REST);
   }
   k_compress<<<gres, B, 0, st>>>(comp, g.n, nullptr);

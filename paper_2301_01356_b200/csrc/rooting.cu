@@ -145,50 +145,68 @@ __global__ void __launch_bounds__(256) k_walk(int64_t K, int S, int64_t N, const
 }
 
 // Final level: <= kFinalMax elements, head = element 0; exclusive weighted
-// prefix along the list by Wyllie pointer jumping over predecessor links,
-// entirely in shared memory (one CTA, 2 x 64 KB).
+// prefix along the list, entirely in shared memory (one CTA).
+// The CTA runs one more ruling-set level in shared memory (one walker per
+// thread over windows of Q = K/1024 elements, ~2 us of smem steps), then
+// Wyllie over the <= 1024 walkers (10 rounds, one element per thread), then
+// expands.  Block-wide Wyllie straight over 16K elements needed 14 rounds of
+// 16 elements per thread (59 us measured).
 constexpr int kFinalThreads = 1024;
-constexpr size_t kFinalSmem = 2 * sizeof(int) * kFinalMax;
+constexpr size_t kFinalSmem = 2 * sizeof(int) * kFinalMax + 4 * sizeof(int) * kFinalThreads;
 
 __global__ void __launch_bounds__(kFinalThreads) k_final_rank(int K, const int* __restrict__ succ,
                                                               const int* __restrict__ w, int* __restrict__ offs) {
   extern __shared__ int fsm[];
-  int* P = fsm;
-  int* V = fsm + kFinalMax;
+  int* S = fsm;                    // succ, then owner walker
+  int* W = fsm + kFinalMax;        // weight, then offset inside the walker's segment
+  int* SS = W + kFinalMax;         // walker -> next walker
+  int* WS = SS + kFinalThreads;    // walker segment weight
+  int* PS = WS + kFinalThreads;    // walker predecessor
+  int* VS = PS + kFinalThreads;    // walker exclusive prefix
   const int t = threadIdx.x;
-  for (int j = t; j < K; j += kFinalThreads) P[j] = -1;
-  __syncthreads();
   for (int j = t; j < K; j += kFinalThreads) {
-    int s = succ[j];
-    if (s >= 0) P[s] = j;
+    S[j] = succ[j];
+    W[j] = w[j];
+  }
+  int Q = 1;
+  while (Q * kFinalThreads < K) Q <<= 1;
+  const int nwin = (K + Q - 1) / Q;
+  PS[t] = -1;
+  __syncthreads();
+  if (t < nwin) {
+    int e = (int)split_elem(t, Q, K);
+    int acc = 0, nj = -1;
+    while (true) {
+      int s = S[e], wt = W[e];
+      S[e] = t;
+      W[e] = acc;
+      acc += wt;
+      if (s < 0) break;
+      int j2 = s / Q;
+      if ((int)split_elem(j2, Q, K) == s) { nj = j2; break; }
+      e = s;
+    }
+    SS[t] = nj;
+    WS[t] = acc;
   }
   __syncthreads();
-  for (int j = t; j < K; j += kFinalThreads) V[j] = P[j] >= 0 ? w[P[j]] : 0;
+  if (t < nwin && SS[t] >= 0) PS[SS[t]] = t;
   __syncthreads();
-  constexpr int PER = kFinalMax / kFinalThreads;
-  for (int round = 0; round < 32; round++) {
-    int np[PER], nv[PER];
-    int active = 0;
-#pragma unroll
-    for (int q = 0; q < PER; q++) {
-      int j = t + q * kFinalThreads;
-      np[q] = -1;
-      nv[q] = 0;
-      if (j < K) {
-        int p = P[j];
-        nv[q] = V[j];
-        if (p >= 0) { nv[q] += V[p]; np[q] = P[p]; active = 1; }
-      }
-    }
-    if (!__syncthreads_or(active)) break;
-#pragma unroll
-    for (int q = 0; q < PER; q++) {
-      int j = t + q * kFinalThreads;
-      if (j < K) { P[j] = np[q]; V[j] = nv[q]; }
-    }
+  int p = PS[t];
+  int v = (t < nwin && p >= 0) ? WS[p] : 0;
+  VS[t] = v;
+  __syncthreads();
+  for (int round = 0; round < 11; round++) {
+    int np = p, nv = v;
+    if (p >= 0) { nv = v + VS[p]; np = PS[p]; }
+    if (!__syncthreads_or(p >= 0)) break;
+    p = np;
+    v = nv;
+    PS[t] = p;
+    VS[t] = v;
     __syncthreads();
   }
-  for (int j = t; j < K; j += kFinalThreads) offs[j] = V[j];
+  for (int j = t; j < K; j += kFinalThreads) offs[j] = VS[S[j]] + W[j];
 }
 
 __global__ void k_expand(int64_t K, const int2* __restrict__ own, const int* __restrict__ offs_up,
