@@ -268,7 +268,8 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e: public API, pinned host CSR in, results out -----------------
     gp = Graph(g.offsets, g.edges)
     gp._pinned = (torch.from_numpy(g.offsets).pin_memory(), torch.from_numpy(g.edges.view(np.int32)).pin_memory())
-    fast_bcc(gp, device=dev)
+    for _ in range(max(args.warmup, 3)):  # >= 2 live result sets before the pinned cache is warm
+        lab = fast_bcc(gp, device=dev)
     torch.cuda.synchronize()
     e2e_s = []
     for _ in range(args.steps):

@@ -178,7 +178,7 @@ struct Pipeline {
     mark(2);
     stage3_tags(g, R, T, st);
     mark(3);
-    stage4_fence(g, R, T, low_out, high_out, st);
+    stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st);
     mark(4);
     stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st);
     mark(5);

@@ -103,8 +103,12 @@ void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st) {
   note(K_CHUNK_ROWS);
 }
 
-__global__ void k_iota(int* __restrict__ comp, int n) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) comp[v] = v;
+// comp = identity; also resets the proposal words (one pass, no memset node)
+__global__ void k_iota(int* __restrict__ comp, int n, unsigned long long* __restrict__ prop) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    comp[v] = v;
+    if (prop) prop[v] = ~0ull;
+  }
 }
 
 // Best-effort sampling round: one CAS attempt on the (post-compress, hence
@@ -395,12 +399,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   // its grid must be fully resident (2048 threads/SM), or grid-stride
   // threads chase pointers owned by blocks that cannot be scheduled yet
   const int gres = grid_for(g.n, B, 2048 / B);
-  k_iota<<<gv, B, 0, st>>>(comp, g.n);
+  k_iota<<<gv, B, 0, st>>>(comp, g.n, propose && kRounds > 0 ? prop : nullptr);
   note(K_IOTA);
-  if (propose && kRounds > 0) {
-    cudaMemsetAsync(prop, 0xFF, sizeof(unsigned long long) * g.n, st);
-    note(K_MEMSET);
-  }
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
     if (propose) {

@@ -59,7 +59,8 @@ void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop
 void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
                     Scalars* sc, cudaStream_t st);
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st);
-void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out,
+void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
+                  int* bmin,
                   cudaStream_t st);
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
                         cudaStream_t st);

@@ -140,9 +140,7 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   const int n = g.n;
   const int B = 256;
   const int gv = grid_for(n + 1, B);
-  cudaMemsetAsync(head, 0xFF, sizeof(int) * n, st);
-  cudaMemsetAsync(cnt, 0, sizeof(int) * n, st);
-  note(K_MEMSET);
+  // head = -1, cnt = 0, bmin = INF were initialised by the stage-4 kernel
   k_heads<<<gv, B, 0, st>>>(n, rec, label, head);
   note(K_HEADS);
   k_count_blocks<<<gv, B, 0, st>>>(n, head, cnt, sc);
@@ -160,8 +158,6 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   k_set_edges<<<1, 1, 0, st>>>(uoff, n, sc);
   note(K_SET_EDGES);
   if (edge_label && g.m > 0) {
-    cudaMemsetAsync(bmin, 0x7F, sizeof(int) * n, st);
-    note(K_MEMSET);
     int64_t nchunks = (g.m + kItems - 1) / kItems;
     k_edge_blocks<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow,
                                                           edge_label, bmin);

@@ -59,9 +59,12 @@ void exclusive_scan(const int* in, int* out, int64_t items, void* tmp, size_t tm
 // ---------------------------------------------------------------------------
 // roots in id order
 // ---------------------------------------------------------------------------
-__global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restrict__ flags) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x)
+// (also clears the out-arc list heads: same index space, no memset node)
+__global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restrict__ flags, int* __restrict__ lhead) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
     flags[v] = (v < n) ? (__ldg(comp + v) == v) : 0;
+    if (v < n) lhead[v] = -1;
+  }
 }
 
 // rlist[rank among roots] = root;  sc->ncomp = c
@@ -259,15 +262,13 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
   const int B = 256;
   const int gv = grid_for(n + 1, B);
   // roots in id order: rank among roots, and the inverse list
-  k_root_flags<<<gv, B, 0, st>>>(comp, n, R.flags);
+  k_root_flags<<<gv, B, 0, st>>>(comp, n, R.flags, R.lhead);
   note(K_ROOT_FLAGS);
   exclusive_scan(R.flags, R.rootidx, n + 1, R.cub_tmp, R.cub_bytes, st);
   note(K_SCAN);
   k_root_list<<<gv, B, 0, st>>>(comp, R.rootidx, n, R.rlist, sc);
   note(K_ROOT_LIST);
   // Euler circuit
-  cudaMemsetAsync(R.lhead, 0xFF, sizeof(int) * n, st);
-  note(K_MEMSET);
   k_out_lists<<<gv, B, 0, st>>>(comp, fe, n, R.lhead, R.nexto);
   note(K_TREE_DEGREE);
   k_link_tour<<<grid_for(2 * (int64_t)n, B), B, 0, st>>>(comp, fe, R.lhead, R.nexto, R.rootidx, R.rlist, n, R.nxt,

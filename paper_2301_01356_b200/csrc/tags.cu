@@ -177,6 +177,24 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int4* __restrict
   }
 }
 
+// all levels of the tile-extreme sparse table in one CTA (levels are
+// published to the block by __syncthreads; every level is tiny next to a
+// launch when ntile <= kTableOneCta)
+constexpr int kTableOneCta = 16384;
+
+__global__ void __launch_bounds__(1024) k_table_all(int2* table, int ntile, int tlev) {
+  for (int k = 1; k < tlev; k++) {
+    const int2* prev = table + (int64_t)(k - 1) * ntile;
+    int2* cur = table + (int64_t)k * ntile;
+    const int half = 1 << (k - 1);
+    for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
+      int2 a = prev[i];
+      cur[i] = (i + half < ntile) ? comb(a, prev[i + half]) : a;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_table_level(int2* table, int ntile, int k) {
   const int2* prev = table + (int64_t)(k - 1) * ntile;
   int2* cur = table + (int64_t)k * ntile;
@@ -198,9 +216,16 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st) {
   k_tile<<<grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st>>>(T.AP, 2 * (int64_t)g.n, T.ntile, T.lh1,
                                                                   T.lh2, T.table);
   note(K_TILE);
-  for (int k = 1; k < T.tlev; k++) {
-    k_table_level<<<grid_for(T.ntile, B), B, 0, st>>>(T.table, T.ntile, k);
-    note(K_TABLE);
+  if (T.ntile <= kTableOneCta) {
+    if (T.tlev > 1) {
+      k_table_all<<<1, 1024, 0, st>>>(T.table, T.ntile, T.tlev);
+      note(K_TABLE);
+    }
+  } else {
+    for (int k = 1; k < T.tlev; k++) {
+      k_table_level<<<grid_for(T.ntile, B), B, 0, st>>>(T.table, T.ntile, k);
+      note(K_TABLE);
+    }
   }
 }
 
@@ -208,7 +233,8 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st) {
 // Stage 4: combine, fence bit
 // ---------------------------------------------------------------------------
 __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const int2* __restrict__ lh2,
-                        const int2* __restrict__ table, int ntile, int* low_out, int* high_out) {
+                        const int2* __restrict__ table, int ntile, int* low_out, int* high_out,
+                        int* __restrict__ head, int* __restrict__ cnt, int* __restrict__ bmin) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
     int ta = r.x / kTile, tb = r.y / kTile;
@@ -231,12 +257,19 @@ __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const in
       low_out[v] = res.x;
       high_out[v] = res.y;
     }
+    // Stage-6 per-vertex state, initialised here (same index space; saves
+    // three memset nodes in the graph)
+    head[v] = -1;
+    cnt[v] = 0;
+    bmin[v] = kINF;
   }
 }
 
-void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, cudaStream_t st) {
+void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
+                  int* bmin, cudaStream_t st) {
   const int B = 256;
-  k_fence<<<grid_for(g.n, B), B, 0, st>>>(g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out);
+  k_fence<<<grid_for(g.n, B), B, 0, st>>>(g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out, head,
+                                          cnt, bmin);
   note(K_FENCE);
 }
 
