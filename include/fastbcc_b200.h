@@ -39,6 +39,17 @@ extern "C" {
 #define FBCC_ERR_CUDA 4       /* a CUDA runtime error (see fbcc_last_cuda_error) */
 #define FBCC_ERR_CYCLE 5      /* list ranking: cycle (euler_tour.py:349-351)  */
 #define FBCC_ERR_COVER 6      /* list ranking: not a disjoint cover (:353-355) */
+#define FBCC_ERR_RANGE 7      /* endpoint out of range (graphs.py:126-130, euler_tour.py:383-384) */
+#define FBCC_ERR_LABELS 8     /* labels inconsistent with the forest (euler_tour.py:435-436) */
+#define FBCC_ERR_NOT_FOREST 9 /* k >= n edges or a cycle (euler_tour.py:381-382) */
+
+/* stand-alone operation codes for fbcc_op_workspace_bytes */
+#define FBCC_OP_CONNECTED_COMPONENTS 1 /* a = n, b = m  */
+#define FBCC_OP_LIST_RANKING 2         /* a = L, b = H  */
+#define FBCC_OP_BUILD_EULER_TOUR 3     /* a = n, b = k  */
+#define FBCC_OP_COMPUTE_TAGS 4         /* a = n, b = m  */
+#define FBCC_OP_EXTRACT_BCCS 5         /* a = n         */
+#define FBCC_OP_SYMMETRIZE 6           /* a = k pairs, b = n */
 
 /* run flags */
 #define FBCC_FLAG_TIMING 1u   /* record per-stage CUDA-event times in stats   */
@@ -115,6 +126,57 @@ int fbcc_plan_destroy(fbcc_plan plan);
    spacing, 4 higher-level splitter spacing (powers of two >= 2). */
 int fbcc_set_option(int key, int value);
 int fbcc_get_option(int key);
+
+/* ---- stand-alone stage operations (the reference's public stage API) ----
+   Each takes a workspace of fbcc_op_workspace_bytes(op, a, b) and
+   synchronises once on ``stream``.  All arrays are DEVICE pointers. */
+int fbcc_op_workspace_bytes(int op, int64_t a, int64_t b, size_t *bytes_out);
+
+/* connected_components(g, keep_edge) connectivity.py:593-611: min-id labels,
+   forest[2x, 2x+1] = the edge that hooked vertex x (x non-root), component
+   count.  keep_mask (per slot, may be NULL) is read at each undirected
+   edge's u < w slot, like _scan_crossing (connectivity.py:279). */
+int fbcc_connected_components(const int64_t *offsets, const uint32_t *edges,
+                              int64_t n, int64_t m, const uint8_t *keep_mask,
+                              void *ws, size_t ws_bytes, int32_t *label,
+                              int32_t *forest, int64_t *ncomp_out,
+                              void *stream);
+
+/* list_ranking(nxt, heads) euler_tour.py:322-358: 0-based rank from each
+   list's head; heads < 0 ignored; FBCC_ERR_CYCLE / FBCC_ERR_COVER like the
+   reference's ValueErrors. */
+int fbcc_list_ranking(const int32_t *nxt, int64_t L, const int32_t *heads,
+                      int64_t H, int32_t *ranks, void *ws, size_t ws_bytes,
+                      void *stream);
+
+/* build_euler_tour(n, tree_edges, labels) euler_tour.py:361-394: roots at
+   min ids, parent/first/last identical to the reference's (same out-arc
+   order).  pairs = k (u, v) int32 pairs; labels may be NULL. */
+int fbcc_build_euler_tour(int64_t n, const int32_t *pairs, int64_t k,
+                          const int32_t *labels, int32_t *parent,
+                          int32_t *first, int32_t *last, void *ws,
+                          size_t ws_bytes, void *stream);
+
+/* compute_tags(g, forest) tagging.py:300-304 on a given rooted forest. */
+int fbcc_compute_tags(const int64_t *offsets, const uint32_t *edges, int64_t n,
+                      int64_t m, const int32_t *parent, const int32_t *first,
+                      const int32_t *last, int32_t *w1, int32_t *w2,
+                      int32_t *low, int32_t *high, void *ws, size_t ws_bytes,
+                      void *stream);
+
+/* extract_bccs(labeling) bcc.py:199-219: block b = block_vtx[block_off[b] ..
+   block_off[b+1]) (sorted, head included), blocks in label order.
+   block_off needs n+1 entries, block_vtx 2n. */
+int fbcc_extract_bccs(const int32_t *label, const int32_t *head, int64_t n,
+                      int32_t *block_off, int32_t *block_vtx,
+                      int64_t *nblocks, void *ws, size_t ws_bytes,
+                      void *stream);
+
+/* symmetrize(edges, n) graphs.py:119-143 on the device: offsets[n+1],
+   edges[<= 2k]; *m_out = directed slots written. */
+int fbcc_symmetrize(const int64_t *u, const int64_t *v, int64_t k, int64_t n,
+                    int64_t *offsets, uint32_t *edges, int64_t *m_out,
+                    void *ws, size_t ws_bytes, void *stream);
 
 /* Name of a kernel kind reported in fbcc_stats.prof_kind. */
 const char *fbcc_kernel_name(int kind);

@@ -84,6 +84,7 @@ def load():
         L.fbcc_kernel_name.restype = ctypes.c_char_p
         L.fbcc_kernel_name.argtypes = [ctypes.c_int]
         _bind_plan(L)
+        bind_ops(L)
         _lib = L
         return L
 
@@ -98,6 +99,10 @@ def check(rc: int) -> None:
     if rc == FBCC_ERR_WORKSPACE:
         raise MemoryError(msg)
     raise ValueError(msg)
+
+
+def all_exports():
+    return EXPORTS + OP_EXPORTS
 
 
 def workspace_bytes(n: int, m: int) -> int:
@@ -119,3 +124,37 @@ def _bind_plan(L):
     L.fbcc_plan_run.argtypes = [P, ctypes.POINTER(FbccStats), P]
     L.fbcc_plan_destroy.restype = ctypes.c_int
     L.fbcc_plan_destroy.argtypes = [P]
+
+
+FBCC_ERR_RANGE = 7
+FBCC_ERR_LABELS = 8
+FBCC_ERR_NOT_FOREST = 9
+OP_CONNECTED_COMPONENTS = 1
+OP_LIST_RANKING = 2
+OP_BUILD_EULER_TOUR = 3
+OP_COMPUTE_TAGS = 4
+OP_EXTRACT_BCCS = 5
+OP_SYMMETRIZE = 6
+OP_EXPORTS = ("fbcc_op_workspace_bytes", "fbcc_connected_components", "fbcc_list_ranking",
+              "fbcc_build_euler_tour", "fbcc_compute_tags", "fbcc_extract_bccs", "fbcc_symmetrize")
+
+
+def bind_ops(L):
+    P = ctypes.c_void_p
+    I64 = ctypes.c_int64
+    L.fbcc_op_workspace_bytes.restype = ctypes.c_int
+    L.fbcc_op_workspace_bytes.argtypes = [ctypes.c_int, I64, I64, ctypes.POINTER(ctypes.c_size_t)]
+    L.fbcc_connected_components.argtypes = [P, P, I64, I64, P, P, ctypes.c_size_t, P, P, ctypes.POINTER(I64), P]
+    L.fbcc_list_ranking.argtypes = [P, I64, P, I64, P, P, ctypes.c_size_t, P]
+    L.fbcc_build_euler_tour.argtypes = [I64, P, I64, P, P, P, P, P, ctypes.c_size_t, P]
+    L.fbcc_compute_tags.argtypes = [P, P, I64, I64, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+    L.fbcc_extract_bccs.argtypes = [P, P, I64, P, P, ctypes.POINTER(I64), P, ctypes.c_size_t, P]
+    L.fbcc_symmetrize.argtypes = [P, P, I64, I64, P, P, ctypes.POINTER(I64), P, ctypes.c_size_t, P]
+    for name in OP_EXPORTS[1:]:
+        getattr(L, name).restype = ctypes.c_int
+
+
+def op_workspace_bytes(op: int, a: int, b: int = 0) -> int:
+    out = ctypes.c_size_t(0)
+    check(load().fbcc_op_workspace_bytes(op, int(a), int(b), ctypes.byref(out)))
+    return int(out.value)

@@ -7,6 +7,7 @@
 #include "../../include/fastbcc_b200.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ops.cuh"
 
 namespace fbcc {
 
@@ -227,6 +228,9 @@ const char* fbcc_strerror(int code) {
     case FBCC_ERR_CUDA: return "CUDA error";
     case FBCC_ERR_CYCLE: return "successor structure contains a cycle";
     case FBCC_ERR_COVER: return "successor structure is not a disjoint list cover";
+    case FBCC_ERR_RANGE: return "edge endpoint out of range";
+    case FBCC_ERR_LABELS: return "labels are inconsistent with the forest edges";
+    case FBCC_ERR_NOT_FOREST: return "a forest on n vertices has at most n-1 edges";
     default: return "unknown error";
   }
 }
@@ -391,6 +395,166 @@ int fbcc_plan_destroy(fbcc_plan plan) {
   delete plan->pipe;
   delete plan;
   return FBCC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stand-alone operations (ops.cu).  Every op keeps a Scalars block at the
+// head of its workspace for error bits and counts, and synchronises once.
+// ---------------------------------------------------------------------------
+static const size_t kOpHead = 256;
+
+static size_t op_bytes(int op, int64_t a, int64_t b) {
+  size_t need = 0;
+  switch (op) {
+    case FBCC_OP_CONNECTED_COMPONENTS:  // a = n
+      return kOpHead + 8 * (size_t)a + 8 * (size_t)a + 512;
+    case FBCC_OP_LIST_RANKING:  // a = L
+      return kOpHead + op_list_ranking_bytes(a);
+    case FBCC_OP_BUILD_EULER_TOUR:  // a = n, b = k
+      op_build_euler_tour(a, nullptr, b, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, true,
+                          &need);
+      return kOpHead + need;
+    case FBCC_OP_COMPUTE_TAGS: {  // a = n, b = m
+      Graph g{nullptr, nullptr, (int)a, b, nullptr};
+      op_compute_tags(g, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, true,
+                      &need);
+      return kOpHead + need;
+    }
+    case FBCC_OP_EXTRACT_BCCS:  // a = n
+      return kOpHead + op_extract_bytes(a);
+    case FBCC_OP_SYMMETRIZE:  // a = k pairs
+      return kOpHead + op_symmetrize_bytes(a);
+    default:
+      return 0;
+  }
+}
+
+int fbcc_op_workspace_bytes(int op, int64_t a, int64_t b, size_t* bytes_out) {
+  if (!bytes_out || a < 0 || b < 0) return FBCC_ERR_ARG;
+  size_t s = op_bytes(op, a, b);
+  if (!s) return FBCC_ERR_ARG;
+  *bytes_out = s;
+  return FBCC_OK;
+}
+
+static int op_finish(Scalars* sc, cudaStream_t st, Scalars* host) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(host, sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "op");
+  int err = host->err;
+  if (err & 1) return FBCC_ERR_RANGE;
+  if (err & 2) return FBCC_ERR_CYCLE;
+  if (err & 16) return FBCC_ERR_NOT_FOREST;
+  if (err & 8) return FBCC_ERR_LABELS;
+  if (err & 4) return FBCC_ERR_COVER;
+  return FBCC_OK;
+}
+
+static Scalars* op_start(void* ws, cudaStream_t st) {
+  Scalars* sc = (Scalars*)ws;
+  cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
+  return sc;
+}
+
+int fbcc_connected_components(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m,
+                              const uint8_t* keep_mask, void* ws, size_t ws_bytes, int32_t* label, int32_t* forest,
+                              int64_t* ncomp_out, void* stream) {
+  int rc = check_sizes(n, m);
+  if (rc) return rc;
+  if (!offsets || (m && !edges) || !label || !ws) return FBCC_ERR_ARG;
+  if (ws_bytes < op_bytes(FBCC_OP_CONNECTED_COMPONENTS, n, m)) return FBCC_ERR_WORKSPACE;
+  if (ncomp_out) *ncomp_out = 0;
+  if (n == 0) return FBCC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scalars* sc = op_start(ws, st);
+  char* p = (char*)ws + kOpHead;
+  int2* fe = forest ? (int2*)forest : (int2*)p;
+  unsigned long long* prop = (unsigned long long*)(p + 8 * n + 256);
+  Graph g{offsets, edges, (int)n, m, nullptr};
+  masked_cc(g, keep_mask, label, fe, prop, sc, st);
+  Scalars host;
+  rc = op_finish(sc, st, &host);
+  if (ncomp_out) *ncomp_out = host.nroots[7];  // counted by the final compress
+  return rc;
+}
+
+int fbcc_list_ranking(const int32_t* nxt, int64_t L, const int32_t* heads, int64_t H, int32_t* ranks, void* ws,
+                      size_t ws_bytes, void* stream) {
+  if (L < 0 || H < 0 || (L && (!nxt || !ranks)) || (H && !heads) || !ws) return FBCC_ERR_ARG;
+  if (L > 2147483647LL) return FBCC_ERR_TOO_LARGE;
+  if (ws_bytes < op_bytes(FBCC_OP_LIST_RANKING, L, H)) return FBCC_ERR_WORKSPACE;
+  if (L == 0) return FBCC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scalars* sc = op_start(ws, st);
+  op_list_ranking(nxt, L, heads, H, ranks, (char*)ws + kOpHead, sc, st);
+  Scalars host;
+  return op_finish(sc, st, &host);
+}
+
+int fbcc_build_euler_tour(int64_t n, const int32_t* pairs, int64_t k, const int32_t* labels, int32_t* parent,
+                          int32_t* first, int32_t* last, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || k < 0 || !ws) return FBCC_ERR_ARG;
+  if (n && 2 * n > 2147483647LL) return FBCC_ERR_TOO_LARGE;
+  if (k >= n && n > 0) return FBCC_ERR_NOT_FOREST;  // euler_tour.py:381-382
+  if (n == 0) return FBCC_OK;
+  if ((k && !pairs) || !parent || !first || !last) return FBCC_ERR_ARG;
+  size_t need = op_bytes(FBCC_OP_BUILD_EULER_TOUR, n, k);
+  if (ws_bytes < need) return FBCC_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scalars* sc = op_start(ws, st);
+  op_build_euler_tour(n, (const int2*)pairs, k, labels, parent, first, last, (char*)ws + kOpHead, need - kOpHead, sc,
+                      st, false, &need);
+  Scalars host;
+  return op_finish(sc, st, &host);
+}
+
+int fbcc_compute_tags(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, const int32_t* parent,
+                      const int32_t* first, const int32_t* last, int32_t* w1, int32_t* w2, int32_t* low,
+                      int32_t* high, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_sizes(n, m);
+  if (rc) return rc;
+  if (n == 0) return FBCC_OK;
+  if (!offsets || (m && !edges) || !parent || !first || !last || !w1 || !w2 || !low || !high || !ws)
+    return FBCC_ERR_ARG;
+  size_t need = op_bytes(FBCC_OP_COMPUTE_TAGS, n, m);
+  if (ws_bytes < need) return FBCC_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scalars* sc = op_start(ws, st);
+  Graph g{offsets, edges, (int)n, m, nullptr};
+  op_compute_tags(g, parent, first, last, w1, w2, low, high, (char*)ws + kOpHead, need - kOpHead, st, false, &need);
+  Scalars host;
+  return op_finish(sc, st, &host);
+}
+
+int fbcc_extract_bccs(const int32_t* label, const int32_t* head, int64_t n, int32_t* block_off, int32_t* block_vtx,
+                      int64_t* nblocks, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !nblocks || !ws) return FBCC_ERR_ARG;
+  *nblocks = 0;
+  if (n == 0) return FBCC_OK;
+  if (!label || !head || !block_off || !block_vtx) return FBCC_ERR_ARG;
+  if (ws_bytes < op_bytes(FBCC_OP_EXTRACT_BCCS, n, 0)) return FBCC_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scalars* sc = op_start(ws, st);
+  op_extract_bccs(label, head, n, block_off, block_vtx, (char*)ws + kOpHead, sc, st);
+  Scalars host;
+  int rc = op_finish(sc, st, &host);
+  *nblocks = host.nbccs;
+  return rc;
+}
+
+int fbcc_symmetrize(const int64_t* u, const int64_t* v, int64_t k, int64_t n, int64_t* offsets, uint32_t* edges,
+                    int64_t* m_out, void* ws, size_t ws_bytes, void* stream) {
+  if (k < 0 || n < 0 || !m_out || !offsets || !ws || (k && (!u || !v || !edges))) return FBCC_ERR_ARG;
+  if (n >= (1LL << 31) || 2 * k > 2147483647LL) return FBCC_ERR_TOO_LARGE;
+  if (ws_bytes < op_bytes(FBCC_OP_SYMMETRIZE, k, n)) return FBCC_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scalars* sc = op_start(ws, st);
+  op_symmetrize(u, v, k, n, offsets, edges, (char*)ws + kOpHead, sc, st);
+  Scalars host;
+  int rc = op_finish(sc, st, &host);
+  *m_out = 2 * (int64_t)host.num_edges;
+  return rc;
 }
 
 }  // extern "C"

@@ -1,34 +1,54 @@
-// connectivity.cu -- Stage 1 (spanning forest + components) and Stage 5
-// (skeleton connectivity).
+// connectivity.cu -- Stage 1 (spanning forest + components), Stage 5
+// (skeleton connectivity) and the stand-alone masked connectivity op.
 //
 // Replaces the reference's clustered connectivity _cc_parts
 // (connectivity.py:541-574: LDD ball growing _ldd_drive 195-246, sequential
-// union batch _union_batch 287-309, label canonicalisation 312-341) and its
+// union batch _union_batch 287-309, label canonicalisation 312-341), its
 // skeleton-filtered second pass (bcc.py:185-189 with _slot_kept
-// connectivity.py:57-81).
+// connectivity.py:57-81) and connected_components(g, keep_edge)
+// (connectivity.py:593-611).
 //
-// B200 design: Afforest-style union-find hooking.  Parents live in one int32
-// array (4 MB per 1M vertices -- L2-resident up to ~30M vertices).  A link
-// CASes the larger root under the smaller, so every root is the minimum id
-// of its set and final labels are canonical (== reference labels) without a
-// min pass.  The CAS winner of Stage 1 records the edge that merged the two
-// sets at fe[hooked root]: exactly n - c winners, an acyclic spanning forest
-// (each win joins two distinct sets), one writer per slot.
-//   1. two neighbour-sampling rounds (arc r of every row), each + compress
-//   2. sample 1024 vertices, the most frequent root is the giant component
-//   3. every remaining arc of every row not (yet) in the giant component --
-//      arc-balanced (kItems arcs per thread), so RMAT hubs do not serialise
-//   4. final compress -> comp[v] = min id of v's component
-// Stage 5 is the same schedule templated on the skeleton predicate (the
-// predicate is symmetric, so the giant-component skip stays exact) and with
-// no forest recording.
+// B200 design: union-find with the root of every set equal to its minimum
+// id, so final labels are canonical (== reference labels) with no min pass.
+// Parents live in one int32 array (4 MB per 1M vertices).
+//   1. k sampling rounds (default 3) over arc r of every row, each a
+//      PROPOSE/ACCEPT step: every vertex fires one fire-and-forget 64-bit
+//      atomicMin((lower root << 32) | proposer) at the higher of the two
+//      component roots; k_accept hooks each proposed-to root under its
+//      minimum proposal and records the forest edge.  Hooks always point to
+//      a smaller round-start root (a forest over the components, no cycles),
+//      and same-address REDs pipeline in the L2 atomic unit instead of
+//      serialising CAS retry loops on a few hot roots (the failure mode of
+//      Afforest's CAS link on a GPU: round 1 merges ~n/17 roots into one).
+//      Proposers are thinned to ~32 per surviving root.
+//   2. compress after round 0 and after the last round (pointer doubling on
+//      a fully resident grid); rounds in between find() through shallow trees
+//   3. sample 1024 vertices: the most frequent root is the giant component
+//   4. every arc of every row outside the giant (Afforest's skip; exact for a
+//      symmetric predicate): union-find with L1-cached finds, path halving
+//      and CAS hooking, one warp per 32 rows, long rows warp-cooperative
+//   5. final compress -> comp[v] = min id of v's component
+// In Stage 1 each successful hook records the arc that merged the two sets
+// at fe[hooked root]: exactly n - c records, an acyclic spanning forest.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace fbcc {
 
+// ---------------------------------------------------------------------------
+// edge predicates
+// ---------------------------------------------------------------------------
+enum : int { PRED_NONE = 0, PRED_SKEL = 1, PRED_MASK = 2 };
+
+struct PredData {
+  const int4* rec;        // PRED_SKEL: {first, last, parent, fence}
+  const uint8_t* mask;    // PRED_MASK: per-slot keep byte
+  const int64_t* off;     // PRED_MASK: to find the canonical (u < w) slot
+  const uint32_t* adj;
+};
+
 // Skeleton predicate (connectivity.py:57-81 / bcc.py classify_edge 54-70):
-// rec = {first, last, parent, fence}.  Keep plain tree edges and cross edges.
+// keep plain tree edges and cross edges.
 __device__ __forceinline__ bool skel_keep(int u, const int4& ru, int w, const int4& rw) {
   if (rw.z == u) return rw.w == 0;  // tree edge, w is the child
   if (ru.z == w) return ru.w == 0;  // tree edge, u is the child
@@ -37,6 +57,29 @@ __device__ __forceinline__ bool skel_keep(int u, const int4& ru, int w, const in
   return true;                                      // cross edge
 }
 
+// The reference reads a keep mask at the u < w slot of each undirected edge
+// only (_scan_crossing connectivity.py:279); the reverse arc finds that slot
+// by binary search in the (sorted) row of its smaller endpoint.
+__device__ __forceinline__ bool mask_keep(const PredData& pd, int v, int w, int64_t a) {
+  if (v < w) return pd.mask[a] != 0;
+  int64_t lo = __ldg(pd.off + w), hi = __ldg(pd.off + w + 1);
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if ((int)__ldg(pd.adj + mid) < v) lo = mid + 1; else hi = mid;
+  }
+  return pd.mask[lo] != 0;
+}
+
+template <int kPred>
+__device__ __forceinline__ bool keep(const PredData& pd, int v, const int4& rv, int w, int64_t a) {
+  if (kPred == PRED_SKEL) return skel_keep(v, rv, w, __ldg(pd.rec + w));
+  if (kPred == PRED_MASK) return mask_keep(pd, v, w, a);
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// union-find primitives
+// ---------------------------------------------------------------------------
 // Root of x with path halving.  Only non-roots are rewritten, always to an
 // ancestor (ancestors stay ancestors: sets only merge), and roots change only
 // through the hooking CAS -- so the concurrent plain stores are benign.
@@ -50,26 +93,25 @@ __device__ __forceinline__ bool skel_keep(int u, const int4& ru, int w, const in
 // requests serialise on a single L2 slice.
 __device__ __forceinline__ int ldp(const int* p) { return __ldca(p); }
 
-__device__ __forceinline__ int find_halve(int* comp, int x, bool halve) {
+__device__ __forceinline__ int find_halve(int* comp, int x) {
   int p = ldp(comp + x);
   while (p != x) {
     int gp = ldp(comp + p);
     if (gp == p) return p;
-    if (halve) comp[x] = gp;
+    comp[x] = gp;
     x = gp;
     p = ldp(comp + x);
   }
   return x;
 }
 
-// Hook the larger root under the smaller.  ru/rw are roots of the sets
-// holding u and w when found; a successful CAS hooks root `hi` under `lo`,
-// whose set holds the other endpoint (roots are set minima, root(lo) <= lo <
-// hi), so (u, w) is a spanning-forest edge joining two distinct sets.
+// Hook the larger root under the smaller.  A successful CAS hooks root `hi`
+// under `lo`, whose set holds the other endpoint (root(lo) <= lo < hi), so
+// (u, w) is a spanning-forest edge joining two distinct sets.
 template <bool kRecord>
-__device__ __forceinline__ void link(int u, int w, int* comp, int2* fe, bool halve) {
-  int ru = find_halve(comp, u, halve);
-  int rw = find_halve(comp, w, halve);
+__device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
+  int ru = find_halve(comp, u);
+  int rw = find_halve(comp, w);
   while (ru != rw) {
     int hi = ru > rw ? ru : rw;
     int lo = ru + rw - hi;
@@ -78,13 +120,15 @@ __device__ __forceinline__ void link(int u, int w, int* comp, int2* fe, bool hal
       if (kRecord) fe[hi] = make_int2(u, w);
       return;
     }
-    ru = find_halve(comp, prev, halve);  // hi was hooked meanwhile: climb on
-    rw = find_halve(comp, lo, halve);
+    ru = find_halve(comp, prev);  // hi was hooked meanwhile: climb on
+    rw = find_halve(comp, lo);
   }
 }
 
+// ---------------------------------------------------------------------------
 // chunk -> row table (see visit_arc_chunks): row v owns the chunks whose
 // first arc lies in it
+// ---------------------------------------------------------------------------
 __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t q0 = (__ldg(off + v) + kItems - 1) / kItems;
@@ -111,61 +155,15 @@ __global__ void k_iota(int* __restrict__ comp, int n, unsigned long long* __rest
   }
 }
 
-// Best-effort sampling round: one CAS attempt on the (post-compress, hence
-// depth-1) parents of v and of its round-th neighbour, no climbing.  A win is
-// still a valid forest edge (hi was a root; lo is an ancestor of the other
-// endpoint, root(lo) <= lo < hi); a loss is simply left to k_link_rest, which
-// re-covers every arc of every row outside the giant component.  Climbing
-// here is what made round 1 contention-bound: after round 0 the ~n/17
-// local-minimum roots all merge into one giant and every failed CAS then
-// chases the same few hot roots.
-template <bool kSkel, bool kRecord>
-__global__ void k_sample_link(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
-                              int round, int* comp, int2* fe, const int4* __restrict__ rec, bool full,
-                              bool halve) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    int64_t s = __ldg(off + v) + round;
-    if (s >= __ldg(off + v + 1)) continue;
-    int w = (int)__ldg(adj + s);
-    if (kSkel) {
-      if (!skel_keep(v, __ldg(rec + v), w, __ldg(rec + w))) continue;
-    }
-    if (full) {  // exact Afforest sampling: climb until joined
-      link<kRecord>(v, w, comp, fe, halve);
-      continue;
-    }
-    int ru = ldp(comp + v), rw = ldp(comp + w);
-    if (ru == rw) continue;
-    int hi = ru > rw ? ru : rw;
-    int lo = ru + rw - hi;
-    // one CAS per distinct target root per warp (later rounds have few roots)
-    unsigned peers = __match_any_sync(__activemask(), hi);
-    if ((threadIdx.x & 31) != __ffs(peers) - 1) continue;
-    if (atomicCAS(comp + hi, hi, lo) == hi && kRecord) fe[hi] = make_int2(v, w);
-  }
-}
-
-// Propose/accept sampling round (the default).  Against the round-start
-// components (comp is flat after the previous compress and is not written
-// during the propose kernel), every vertex proposes its round-th arc to the
-// HIGHER of the two component roots with one fire-and-forget 64-bit
-// atomicMin of (lower root << 32 | arc slot).  Same-address REDs pipeline in
-// the L2 atomic unit instead of serialising retry loops, so the many-to-few
-// merges of later rounds are cheap.  k_accept then hooks every proposed-to
-// root under its minimum proposal: hooks always point to a smaller
-// round-start root, so they form a forest over the components (no cycles),
-// and each accepted hook records its arc -- one forest edge per merge.
-//
-// Proposers are thinned to ~kPerRoot per surviving root: on config 2 the
-// rounds go 1M -> 65k -> 565 -> 1 components, and round 2 would otherwise
-// aim 941k proposals at 565 roots (up to 18k REDs on one word).  A root that
-// draws no proposer simply stays for the next round / k_link_rest.
+// ---------------------------------------------------------------------------
+// sampling rounds
+// ---------------------------------------------------------------------------
 constexpr int kPerRoot = 32;
 
-template <bool kSkel>
+template <int kPred>
 __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round,
-                          int* comp, unsigned long long* prop, const int4* __restrict__ rec,
-                          const int* __restrict__ nroots, const int* __restrict__ hooks, bool flat) {
+                          int* comp, unsigned long long* prop, PredData pd, const int* __restrict__ nroots,
+                          const int* __restrict__ hooks, bool flat) {
   // participate iff hash < thr / 2^24, thr = min(1, kPerRoot * roots / n);
   // roots at round start = roots counted after round 0 minus later hooks
   uint32_t thr = 1u << 24;
@@ -180,18 +178,17 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
     int64_t s = __ldg(off + v) + round;
     if (s >= __ldg(off + v + 1)) continue;
     int w = (int)__ldg(adj + s);
-    if (kSkel) {
-      if (!skel_keep(v, __ldg(rec + v), w, __ldg(rec + w))) continue;
-    }
+    int4 rv;
+    if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
+    if (!keep<kPred>(pd, v, rv, w, s)) continue;
     // flat after a compress; otherwise (rounds >= 1 hook root -> root only,
     // so trees stay shallow) find with halving
-    int ru = flat ? ldp(comp + v) : find_halve(comp, v, true);
-    int rw = flat ? ldp(comp + w) : find_halve(comp, w, true);
+    int ru = flat ? ldp(comp + v) : find_halve(comp, v);
+    int rw = flat ? ldp(comp + w) : find_halve(comp, w);
     if (ru == rw) continue;
     int hi = ru > rw ? ru : rw;
     int lo = ru + rw - hi;
     // any proposal is a valid hook, so lanes aiming at the same root send one
-    // (small components below the giant's root all aim at it in round 2)
     unsigned peers = __match_any_sync(__activemask(), hi);
     if ((threadIdx.x & 31) != __ffs(peers) - 1) continue;
     // low word = the proposer: its arc is off[v] + round, no search on accept
@@ -218,18 +215,15 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
   block_count_add(hooks + round, hooked);
 }
 
-// pointer jumping to the root (the root is the component minimum)
-// (optionally counting the roots into *nroots).  Every step stores the
-// advanced pointer and reads the parent's CURRENT pointer from L2, so
-// concurrent threads ride each other's progress: pointer doubling, ~log2(depth)
-// steps per thread.  Walking to the root and storing once at the end is
-// O(depth) per thread -- O(n^2) on a 10^8-vertex path whose round-0 hooks
-// form one chain (3.2 s measured on config 4c).
-//
-// No hooks happen during a compress, so a root's entry is stable: the
-// "is c a root" test may use an L1-cached load (the giant root's word is then
-// served per SM instead of hammering one L2 slice), and only non-root
-// pointers -- which other threads are advancing -- are re-read from L2.
+// Pointer jumping to the root (the component minimum), optionally counting
+// the roots.  Every step stores the advanced pointer and reads the parent's
+// CURRENT pointer from L2, so concurrent threads ride each other's progress:
+// pointer doubling, ~log2(depth) steps per thread (storing only at the end is
+// O(depth) per thread -- O(n^2) on a 10^8-vertex path whose round-0 hooks form
+// one chain).  No hooks happen during a compress, so a root's entry is stable
+// and the "is c a root" test may use an L1-cached load (the giant root's word
+// is then served per SM instead of hammering one L2 slice).  The grid must
+// be fully resident (see run_cc).
 __global__ void k_compress(int* comp, int n, int* nroots) {
   int roots = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
@@ -264,9 +258,9 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, b
     if (k == -1 || k == mine) break;
     slot = (slot + 1) & (H - 1);
   }
-  int cnt = atomicAdd(&num[slot], 1) + 1;  // any member's final count works below
+  atomicAdd(&num[slot], 1);
   __syncthreads();
-  cnt = num[slot];
+  int cnt = num[slot];
   // argmax (ties -> smaller root id, deterministic)
   for (int o = 16; o > 0; o >>= 1) {
     int oc = __shfl_down_sync(0xffffffffu, cnt, o);
@@ -286,58 +280,15 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, b
   }
 }
 
-template <bool kSkel, bool kRecord>
-struct LinkRestVisitor {
-  int* comp;
-  int2* fe;
-  const int4* rec;
-  int giant;
-  int rounds;
-  bool halve;
-  int64_t rs;
-  bool skip;
-  int4 rv;
-  __device__ __forceinline__ void begin(int v, int64_t s, int64_t e) {
-    rs = s;
-    int p = ldp(comp + v);
-    skip = p == giant || ldp(comp + p) == giant;  // sound: giant is an ancestor
-    if (kSkel && !skip) rv = __ldg(rec + v);
-  }
-  __device__ __forceinline__ void arc(int v, int64_t a, int w) {
-    if (skip || a - rs < rounds) return;
-    if (kSkel) {
-      if (!skel_keep(v, rv, w, __ldg(rec + w))) return;
-    }
-    link<kRecord>(v, w, comp, fe, halve);
-  }
-  __device__ __forceinline__ void end(int, bool) {}
-};
-
-template <bool kSkel, bool kRecord>
-__global__ void __launch_bounds__(256) k_link_rest(const int64_t* __restrict__ off,
-                                                   const uint32_t* __restrict__ adj, const int* __restrict__ crow, int n, int64_t m,
-                                                   int rounds, int* comp, int2* fe,
-                                                   const int4* __restrict__ rec, const Scalars* sc, bool halve) {
-  LinkRestVisitor<kSkel, kRecord> vis;
-  vis.comp = comp;
-  vis.fe = fe;
-  vis.rec = rec;
-  vis.giant = sc->giant;
-  vis.rounds = rounds;
-  vis.halve = halve;
-  visit_arc_chunks(off, adj, crow, n, m, vis);
-}
-
 // Remaining arcs, row-filtered: each warp takes 32 consecutive rows and drops
 // the ones already in the sampled giant before touching their adjacency
 // (after the sampling rounds that is almost every row of a low-diameter
 // graph, so the 4m bytes of targets are mostly never read).  Rows of <= 32
 // arcs are linked by their own lane; longer rows are linked by the whole warp
 // striding over the arcs (a non-giant hub cannot serialise one thread).
-template <bool kSkel, bool kRecord>
+template <int kPred, bool kRecord>
 __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                                   int n, int* comp, int2* fe, const int4* __restrict__ rec,
-                                                   const Scalars* sc, bool halve) {
+                                                   int n, int* comp, int2* fe, PredData pd, const Scalars* sc) {
   const int giant = sc->giant;
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -346,7 +297,7 @@ __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ o
     int64_t rs = 0, re = 0;
     int p = v < n ? ldp(comp + v) : giant;
     // skip rows whose parent or grandparent is the giant root (sound: an
-    // ancestor; comp need not be flat after the last sampling round)
+    // ancestor)
     if (p != giant && ldp(comp + p) != giant) {
       rs = __ldg(off + v);
       re = __ldg(off + v + 1);
@@ -354,11 +305,11 @@ __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ o
     const bool heavy = re - rs > 32;
     if (!heavy && re > rs) {
       int4 rv;
-      if (kSkel) rv = __ldg(rec + v);
+      if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
       for (int64_t a = rs; a < re; a++) {
         int w = (int)__ldg(adj + a);
-        if (kSkel && !skel_keep(v, rv, w, __ldg(rec + w))) continue;
-        link<kRecord>(v, w, comp, fe, halve);
+        if (!keep<kPred>(pd, v, rv, w, a)) continue;
+        link<kRecord>(v, w, comp, fe);
       }
     }
     unsigned hb = __ballot_sync(0xffffffffu, heavy);
@@ -368,55 +319,45 @@ __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ o
       const int hv = __shfl_sync(0xffffffffu, v, src);
       const int64_t hs = __shfl_sync(0xffffffffu, rs, src), he = __shfl_sync(0xffffffffu, re, src);
       int4 rv;
-      if (kSkel) rv = __ldg(rec + hv);
+      if (kPred == PRED_SKEL) rv = __ldg(pd.rec + hv);
       for (int64_t a = hs + lane; a < he; a += 32) {
         int w = (int)__ldg(adj + a);
-        if (kSkel && !skel_keep(hv, rv, w, __ldg(rec + w))) continue;
-        link<kRecord>(hv, w, comp, fe, halve);
+        if (!keep<kPred>(pd, hv, rv, w, a)) continue;
+        link<kRecord>(hv, w, comp, fe);
       }
     }
   }
 }
 
-// Afforest schedule shared by Stage 1 (kSkel=false, record forest) and
-// Stage 5 (kSkel=true, no forest).
-template <bool kSkel, bool kRecord>
-static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop, const int4* rec, Scalars* sc,
-                   cudaStream_t st) {
+// The schedule shared by Stage 1 (no predicate, forest recorded), Stage 5
+// (skeleton predicate) and the masked stand-alone op.  `slot` picks the
+// sampling counters (0 / 8) in Scalars.
+template <int kPred, bool kRecord>
+static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop, PredData pd, Scalars* sc,
+                   int slot, cudaStream_t st) {
   const int B = 256;
   const int kRounds = g_opt[OPT_SAMPLE_ROUNDS];
-  const bool halve = g_opt[OPT_FIND_HALVING] != 0;
-  const bool propose = g_opt[OPT_SAMPLE_MODE] == 0;
-  int* nroots = sc->nroots + (kSkel ? 8 : 0);  // device addresses (sc is a device pointer)
-  int* hooks = sc->hooks + (kSkel ? 8 : 0);
+  const int gv = grid_for(g.n, B);
+  // k_compress relies on concurrent threads advancing each other's pointers:
+  // its grid must be fully resident (2048 threads/SM), or grid-stride
+  // threads chase pointers owned by blocks that cannot be scheduled yet
+  const int gres = grid_for(g.n, B, 2048 / B);
+  int* nroots = sc->nroots + slot;  // device addresses (sc is a device pointer)
+  int* hooks = sc->hooks + slot;
   // compress after round 0 (flattens the deep min-neighbour forest) and after
   // the last round (k_link_rows' giant test wants a flat array); rounds in
   // between only hook roots under roots and their proposers find() instead
   int cmask = g_opt[OPT_COMPRESS_MASK];
   if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
-  int gv = grid_for(g.n, B);
-  // k_compress relies on concurrent threads advancing each other's pointers:
-  // its grid must be fully resident (2048 threads/SM), or grid-stride
-  // threads chase pointers owned by blocks that cannot be scheduled yet
-  const int gres = grid_for(g.n, B, 2048 / B);
-  k_iota<<<gv, B, 0, st>>>(comp, g.n, propose && kRounds > 0 ? prop : nullptr);
+  k_iota<<<gv, B, 0, st>>>(comp, g.n, kRounds > 0 ? prop : nullptr);
   note(K_IOTA);
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
-    if (propose) {
-      k_propose<kSkel><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, rec, nroots, hooks, flat);
-      note(K_SAMPLE_LINK);
-      k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, fe, hooks);
-      note(K_ACCEPT);
-    } else {
-      k_sample_link<kSkel, kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, fe, rec,
-                                                      (g_opt[OPT_SAMPLE_FULL] >> r) & 1, halve);
-      note(K_SAMPLE_LINK);
-    }
-    // round 0 hooks every vertex to its smallest neighbour (deep trees: a
-    // path becomes one chain) and must be flattened; later rounds hook roots
-    // under roots, and their proposers find() through the shallow result
-    if (((cmask >> r) & 1) || !propose) {
+    k_propose<kPred><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat);
+    note(K_SAMPLE_LINK);
+    k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, fe, hooks);
+    note(K_ACCEPT);
+    if ((cmask >> r) & 1) {
       k_compress<<<gres, B, 0, st>>>(comp, g.n, r == 0 ? nroots : nullptr);
       note(K_COMPRESS);
     }
@@ -424,27 +365,35 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   k_find_giant<<<1, 1024, 0, st>>>(comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
   note(K_FIND_GIANT);
   if (g.m > 0) {
-    if (g_opt[OPT_LINK_MODE] == 0) {
-      k_link_rows<kSkel, kRecord><<<grid_for(g.n, B, 32), B, 0, st>>>(g.off, g.adj, g.n, comp, fe, rec, sc, halve);
-    } else {
-      int64_t nchunks = (g.m + kItems - 1) / kItems;
-      k_link_rest<kSkel, kRecord><<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m,
-                                                                            /*skip arcs below*/ 0, comp, fe, rec,
-                                                                            sc, halve);
-    }
+    k_link_rows<kPred, kRecord><<<grid_for(g.n, B, 32), B, 0, st>>>(g.off, g.adj, g.n, comp, fe, pd, sc);
     note(K_LINK_REST);
   }
-  k_compress<<<gres, B, 0, st>>>(comp, g.n, nullptr);
+  k_compress<<<gres, B, 0, st>>>(comp, g.n, nroots + 7);  // final root count (= components)
   note(K_COMPRESS);
 }
 
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st) {
-  run_cc<false, true>(g, comp, fe, prop, nullptr, sc, st);
+  run_cc<PRED_NONE, true>(g, comp, fe, prop, PredData{}, sc, 0, st);
 }
 
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
                         cudaStream_t st) {
-  run_cc<true, false>(g, label, nullptr, prop, rec, sc, st);
+  PredData pd{};
+  pd.rec = rec;
+  run_cc<PRED_SKEL, false>(g, label, nullptr, prop, pd, sc, 8, st);
+}
+
+void masked_cc(const Graph& g, const uint8_t* mask, int* comp, int2* fe, unsigned long long* prop, Scalars* sc,
+               cudaStream_t st) {
+  if (!mask) {
+    run_cc<PRED_NONE, true>(g, comp, fe, prop, PredData{}, sc, 0, st);
+    return;
+  }
+  PredData pd{};
+  pd.mask = mask;
+  pd.off = g.off;
+  pd.adj = g.adj;
+  run_cc<PRED_MASK, true>(g, comp, fe, prop, pd, sc, 0, st);
 }
 
 }  // namespace fbcc

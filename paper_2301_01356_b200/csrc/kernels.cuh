@@ -55,6 +55,10 @@ struct Tags {
 
 constexpr int kTile = 4096;      // tour positions per tile in the low/high pass
 
+void rooting_roots(int n, const int* comp, Rooting& R, Scalars* sc, cudaStream_t st);
+void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc, cudaStream_t st);
+void masked_cc(const Graph& g, const uint8_t* mask, int* comp, int2* fe, unsigned long long* prop, Scalars* sc,
+               cudaStream_t st);
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st);
 void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
                     Scalars* sc, cudaStream_t st);

@@ -256,21 +256,32 @@ __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict
   }
 }
 
-void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
-                    Scalars* sc, cudaStream_t st) {
-  const int n = g.n;
+// roots in id order: rank among roots, the inverse list, c; clears lhead
+void rooting_roots(int n, const int* comp, Rooting& R, Scalars* sc, cudaStream_t st) {
   const int B = 256;
   const int gv = grid_for(n + 1, B);
-  // roots in id order: rank among roots, and the inverse list
   k_root_flags<<<gv, B, 0, st>>>(comp, n, R.flags, R.lhead);
   note(K_ROOT_FLAGS);
   exclusive_scan(R.flags, R.rootidx, n + 1, R.cub_tmp, R.cub_bytes, st);
   note(K_SCAN);
   k_root_list<<<gv, B, 0, st>>>(comp, R.rootidx, n, R.rlist, sc);
   note(K_ROOT_LIST);
-  // Euler circuit
-  k_out_lists<<<gv, B, 0, st>>>(comp, fe, n, R.lhead, R.nexto);
+}
+
+void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
+                    Scalars* sc, cudaStream_t st) {
+  rooting_roots(g.n, comp, R, sc, st);
+  // Euler circuit: out-arc lists in atomicExch order (any order is a valid
+  // tour; the final outputs do not depend on it)
+  k_out_lists<<<grid_for(g.n, 256), 256, 0, st>>>(comp, fe, g.n, R.lhead, R.nexto);
   note(K_TREE_DEGREE);
+  rooting_tour(g.n, comp, fe, R, AP, sc, st);
+}
+
+// tour linking, list ranking, positions (needs lhead/nexto built)
+void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc, cudaStream_t st) {
+  const int B = 256;
+  const int gv = grid_for(n + 1, B);
   k_link_tour<<<grid_for(2 * (int64_t)n, B), B, 0, st>>>(comp, fe, R.lhead, R.nexto, R.rootidx, R.rlist, n, R.nxt,
                                                          sc);
   note(K_LINK_SLOTS);

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol(lib):
     declared = set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(fbcc_\w+)\s*\(", hdr, re.M))
     from paper_2301_01356_b200 import _lib
 
-    assert declared == set(_lib.EXPORTS)
+    assert declared == set(_lib.all_exports())
     for name in declared:
         assert hasattr(lib, name), name
 
