@@ -135,3 +135,58 @@ def symmetrize(edges, n: int) -> Graph:
     offsets = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(np.bincount(src, minlength=n), out=offsets[1:])
     return Graph(offsets, dst)
+
+
+# ---------------------------------------------------------------------------
+# binary CSR artifact (reference format, graphs.py:146-204): little-endian
+# u64 n, u64 m, u64 size, (n+1) u64 offsets, m u32 targets.  The size word is
+# 24 + 8(n+1) + 4m; the legacy value 24 + 8(n-1) + 4m is accepted with a
+# warning, like the reference.
+# ---------------------------------------------------------------------------
+_HEADER_BYTES = 24
+
+
+def expected_bin_size(n: int, m: int) -> int:
+    return _HEADER_BYTES + 8 * (n + 1) + 4 * m
+
+
+def write_bin(g: Graph, path) -> None:
+    n, m = g.n, g.m
+    with open(path, "wb") as f:
+        np.array([n, m, expected_bin_size(n, m)], dtype="<u8").tofile(f)
+        np.asarray(g.offsets, dtype="<u8").tofile(f)
+        np.asarray(g.edges, dtype="<u4").tofile(f)
+
+
+def load_bin(path, device=None) -> Graph:
+    """Read a .bin CSR; with ``device`` set, the arrays go straight from a
+    pinned staging buffer to HBM and a device Graph is returned."""
+    import warnings
+
+    with open(path, "rb") as f:
+        header = np.fromfile(f, dtype="<u8", count=3)
+        if header.size != 3:
+            raise ValueError(f"{path}: truncated header (need {_HEADER_BYTES} bytes)")
+        n, m, size_field = (int(x) for x in header)
+        want = expected_bin_size(n, m)
+        offsets = np.fromfile(f, dtype="<u8", count=n + 1)
+        edges = np.fromfile(f, dtype="<u4", count=m)
+        extra = f.read(1)
+    if offsets.size != n + 1 or edges.size != m or extra:
+        have = _HEADER_BYTES + offsets.size * 8 + edges.size * 4 + len(extra)
+        raise ValueError(f"{path}: size mismatch, expected {want} bytes for n={n} m={m}, "
+                         f"got {have}{'+' if extra else ''}")
+    if size_field != want:
+        legacy = _HEADER_BYTES + 8 * (n - 1) + 4 * m
+        if size_field != legacy:
+            raise ValueError(f"{path}: size field {size_field} matches neither {want} nor the legacy value {legacy}")
+        warnings.warn(f"{path}: legacy size field {size_field} (expected {want}); accepting", stacklevel=2)
+    if offsets[0] != 0 or offsets[-1] != m:
+        raise ValueError(f"{path}: offsets must run from 0 to m")
+    if device is None:
+        return Graph(offsets.astype(np.int64), edges)
+    import torch
+
+    off_t = torch.from_numpy(offsets.view(np.int64)).pin_memory().to(device, non_blocking=True)
+    adj_t = torch.from_numpy(edges.view(np.int32)).pin_memory().to(device, non_blocking=True)
+    return Graph.from_device(off_t, adj_t)

@@ -117,3 +117,30 @@ def test_symmetrize_matches_golden_corpus(corpus):
         g2 = symmetrize(g.edge_pairs(), g.n)
         assert np.array_equal(g2.offsets, g.offsets), name
         assert np.array_equal(g2.edges, g.edges), name
+
+
+def test_bin_roundtrip_and_errors(tmp_path):
+    import warnings
+
+    from paper_2301_01356_b200.graphs import Graph, load_bin, symmetrize, write_bin
+
+    g = symmetrize([(0, 1), (1, 2), (2, 0), (2, 3)], 5)
+    p = tmp_path / "g.bin"
+    write_bin(g, p)
+    h = load_bin(p)
+    assert np.array_equal(h.offsets, g.offsets) and np.array_equal(h.edges, g.edges)
+    raw = p.read_bytes()
+    (tmp_path / "t.bin").write_bytes(raw[:10])
+    with pytest.raises(ValueError, match="truncated"):
+        load_bin(tmp_path / "t.bin")
+    (tmp_path / "s.bin").write_bytes(raw[:-4])
+    with pytest.raises(ValueError, match="size mismatch"):
+        load_bin(tmp_path / "s.bin")
+    legacy = bytearray(raw)
+    n, m = g.n, g.m
+    legacy[16:24] = np.array([24 + 8 * (n - 1) + 4 * m], "<u8").tobytes()
+    (tmp_path / "l.bin").write_bytes(bytes(legacy))
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        load_bin(tmp_path / "l.bin")
+        assert any("legacy" in str(x.message) for x in w)
