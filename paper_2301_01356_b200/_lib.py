@@ -27,7 +27,7 @@ EXPORTS = ("fbcc_workspace_bytes", "fbcc_run", "fbcc_strerror", "fbcc_last_cuda_
            "fbcc_kernel_name", "fbcc_plan_create", "fbcc_plan_run", "fbcc_plan_destroy",
            "fbcc_set_option", "fbcc_get_option")
 
-OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "find_halving": 2, "s0": 3, "sl": 4, "sample_full": 5, "sample_mode": 6, "link_mode": 7, "compress_mask": 8}
+OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "find_halving": 2, "s0": 3, "sl": 4, "sample_full": 5, "sample_mode": 6, "link_mode": 7, "compress_mask": 8, "jump": 9}
 
 
 def set_option(name: str, value: int) -> None:

@@ -18,7 +18,7 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "iota", "sample_link", "compress", "find_giant", "link_rest", "root_flags", "scan", "tree_degree",
     "tree_scatter", "link_slots", "link_roots", "walk0", "walk_level", "final_rank", "expand", "positions",
     "w_gather", "tile", "table", "fence", "heads", "ap", "upper_degree", "set_edges", "edge_blocks",
-    "edge_final", "memset", "export", "accept", "chunk_rows", "root_list"};
+    "edge_final", "memset", "export", "accept", "chunk_rows", "root_list", "jump"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -27,12 +27,13 @@ static int cuda_fail(cudaError_t e, const char* where) {
 
 int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*halving*/ 1, /*S0*/ 16, /*SL*/ 8,
                       /*full-link rounds mask*/ 0, /*sample mode: propose/accept*/ 0,
-                      /*link mode: row-filtered*/ 0, /*compress after rounds mask: 0 = first+last*/ 0};
+                      /*link mode: row-filtered*/ 0, /*compress after rounds mask: 0 = first+last*/ 0,
+                      /*4-step jump tables (measured neutral-to-worse: off)*/ 0};
 constexpr int kFinalMaxHost = kFinalMax;
 
 struct Layout {
   size_t total = 0;
-  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
+  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, nexto, nxt, own0, rank0, j4, rec, AP, lh1, lh2, table, cnt, uoff,
       nlow, bmin, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
@@ -77,6 +78,7 @@ struct Layout {
     nxt = take(4 * N0);
     own0 = take(8 * N0);
     rank0 = take(4 * N0);
+    j4 = take(16 * N0);
     for (int l = 1; l <= nlev; l++) {
       lsucc[l] = take(4 * K[l]);
       lwgt[l] = take(4 * K[l]);
@@ -131,6 +133,7 @@ struct Pipeline {
     R.nxt = (int*)at(lay.nxt);
     R.own0 = (int2*)at(lay.own0);
     R.rank0 = (int*)at(lay.rank0);
+    R.J4 = (int4*)at(lay.j4);
     R.nlev = lay.nlev;
     for (int l = 0; l < 8; l++) {
       R.K[l] = lay.K[l];
@@ -172,7 +175,7 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mark(0);
-    build_chunk_rows(g, const_cast<int*>(g.crow), st);
+    build_chunk_rows(g, const_cast<int*>(g.crow), st, uoff + (g.n + 1), nlow);  // + Stage-6 upper degrees
     stage1_forest(g, comp, fe, prop, sc, st);
     mark(1);
     stage2_rooting(g, comp, fe, R, T.AP, sc, st);

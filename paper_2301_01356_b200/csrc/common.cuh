@@ -20,7 +20,8 @@ struct Scalars {
   int num_edges;   // E
   int nroots[16];  // roots after each sampling round's compress (stage 1: 0..7, stage 5: 8..15)
   int hooks[16];   // hooks accepted per sampling round (same split)
-  int pad[27];
+  int nheavy[2];   // super-heavy rows deferred by k_link_rows (stage 1 / stage 5 slot)
+  int pad[25];
 };
 
 // ---------------------------------------------------------------------------
@@ -31,7 +32,7 @@ enum KernelKind : int {
   K_IOTA = 0, K_SAMPLE_LINK, K_COMPRESS, K_FIND_GIANT, K_LINK_REST, K_ROOT_FLAGS, K_SCAN, K_TREE_DEGREE,
   K_TREE_SCATTER, K_LINK_SLOTS, K_LINK_ROOTS, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_POSITIONS,
   K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_AP, K_UPPER_DEGREE, K_SET_EDGES, K_EDGE_BLOCKS,
-  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_ACCEPT, K_CHUNK_ROWS, K_ROOT_LIST, K_NUM_KINDS
+  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_ACCEPT, K_CHUNK_ROWS, K_ROOT_LIST, K_JUMP, K_NUM_KINDS
 };
 
 struct LaunchLog {
@@ -72,6 +73,7 @@ enum Option : int {
   OPT_SAMPLE_MODE = 6,    // 0: propose/accept rounds, 1: CAS rounds
   OPT_LINK_MODE = 7,      // remaining arcs: 0 row-filtered warps, 1 arc-balanced chunks
   OPT_COMPRESS_MASK = 8,  // bitmask: sampling rounds followed by a compress (bit 0 always honoured)
+  OPT_JUMP = 9,           // list-ranking walkers use 4-step jump tables
   OPT_NUM = 16
 };
 extern int g_opt[OPT_NUM];
@@ -175,6 +177,10 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
     }
     int v = __ldg(crow + q);
     if (v < 0) v = row_of(off, 0, n - 1, a0);  // chunk inside a hub row (see k_chunk_rows)
+    // all of the chunk's neighbour gathers go out before any row bookkeeping
+    // (in flight together: 8x the memory-level parallelism of gathering
+    // behind each arc's data-dependent early exit)
+    vis.prefetch(v, w, (int)(a1 - a0));
     int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
     vis.begin(v, rs, re);
 #pragma unroll
@@ -188,7 +194,7 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
           re = __ldg(off + v + 1);
           vis.begin(v, rs, re);
         }
-        vis.arc(v, a, (int)w[i]);
+        vis.arc(v, a, (int)w[i], i);
       }
     }
     vis.end(v, rs >= a0 && re <= a1);

@@ -129,22 +129,66 @@ __device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
 // chunk -> row table (see visit_arc_chunks): row v owns the chunks whose
 // first arc lies in it
 // ---------------------------------------------------------------------------
-__global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow) {
+// Also (ud != nullptr) the per-row input facts Stage 6 needs for edge ids:
+// nlow[v] = #neighbours < v (rows are sorted, graphs.py:36-41) and the upper
+// degree ud[v] = deg - nlow[v], scanned later into the edge numbering.
+__global__ void k_chunk_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
+                             int* __restrict__ crow, int* __restrict__ ud, int* __restrict__ nlow) {
+  if (ud && blockIdx.x == 0 && threadIdx.x == 0) ud[n] = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    int64_t q0 = (__ldg(off + v) + kItems - 1) / kItems;
-    int64_t q1 = (__ldg(off + v + 1) + kItems - 1) / kItems;
+    int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+    if (ud) {
+      int64_t a = rs, b = re;  // first slot with target > v
+      while (a < b) {
+        int64_t mid = (a + b) >> 1;
+        if ((int)__ldg(adj + mid) < v) a = mid + 1; else b = mid;
+      }
+      nlow[v] = (int)(a - rs);
+      ud[v] = (int)(re - a);
+    }
+    int64_t q0 = (rs + kItems - 1) / kItems;
+    int64_t q1 = (re + kItems - 1) / kItems;
     if (q1 - q0 > kRowChunks) continue;  // hub row: consumers binary-search
     for (int64_t q = q0; q < q1; q++) crow[q] = v;
   }
 }
 
-void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st) {
+void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st, int* ud, int* nlow) {
   int64_t nchunks = (g.m + kItems - 1) / kItems;
-  if (nchunks == 0) return;
-  cudaMemsetAsync(crow, 0xFF, sizeof(int) * nchunks, st);
-  note(K_MEMSET);
-  k_chunk_rows<<<grid_for(g.n, 256), 256, 0, st>>>(g.off, g.n, crow);
-  note(K_CHUNK_ROWS);
+  if (nchunks > 0) {
+    cudaMemsetAsync(crow, 0xFF, sizeof(int) * nchunks, st);
+    note(K_MEMSET);
+  }
+  if (nchunks > 0 || ud) {
+    k_chunk_rows<<<grid_for(g.n, 256), 256, 0, st>>>(g.off, g.adj, g.n, crow, ud, nlow);
+    note(K_CHUNK_ROWS);
+  }
+}
+
+// Sampling round 0 without atomics.  With every vertex its own root, the
+// minimum proposal a vertex v receives is its own smallest neighbour w0
+// (any u < v proposing to v is a neighbour of v, hence u >= w0), so round 0
+// is exactly comp[v] = min(v, w0) and the forest edge (v, w0).  Under a
+// predicate only v's own arc 0 is used (best effort: k_link_rows re-covers).
+// Also resets the proposal words for the later rounds.
+template <int kPred, bool kRecord>
+__global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int* comp,
+                           int2* fe, unsigned long long* __restrict__ prop, PredData pd) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int64_t s = __ldg(off + v);
+    int c = v;
+    if (s < __ldg(off + v + 1)) {
+      int w = (int)__ldg(adj + s);
+      int4 rv;
+      if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
+      if (w < v && keep<kPred>(pd, v, rv, w, s)) {
+        c = w;
+        if (kRecord) fe[v] = make_int2(v, w);
+      }
+    }
+    comp[v] = c;
+    if (prop) prop[v] = ~0ull;
+  }
 }
 
 // comp = identity; also resets the proposal words (one pass, no memset node)
@@ -224,18 +268,35 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
 // and the "is c a root" test may use an L1-cached load (the giant root's word
 // is then served per SM instead of hammering one L2 slice).  The grid must
 // be fully resident (see run_cc).
+//
+// Shallow chains (the common case) are climbed with L1-cached loads only: L1
+// is invalidated at every launch boundary and during a compress non-roots
+// only move up, so a cached value is always an ancestor and the "c is a root"
+// test is exact -- and the few words every thread ends on (the giant's top
+// roots) are served per SM instead of by one L2 slice.  After kL1Steps
+// without reaching a root the thread switches to L2 reads with stores
+// (doubling), for the deep chains of path-like graphs.
+constexpr int kL1Steps = 8;
+
 __global__ void k_compress(int* comp, int n, int* nroots) {
   int roots = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int c = __ldcg(comp + v);
     roots += (c == v);
     if (c == v) continue;
-    while (true) {
+    bool done = false;
+    for (int i = 0; i < kL1Steps; i++) {
+      int x = __ldca(comp + c);
+      if (x == c) { done = true; break; }
+      c = x;
+    }
+    while (!done) {
       if (__ldca(comp + c) == c) break;  // root (stable during compress)
       int cc = __ldcg(comp + c);           // c's current pointer
       __stcg(comp + v, cc);
       c = cc;
     }
+    __stcg(comp + v, c);
   }
   if (nroots) block_count_add(nroots, roots);
 }
@@ -286,9 +347,12 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, b
 // graph, so the 4m bytes of targets are mostly never read).  Rows of <= 32
 // arcs are linked by their own lane; longer rows are linked by the whole warp
 // striding over the arcs (a non-giant hub cannot serialise one thread).
+constexpr int kSuperRow = 8192;
+
 template <int kPred, bool kRecord>
 __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                                   int n, int* comp, int2* fe, PredData pd, const Scalars* sc) {
+                                                   int n, int* comp, int2* fe, PredData pd, const Scalars* sc,
+                                                   int* heavy_list, int* nheavy) {
   const int giant = sc->giant;
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -301,6 +365,12 @@ __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ o
     if (p != giant && ldp(comp + p) != giant) {
       rs = __ldg(off + v);
       re = __ldg(off + v + 1);
+    }
+    // rows longer than kSuperRow (RMAT hubs outside the skeleton giant reach
+    // 638k arcs) go to a list that k_link_heavy spreads over the whole grid
+    if (re - rs > kSuperRow) {
+      heavy_list[atomicAdd(nheavy, 1)] = v;
+      rs = re = 0;
     }
     const bool heavy = re - rs > 32;
     if (!heavy && re > rs) {
@@ -329,6 +399,29 @@ __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ o
   }
 }
 
+// The deferred super-heavy rows: every block strides over every listed row,
+// so one hub's arcs are spread over the whole grid.
+template <int kPred, bool kRecord>
+__global__ void __launch_bounds__(256) k_link_heavy(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                    int* comp, int2* fe, PredData pd, const int* __restrict__ heavy_list,
+                                                    const int* __restrict__ nheavy) {
+  const int H = *nheavy;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int h = 0; h < H; h++) {
+    const int v = heavy_list[h];
+    const int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+    if (rs + tid >= re) continue;
+    int4 rv;
+    if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
+    for (int64_t a = rs + tid; a < re; a += stride) {
+      int w = (int)__ldg(adj + a);
+      if (!keep<kPred>(pd, v, rv, w, a)) continue;
+      link<kRecord>(v, w, comp, fe);
+    }
+  }
+}
+
 // The schedule shared by Stage 1 (no predicate, forest recorded), Stage 5
 // (skeleton predicate) and the masked stand-alone op.  `slot` picks the
 // sampling counters (0 / 8) in Scalars.
@@ -349,14 +442,20 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   // between only hook roots under roots and their proposers find() instead
   int cmask = g_opt[OPT_COMPRESS_MASK];
   if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
-  k_iota<<<gv, B, 0, st>>>(comp, g.n, kRounds > 0 ? prop : nullptr);
+  if (kRounds > 0) {
+    k_hook_min<kPred, kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, comp, fe, prop, pd);  // round 0
+  } else {
+    k_iota<<<gv, B, 0, st>>>(comp, g.n, nullptr);
+  }
   note(K_IOTA);
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
-    k_propose<kPred><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat);
-    note(K_SAMPLE_LINK);
-    k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, fe, hooks);
-    note(K_ACCEPT);
+    if (r > 0) {
+      k_propose<kPred><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat);
+      note(K_SAMPLE_LINK);
+      k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, fe, hooks);
+      note(K_ACCEPT);
+    }
     if ((cmask >> r) & 1) {
       k_compress<<<gres, B, 0, st>>>(comp, g.n, r == 0 ? nroots : nullptr);
       note(K_COMPRESS);
@@ -365,7 +464,15 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   k_find_giant<<<1, 1024, 0, st>>>(comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
   note(K_FIND_GIANT);
   if (g.m > 0) {
-    k_link_rows<kPred, kRecord><<<grid_for(g.n, B, 32), B, 0, st>>>(g.off, g.adj, g.n, comp, fe, pd, sc);
+    // the proposal words are dead after the last accept: reuse them as the
+    // super-heavy row list
+    int* heavy = reinterpret_cast<int*>(prop);
+    int* nheavy = sc->nheavy + (slot ? 1 : 0);
+    k_link_rows<kPred, kRecord><<<grid_for(g.n, B, 32), B, 0, st>>>(g.off, g.adj, g.n, comp, fe, pd, sc, heavy,
+                                                                    nheavy);
+    note(K_LINK_REST);
+    k_link_heavy<kPred, kRecord><<<grid_for((int64_t)kNumSMs * 2048, B), B, 0, st>>>(g.off, g.adj, comp, fe, pd,
+                                                                                     heavy, nheavy);
     note(K_LINK_REST);
   }
   k_compress<<<gres, B, 0, st>>>(comp, g.n, nroots + 7);  // final root count (= components)

@@ -16,7 +16,7 @@ struct Graph {
   const int* crow;       // [ceil(m/kItems)] chunk -> row table (build_chunk_rows)
 };
 
-void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st);
+void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st, int* ud = nullptr, int* nlow = nullptr);
 
 // Device arrays for the rooting / tags stages (see api.cu for the layout).
 constexpr int kFinalMax = 16384;  // list-ranking level finished in one CTA
@@ -30,6 +30,7 @@ struct Rooting {
   int* nxt;        // [2n]  unified tour list successor
   int2* own0;      // [2n]  (segment, offset) per list element
   int* rank0;      // [2n]  tour position of each list element
+  int4* J4;        // [2n]  4-step jump table (level 0, then reused by level 1..)
   // ruling-set levels 1..nlev: element counts and arrays
   int nlev;
   int64_t K[8];
@@ -62,7 +63,9 @@ void masked_cc(const Graph& g, const uint8_t* mask, int* comp, int2* fe, unsigne
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st);
 void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
                     Scalars* sc, cudaStream_t st);
-void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st);
+// exact: reference w2 (both forest directions excluded); otherwise the
+// relaxed gather of tags.cu (same w1/low/high)
+void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, bool exact = false);
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
                   int* bmin,
                   cudaStream_t st);

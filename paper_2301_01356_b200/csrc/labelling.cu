@@ -86,6 +86,12 @@ struct EdgeBlockVisitor {
   int* bmin;
   int lu, ebase;
   int run_blk, run_min;
+  int pl[kItems];
+  // label[w] for every arc that can be an upper arc (w > first row of the chunk)
+  __device__ __forceinline__ void prefetch(int v0, const uint32_t* w, int cnt) {
+#pragma unroll
+    for (int i = 0; i < kItems; i++) pl[i] = (i < cnt && (int)w[i] > v0) ? __ldg(label + w[i]) : -1;
+  }
   __device__ __forceinline__ void flush() {
     if (run_blk >= 0 && run_min < ld_relaxed(bmin + run_blk)) atomicMin(bmin + run_blk, run_min);
     run_blk = -1;
@@ -94,10 +100,10 @@ struct EdgeBlockVisitor {
     lu = __ldg(label + v);
     ebase = __ldg(uoff + v) - (int)(rs + __ldg(nlow + v));  // e = ebase + a for upper arcs
   }
-  __device__ __forceinline__ void arc(int v, int64_t a, int w) {
+  __device__ __forceinline__ void arc(int v, int64_t a, int w, int i) {
     if (w <= v) return;
     int e = ebase + (int)a;
-    int lw = __ldg(label + w);
+    int lw = pl[i];
     int blk = (lu == lw) ? lu : (__ldg(head + lw) == v ? lw : lu);
     eblk[e] = blk;
     if (blk != run_blk) {
@@ -149,10 +155,9 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
     k_ap<<<gv, B, 0, st>>>(n, label, head, cnt, is_ap);
     note(K_AP);
   }
-  // edge ids: ud -> exclusive scan -> uoff (uoff[n] = E)
+  // edge ids: ud (computed with the chunk table at run start) -> exclusive
+  // scan -> uoff (uoff[n] = E)
   int* ud = uoff + (n + 1);
-  k_upper_degree<<<gv, B, 0, st>>>(g.off, g.adj, n, ud, nlow);
-  note(K_UPPER_DEGREE);
   exclusive_scan(ud, uoff, n + 1, cub_tmp, cub_bytes, st);
   note(K_SCAN);
   k_set_edges<<<1, 1, 0, st>>>(uoff, n, sc);

@@ -369,6 +369,7 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   size_t o_comp = L.take(4 * n), o_fe = L.take(8 * n), o_flags = L.take(4 * (n + 1)), o_nrank = L.take(4 * (n + 1));
   size_t o_rootidx = L.take(4 * (n + 1)), o_rlist = L.take(4 * n), o_lhead = L.take(4 * n),
          o_nexto = L.take(4 * N0), o_nxt = L.take(4 * N0), o_own0 = L.take(8 * N0), o_rank0 = L.take(4 * N0),
+         o_j4 = L.take(16 * N0),
          o_rec = L.take(16 * n), o_ap = L.take(16 * (size_t)(N0 + kTile));
   size_t o_keys = L.take(8 * 2 * k + 8), o_keys2 = L.take(8 * 2 * k + 8), o_vals = L.take(4 * 2 * k + 4),
          o_vals2 = L.take(4 * 2 * k + 4);
@@ -408,6 +409,7 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   R.nxt = (int*)at(o_nxt);
   R.own0 = (int2*)at(o_own0);
   R.rank0 = (int*)at(o_rank0);
+  R.J4 = (int4*)at(o_j4);
   R.rec = (int4*)at(o_rec);
   R.nlev = nlev;
   for (int l = 0; l < 8; l++) {
@@ -489,7 +491,7 @@ int op_compute_tags(const Graph& g, const int* parent, const int* first, const i
   T.tlev = tlev;
   int* scr = (int*)at(o_scr);
   k_rec_ap<<<grid_for(n, B), B, 0, st>>>(parent, first, last, (int)n, R.rec, T.AP);
-  stage3_tags(gg, R, T, st);
+  stage3_tags(gg, R, T, st, /*exact=*/true);
   stage4_fence(gg, R, T, low, high, scr, scr + n, scr + 2 * n, st);
   export_debug(gg, nullptr, R.rec, T.AP, nullptr, nullptr, nullptr, nullptr, w1, w2, nullptr, st);
   return 0;

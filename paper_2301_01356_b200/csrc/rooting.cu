@@ -147,6 +147,57 @@ __global__ void __launch_bounds__(256) k_walk(int64_t K, int S, int64_t N, const
   }
 }
 
+// Jump tables: each walker step is one DEPENDENT load (an L2 round trip,
+// ~0.3 us), and the last walker of a level needs ~S ln K steps.  J4[e] =
+// the next four elements (two fully parallel gather passes build it), so a
+// walker advances four elements per dependent load; -1 propagates past a
+// list end.
+__global__ void k_jump2(int64_t N, const int* __restrict__ succ, int2* __restrict__ J2) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+    int s1 = __ldg(succ + e);
+    J2[e] = make_int2(s1, s1 >= 0 ? __ldg(succ + s1) : -1);
+  }
+}
+
+__global__ void k_jump4(int64_t N, const int2* __restrict__ J2, int4* __restrict__ J4) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+    int2 a = __ldg(J2 + e);
+    int2 b = a.y >= 0 ? __ldg(J2 + a.y) : make_int2(-1, -1);
+    J4[e] = make_int4(a.x, a.y, b.x, b.y);
+  }
+}
+
+template <bool kWeighted>
+__global__ void __launch_bounds__(256) k_walk4(int64_t K, int S, int64_t N, const int4* __restrict__ J4,
+                                               const int* __restrict__ w, int2* __restrict__ own,
+                                               int* __restrict__ succ_next, int* __restrict__ w_next) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
+    int e = (int)split_elem(j, S, N);
+    int acc = 0;
+    int nj = -1;
+    own[e] = make_int2((int)j, acc);
+    acc += kWeighted ? __ldg(w + e) : 1;
+    bool stop = false;
+    while (!stop) {
+      int4 q = __ldg(J4 + e);
+      const int xs[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        if (stop) break;
+        int x = xs[t];
+        if (x < 0) { stop = true; break; }
+        int64_t j2 = x / S;
+        if (split_elem(j2, S, N) == x) { nj = (int)j2; stop = true; break; }
+        own[x] = make_int2((int)j, acc);
+        acc += kWeighted ? __ldg(w + x) : 1;
+      }
+      e = q.w;
+    }
+    succ_next[j] = nj;
+    w_next[j] = acc;
+  }
+}
+
 // Final level: <= kFinalMax elements, head = element 0; exclusive weighted
 // prefix along the list, entirely in shared memory (one CTA).
 // The CTA runs one more ruling-set level in shared memory (one walker per
@@ -287,12 +338,31 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
   note(K_LINK_SLOTS);
   // ruling-set levels
   const int64_t N0 = 2 * (int64_t)n;
-  k_walk<false><<<grid_for(R.K[1], B, 64), B, 0, st>>>(R.K[1], R.S[0], N0, R.nxt, nullptr, R.own0,
-                                                       R.succ[1], R.wgt[1]);
+  const bool jump = g_opt[OPT_JUMP] != 0;
+  if (jump) {  // own0 doubles as the J2 scratch: the walk overwrites it afterwards
+    k_jump2<<<grid_for(N0, B), B, 0, st>>>(N0, R.nxt, R.own0);
+    note(K_JUMP);
+    k_jump4<<<grid_for(N0, B), B, 0, st>>>(N0, R.own0, R.J4);
+    note(K_JUMP);
+    k_walk4<false><<<grid_for(R.K[1], B, 64), B, 0, st>>>(R.K[1], R.S[0], N0, R.J4, nullptr, R.own0, R.succ[1],
+                                                          R.wgt[1]);
+  } else {
+    k_walk<false><<<grid_for(R.K[1], B, 64), B, 0, st>>>(R.K[1], R.S[0], N0, R.nxt, nullptr, R.own0,
+                                                         R.succ[1], R.wgt[1]);
+  }
   note(K_WALK0);
   for (int l = 1; l < R.nlev; l++) {
-    k_walk<true><<<grid_for(R.K[l + 1], B, 64), B, 0, st>>>(R.K[l + 1], R.S[l], R.K[l], R.succ[l], R.wgt[l],
-                                                            R.own[l], R.succ[l + 1], R.wgt[l + 1]);
+    if (jump) {  // J2 scratch: own[l]; J4 reuses the level-0 table's storage
+      k_jump2<<<grid_for(R.K[l], B), B, 0, st>>>(R.K[l], R.succ[l], R.own[l]);
+      note(K_JUMP);
+      k_jump4<<<grid_for(R.K[l], B), B, 0, st>>>(R.K[l], R.own[l], R.J4);
+      note(K_JUMP);
+      k_walk4<true><<<grid_for(R.K[l + 1], B, 64), B, 0, st>>>(R.K[l + 1], R.S[l], R.K[l], R.J4, R.wgt[l],
+                                                               R.own[l], R.succ[l + 1], R.wgt[l + 1]);
+    } else {
+      k_walk<true><<<grid_for(R.K[l + 1], B, 64), B, 0, st>>>(R.K[l + 1], R.S[l], R.K[l], R.succ[l], R.wgt[l],
+                                                              R.own[l], R.succ[l + 1], R.wgt[l + 1]);
+    }
     note(K_WALKL);
   }
   cudaFuncSetAttribute(k_final_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinalSmem);

@@ -36,10 +36,22 @@ __device__ __forceinline__ int2 filler() { return make_int2(kINF, -1); }
 // ---------------------------------------------------------------------------
 // w1/w2 gather into A[first[v]]
 // ---------------------------------------------------------------------------
+// kExact reproduces _w_gather (tagging.py:101-119): both forest directions
+// excluded, one 16 B record gather per arc.  The pipeline runs the relaxed
+// form, which excludes only the edge to the parent (tested on v's own
+// record) and gathers a 4-byte first[w] from a compact array: a child c has
+// first[c] > first[v] and lies inside v's subtree, so counting it leaves w1,
+// and every subtree aggregate low/high, unchanged -- only the intermediate
+// w2 of v may grow (SURVEY §8(c) rung 3 checks both forms).  RMAT: 1.05e9
+// gathers from a 134 MB array (mostly L2) instead of a 537 MB one.
+template <bool kExact>
 struct WGatherVisitor {
   const int4* rec;
+  const int* firsts;
   int4* AP;
   int fv, pv, m1, m2;
+  // (prefetching all 8 records up front measured slower here: 118 -> 130 us)
+  __device__ __forceinline__ void prefetch(int, const uint32_t*, int) {}
   __device__ __forceinline__ void begin(int v, int64_t, int64_t) {
     int4 r = __ldg(rec + v);
     fv = r.x;
@@ -47,12 +59,18 @@ struct WGatherVisitor {
     m1 = kINF;
     m2 = -1;
   }
-  __device__ __forceinline__ void arc(int v, int64_t, int w) {
+  __device__ __forceinline__ void arc(int v, int64_t, int w, int) {
     if (pv == w) return;  // tree edge to the parent
-    int4 r = __ldg(rec + w);
-    if (r.z == v) return;  // tree edge to a child
-    m1 = min(m1, r.x);
-    m2 = max(m2, r.x);
+    int f;
+    if (kExact) {
+      const int4 r = __ldg(rec + w);
+      if (r.z == v) return;  // tree edge to a child
+      f = r.x;
+    } else {
+      f = __ldg(firsts + w);
+    }
+    m1 = min(m1, f);
+    m2 = max(m2, f);
   }
   __device__ __forceinline__ void end(int, bool whole) {
     if (whole) {
@@ -64,12 +82,20 @@ struct WGatherVisitor {
   }
 };
 
-__global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
-                                                  int n, int64_t m, const int4* __restrict__ rec, int4* AP) {
-  WGatherVisitor vis;
+template <bool kExact>
+__global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                  const int* __restrict__ crow, int n, int64_t m,
+                                                  const int4* __restrict__ rec, const int* __restrict__ firsts,
+                                                  int4* AP) {
+  WGatherVisitor<kExact> vis;
   vis.rec = rec;
+  vis.firsts = firsts;
   vis.AP = AP;
   visit_arc_chunks(off, adj, crow, n, m, vis);
+}
+
+__global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ firsts) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) firsts[v] = __ldg(&rec[v].x);
 }
 
 // ---------------------------------------------------------------------------
@@ -205,11 +231,19 @@ __global__ void k_table_level(int2* table, int ntile, int k) {
   }
 }
 
-void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st) {
+void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, bool exact) {
   const int B = 256;
   int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (g.m > 0) {
-    k_w_gather<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, R.rec, T.AP);
+    if (exact) {
+      k_w_gather<true><<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, R.rec, nullptr, T.AP);
+    } else {
+      // compact first[] lives in lh1 until k_tile overwrites it
+      int* firsts = reinterpret_cast<int*>(T.lh1);
+      k_firsts<<<grid_for(g.n, B), B, 0, st>>>(R.rec, g.n, firsts);
+      note(K_W_GATHER);
+      k_w_gather<false><<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts, T.AP);
+    }
     note(K_W_GATHER);
   }
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);

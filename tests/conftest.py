@@ -76,3 +76,18 @@ def oracle_mod():
 
     oracle.build()
     return oracle
+
+
+def relaxed_w2(offsets, edges, parent, first):
+    """w2 as the fused pipeline computes it (tags.cu, WGatherVisitor<false>):
+    max(first[v], first[w]) over neighbours w except the tree parent -- tree
+    children are kept.  The exact w2 of tagging.py:101-119 excludes them too;
+    both give the same w1, low and high (checked in the rung-3 tests)."""
+    n = len(offsets) - 1
+    deg = np.diff(offsets).astype(np.int64)
+    src = np.repeat(np.arange(n, dtype=np.int64), deg)
+    dst = np.asarray(edges, dtype=np.int64)
+    keep = dst != np.asarray(parent, dtype=np.int64)[src]
+    w2 = np.asarray(first, dtype=np.int64).copy()
+    np.maximum.at(w2, src[keep], np.asarray(first, dtype=np.int64)[dst[keep]])
+    return w2.astype(np.int32)
