@@ -118,6 +118,12 @@ int fbcc_plan_create(const int64_t *offsets, const uint32_t *edges, int64_t n,
                      const fbcc_outputs *out, uint32_t flags,
                      fbcc_plan *plan_out);
 int fbcc_plan_run(fbcc_plan plan, fbcc_stats *stats, void *stream);
+/* Asynchronous form of fbcc_plan_run: enqueue the graph and the copy of the
+   device counts on `stream` and return.  fbcc_plan_stats fills `stats` once
+   the caller has synchronised that stream (pipelined replays, no host round
+   trip per run). */
+int fbcc_plan_launch(fbcc_plan plan, void *stream);
+int fbcc_plan_stats(fbcc_plan plan, fbcc_stats *stats);
 int fbcc_plan_destroy(fbcc_plan plan);
 
 /* Process-wide tuning knobs (result-neutral, like the reference's beta /

@@ -24,10 +24,10 @@ FBCC_MAX_PROFILE = 512
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = ("fbcc_workspace_bytes", "fbcc_run", "fbcc_strerror", "fbcc_last_cuda_error", "fbcc_version",
-           "fbcc_kernel_name", "fbcc_plan_create", "fbcc_plan_run", "fbcc_plan_destroy",
+           "fbcc_kernel_name", "fbcc_plan_create", "fbcc_plan_run", "fbcc_plan_launch", "fbcc_plan_stats", "fbcc_plan_destroy",
            "fbcc_set_option", "fbcc_get_option")
 
-OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "find_halving": 2, "s0": 3, "sl": 4, "sample_full": 5, "sample_mode": 6, "link_mode": 7, "compress_mask": 8, "jump": 9}
+OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "s0": 3, "sl": 4, "compress_mask": 8, "gather_prefetch": 10, "pdl": 11}
 
 
 def set_option(name: str, value: int) -> None:
@@ -122,6 +122,10 @@ def _bind_plan(L):
                                    ctypes.POINTER(FbccOutputs), ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p)]
     L.fbcc_plan_run.restype = ctypes.c_int
     L.fbcc_plan_run.argtypes = [P, ctypes.POINTER(FbccStats), P]
+    L.fbcc_plan_launch.restype = ctypes.c_int
+    L.fbcc_plan_launch.argtypes = [P, P]
+    L.fbcc_plan_stats.restype = ctypes.c_int
+    L.fbcc_plan_stats.argtypes = [P, ctypes.POINTER(FbccStats)]
     L.fbcc_plan_destroy.restype = ctypes.c_int
     L.fbcc_plan_destroy.argtypes = [P]
 

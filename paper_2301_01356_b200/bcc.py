@@ -183,7 +183,7 @@ class Plan:
     (``fbcc_plan_*`` in the C ABI).  ``run()`` launches the graph, waits and
     returns the counts; outputs land in ``self.label`` etc."""
 
-    def __init__(self, off, adj, *, edge_labels=True, articulation=True, profile=False):
+    def __init__(self, off, adj, *, edge_labels=True, articulation=True, profile=False, timing=False):
         import torch
 
         self.L = _lib.load()
@@ -203,7 +203,8 @@ class Plan:
         h = ctypes.c_void_p()
         _lib.check(self.L.fbcc_plan_create(off.data_ptr(), adj.data_ptr() if m else None, n, m,
                                            self.ws.data_ptr(), self.ws.numel(), ctypes.byref(outs),
-                                           _lib.FBCC_FLAG_PROFILE if profile else 0, ctypes.byref(h)))
+                                           (_lib.FBCC_FLAG_PROFILE if profile else 0)
+                                           | (_lib.FBCC_FLAG_TIMING if timing else 0), ctypes.byref(h)))
         self._h = h
         self.stats = _lib.FbccStats()
 
@@ -212,6 +213,18 @@ class Plan:
 
         s = stream if stream is not None else torch.cuda.current_stream(self.off.device)
         _lib.check(self.L.fbcc_plan_run(self._h, ctypes.byref(self.stats), ctypes.c_void_p(s.cuda_stream)))
+        return self.stats
+
+    def launch(self, stream=None):
+        """Enqueue one replay (graph + counts copy) without waiting; call
+        ``collect()`` after synchronising the stream."""
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.off.device)
+        _lib.check(self.L.fbcc_plan_launch(self._h, ctypes.c_void_p(s.cuda_stream)))
+
+    def collect(self):
+        _lib.check(self.L.fbcc_plan_stats(self._h, ctypes.byref(self.stats)))
         return self.stats
 
     def outputs(self):

@@ -18,22 +18,22 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "iota", "sample_link", "compress", "find_giant", "link_rest", "root_flags", "scan", "tree_degree",
     "tree_scatter", "link_slots", "link_roots", "walk0", "walk_level", "final_rank", "expand", "positions",
     "w_gather", "tile", "table", "fence", "heads", "ap", "upper_degree", "set_edges", "edge_blocks",
-    "edge_final", "memset", "export", "accept", "chunk_rows", "root_list", "jump"};
+    "edge_final", "memset", "export", "accept", "chunk_rows", "root_list", "unused"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
   return FBCC_ERR_CUDA;
 }
 
-int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*halving*/ 1, /*S0*/ 16, /*SL*/ 8,
-                      /*full-link rounds mask*/ 0, /*sample mode: propose/accept*/ 0,
-                      /*link mode: row-filtered*/ 0, /*compress after rounds mask: 0 = first+last*/ 0,
-                      /*4-step jump tables (measured neutral-to-worse: off)*/ 0};
+int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*retired*/ 0, /*S0*/ 16, /*SL*/ 8,
+                      /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last*/ 0,
+                      /*retired*/ 0, /*gather prefetch (measured neutral: off)*/ 0,
+                      /*programmatic dependent launch (measured 5% slower on config 2: off)*/ 0};
 constexpr int kFinalMaxHost = kFinalMax;
 
 struct Layout {
   size_t total = 0;
-  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, nexto, nxt, own0, rank0, j4, rec, AP, lh1, lh2, table, cnt, uoff,
+  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
       nlow, bmin, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
@@ -78,7 +78,6 @@ struct Layout {
     nxt = take(4 * N0);
     own0 = take(8 * N0);
     rank0 = take(4 * N0);
-    j4 = take(16 * N0);
     for (int l = 1; l <= nlev; l++) {
       lsucc[l] = take(4 * K[l]);
       lwgt[l] = take(4 * K[l]);
@@ -133,7 +132,6 @@ struct Pipeline {
     R.nxt = (int*)at(lay.nxt);
     R.own0 = (int2*)at(lay.own0);
     R.rank0 = (int*)at(lay.rank0);
-    R.J4 = (int4*)at(lay.j4);
     R.nlev = lay.nlev;
     for (int l = 0; l < 8; l++) {
       R.K[l] = lay.K[l];
@@ -201,7 +199,8 @@ struct fbcc_plan_s {
   cudaGraphExec_t exec = nullptr;
   Scalars* host = nullptr;  // pinned
   LaunchLog* log = nullptr;  // launch count (+ event nodes when profiled)
-  cudaEvent_t ev[7] = {};    // stage boundaries, recorded by the graph itself
+  cudaEvent_t ev[7] = {};    // stage boundaries, recorded by the graph itself (TIMING / PROFILE)
+  bool timing = false;
 };
 
 extern "C" {
@@ -343,12 +342,15 @@ int fbcc_plan_create(const int64_t* offsets, const uint32_t* edges, int64_t n, i
     p->log->st = cap;
     p->log->capturing = true;
     p->log->profile = (flags & FBCC_FLAG_PROFILE) != 0;
-    for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreate(&p->ev[i]);
+    // stage-boundary event nodes only on request: an event node between two
+    // kernels also cuts their programmatic (PDL) edge
+    p->timing = (flags & (FBCC_FLAG_TIMING | FBCC_FLAG_PROFILE)) != 0;
+    for (int i = 0; i < 7 && e == cudaSuccess && p->timing; i++) e = cudaEventCreate(&p->ev[i]);
     if (e == cudaSuccess) e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
       g_log = p->log;
       p->log->start();
-      p->pipe->enqueue(cap, p->ev, nullptr, nullptr, true);
+      p->pipe->enqueue(cap, p->timing ? p->ev : nullptr, nullptr, nullptr, true);
       g_log = nullptr;
       e = cudaStreamEndCapture(cap, &graph);
     }
@@ -365,24 +367,41 @@ int fbcc_plan_create(const int64_t* offsets, const uint32_t* edges, int64_t n, i
   return FBCC_OK;
 }
 
-int fbcc_plan_run(fbcc_plan plan, fbcc_stats* stats, void* stream) {
+int fbcc_plan_launch(fbcc_plan plan, void* stream) {
   if (!plan) return FBCC_ERR_ARG;
-  if (stats) memset(stats, 0, sizeof(*stats));
   if (!plan->pipe) return FBCC_OK;  // n == 0
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaGraphLaunch(plan->exec, st);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(plan->host, plan->pipe->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return cuda_fail(e, "plan_run");
-  if (stats) {
+  if (e != cudaSuccess) return cuda_fail(e, "plan_launch");
+  return FBCC_OK;
+}
+
+int fbcc_plan_stats(fbcc_plan plan, fbcc_stats* stats) {
+  if (!plan || !stats) return FBCC_ERR_ARG;
+  memset(stats, 0, sizeof(*stats));
+  if (!plan->pipe) return FBCC_OK;
+  {
     fill_counts(stats, *plan->host);
     stats->launches = plan->log->count;
     fill_profile(stats, *plan->log);
-    for (int i = 0; i < 6; i++) cudaEventElapsedTime(&stats->stage_ms[i], plan->ev[i], plan->ev[i + 1]);
-    cudaEventElapsedTime(&stats->total_ms, plan->ev[0], plan->ev[6]);
+    if (plan->timing) {
+      for (int i = 0; i < 6; i++) cudaEventElapsedTime(&stats->stage_ms[i], plan->ev[i], plan->ev[i + 1]);
+      cudaEventElapsedTime(&stats->total_ms, plan->ev[0], plan->ev[6]);
+    }
   }
   return FBCC_OK;
+}
+
+int fbcc_plan_run(fbcc_plan plan, fbcc_stats* stats, void* stream) {
+  int rc = fbcc_plan_launch(plan, stream);
+  if (rc != FBCC_OK) return rc;
+  if (plan->pipe) {
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "plan_run");
+  }
+  return stats ? fbcc_plan_stats(plan, stats) : FBCC_OK;
 }
 
 int fbcc_plan_destroy(fbcc_plan plan) {

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace fbcc {
 
 constexpr int kNumSMs = 148;   // B200
@@ -66,17 +68,45 @@ extern thread_local LaunchLog* g_log;
 enum Option : int {
   OPT_SAMPLE_ROUNDS = 0,  // Afforest neighbour-sampling rounds
   OPT_GIANT_SKIP = 1,     // skip rows already in the sampled giant component
-  OPT_FIND_HALVING = 2,   // path halving during finds
   OPT_S0 = 3,             // level-0 splitter spacing (power of two)
   OPT_SL = 4,             // spacing on higher ranking levels (power of two)
-  OPT_SAMPLE_FULL = 5,    // CAS mode: bitmask of sampling rounds that climb (exact Afforest link)
-  OPT_SAMPLE_MODE = 6,    // 0: propose/accept rounds, 1: CAS rounds
-  OPT_LINK_MODE = 7,      // remaining arcs: 0 row-filtered warps, 1 arc-balanced chunks
   OPT_COMPRESS_MASK = 8,  // bitmask: sampling rounds followed by a compress (bit 0 always honoured)
-  OPT_JUMP = 9,           // list-ranking walkers use 4-step jump tables
+  OPT_GATHER_PREFETCH = 10,  // relaxed w gather issues all 8 first[] loads of a chunk up front
+  OPT_PDL = 11,           // programmatic dependent launch between consecutive kernels
+  // (keys 2, 5, 6, 7, 9: retired experiments -- accepted, ignored)
   OPT_NUM = 16
 };
 extern int g_opt[OPT_NUM];
+
+// ---------------------------------------------------------------------------
+// launches: programmatic dependent launch (PDL).  Every kernel of ours starts
+// with pdl_enter(): it waits until the preceding grid has completed and its
+// writes are visible (griddepcontrol.wait -- a no-op for a normal launch),
+// then allows the next grid to be scheduled.  The next kernel's CTAs are thus
+// resident and waiting while this one drains, instead of paying the launch
+// gap after it (~50 dependent kernels per run; CUDA-graph capture keeps the
+// programmatic edges).  No kernel touches global memory before the wait, so
+// write-after-read across kernels is ordered as with plain launches.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_opt[OPT_PDL] ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 inline void note(KernelKind k) {
   LaunchLog* L = g_log;

@@ -134,6 +134,7 @@ __device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
 // degree ud[v] = deg - nlow[v], scanned later into the edge numbering.
 __global__ void k_chunk_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
                              int* __restrict__ crow, int* __restrict__ ud, int* __restrict__ nlow) {
+  pdl_enter();
   if (ud && blockIdx.x == 0 && threadIdx.x == 0) ud[n] = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
@@ -160,7 +161,7 @@ void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st, int* ud, int* 
     note(K_MEMSET);
   }
   if (nchunks > 0 || ud) {
-    k_chunk_rows<<<grid_for(g.n, 256), 256, 0, st>>>(g.off, g.adj, g.n, crow, ud, nlow);
+    launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.adj, g.n, crow, ud, nlow);
     note(K_CHUNK_ROWS);
   }
 }
@@ -174,6 +175,7 @@ void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st, int* ud, int* 
 template <int kPred, bool kRecord>
 __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int* comp,
                            int2* fe, unsigned long long* __restrict__ prop, PredData pd) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t s = __ldg(off + v);
     int c = v;
@@ -193,6 +195,7 @@ __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __re
 
 // comp = identity; also resets the proposal words (one pass, no memset node)
 __global__ void k_iota(int* __restrict__ comp, int n, unsigned long long* __restrict__ prop) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     comp[v] = v;
     if (prop) prop[v] = ~0ull;
@@ -208,6 +211,7 @@ template <int kPred>
 __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round,
                           int* comp, unsigned long long* prop, PredData pd, const int* __restrict__ nroots,
                           const int* __restrict__ hooks, bool flat) {
+  pdl_enter();
   // participate iff hash < thr / 2^24, thr = min(1, kPerRoot * roots / n);
   // roots at round start = roots counted after round 0 minus later hooks
   uint32_t thr = 1u << 24;
@@ -243,6 +247,7 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
 template <bool kRecord>
 __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
                          unsigned long long* prop, int2* fe, int* hooks) {
+  pdl_enter();
   int hooked = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     unsigned long long key = prop[v];
@@ -279,6 +284,7 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
 constexpr int kL1Steps = 8;
 
 __global__ void k_compress(int* comp, int n, int* nroots) {
+  pdl_enter();
   int roots = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int c = __ldcg(comp + v);
@@ -304,6 +310,7 @@ __global__ void k_compress(int* comp, int n, int* nroots) {
 // Most frequent root among 1024 sampled vertices (one block of 1024):
 // shared-memory open-addressing histogram, then a block argmax.
 __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, bool enable) {
+  pdl_enter();
   constexpr int H = 2048;
   __shared__ int key[H], num[H];
   __shared__ int bestc[32], bestv[32];
@@ -353,6 +360,7 @@ template <int kPred, bool kRecord>
 __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                    int n, int* comp, int2* fe, PredData pd, const Scalars* sc,
                                                    int* heavy_list, int* nheavy) {
+  pdl_enter();
   const int giant = sc->giant;
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -405,6 +413,7 @@ template <int kPred, bool kRecord>
 __global__ void __launch_bounds__(256) k_link_heavy(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                     int* comp, int2* fe, PredData pd, const int* __restrict__ heavy_list,
                                                     const int* __restrict__ nheavy) {
+  pdl_enter();
   const int H = *nheavy;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -443,39 +452,39 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   int cmask = g_opt[OPT_COMPRESS_MASK];
   if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
   if (kRounds > 0) {
-    k_hook_min<kPred, kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, comp, fe, prop, pd);  // round 0
+    launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd);  // round 0
   } else {
-    k_iota<<<gv, B, 0, st>>>(comp, g.n, nullptr);
+    launch(k_iota, gv, B, 0, st, comp, g.n, nullptr);
   }
   note(K_IOTA);
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
     if (r > 0) {
-      k_propose<kPred><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat);
+      launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat);
       note(K_SAMPLE_LINK);
-      k_accept<kRecord><<<gv, B, 0, st>>>(g.off, g.adj, g.n, r, comp, prop, fe, hooks);
+      launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks);
       note(K_ACCEPT);
     }
     if ((cmask >> r) & 1) {
-      k_compress<<<gres, B, 0, st>>>(comp, g.n, r == 0 ? nroots : nullptr);
+      launch(k_compress, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr);
       note(K_COMPRESS);
     }
   }
-  k_find_giant<<<1, 1024, 0, st>>>(comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
+  launch(k_find_giant, 1, 1024, 0, st, comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
   note(K_FIND_GIANT);
   if (g.m > 0) {
     // the proposal words are dead after the last accept: reuse them as the
     // super-heavy row list
     int* heavy = reinterpret_cast<int*>(prop);
     int* nheavy = sc->nheavy + (slot ? 1 : 0);
-    k_link_rows<kPred, kRecord><<<grid_for(g.n, B, 32), B, 0, st>>>(g.off, g.adj, g.n, comp, fe, pd, sc, heavy,
+    launch(k_link_rows<kPred, kRecord>, grid_for(g.n, B, 32), B, 0, st, g.off, g.adj, g.n, comp, fe, pd, sc, heavy,
                                                                     nheavy);
     note(K_LINK_REST);
-    k_link_heavy<kPred, kRecord><<<grid_for((int64_t)kNumSMs * 2048, B), B, 0, st>>>(g.off, g.adj, comp, fe, pd,
+    launch(k_link_heavy<kPred, kRecord>, grid_for((int64_t)kNumSMs * 2048, B), B, 0, st, g.off, g.adj, comp, fe, pd,
                                                                                      heavy, nheavy);
     note(K_LINK_REST);
   }
-  k_compress<<<gres, B, 0, st>>>(comp, g.n, nroots + 7);  // final root count (= components)
+  launch(k_compress, gres, B, 0, st, comp, g.n, nroots + 7);  // final root count (= components)
   note(K_COMPRESS);
 }
 

@@ -30,7 +30,6 @@ struct Rooting {
   int* nxt;        // [2n]  unified tour list successor
   int2* own0;      // [2n]  (segment, offset) per list element
   int* rank0;      // [2n]  tour position of each list element
-  int4* J4;        // [2n]  4-step jump table (level 0, then reused by level 1..)
   // ruling-set levels 1..nlev: element counts and arrays
   int nlev;
   int64_t K[8];

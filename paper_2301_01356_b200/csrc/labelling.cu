@@ -29,6 +29,7 @@ namespace fbcc {
 // head: the block is tree-connected through its head),
 // so the concurrent stores are idempotent.
 __global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restrict__ label, int* head) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int p = __ldg(&rec[v].z);
     if (p >= 0) {
@@ -41,6 +42,7 @@ __global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restri
 // one thread per label: count the block and bump its head's (saturating)
 // headed-count for the articulation rule of bcc.py:229-234
 __global__ void k_count_blocks(int n, const int* __restrict__ head, int* cnt, Scalars* sc) {
+  pdl_enter();
   int blocks = 0;
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
     int h = __ldg(head + l);
@@ -53,6 +55,7 @@ __global__ void k_count_blocks(int n, const int* __restrict__ head, int* cnt, Sc
 
 __global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict__ head,
                      const int* __restrict__ cnt, uint8_t* __restrict__ is_ap) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     bool root = (__ldg(label + v) == v) && (__ldg(head + v) == -1);
     int c = __ldg(cnt + v);
@@ -63,6 +66,7 @@ __global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict
 // upper degree (neighbours > v) of each row; rows are sorted (graphs.py:36-41)
 __global__ void k_upper_degree(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
                                int* __restrict__ ud, int* __restrict__ nlow) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
     if (v == n) { ud[n] = 0; continue; }
     int64_t lo = __ldg(off + v), hi = __ldg(off + v + 1);
@@ -119,6 +123,7 @@ __global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__
                                                      int n, int64_t m, const int* __restrict__ label,
                                                      const int* __restrict__ head, const int* __restrict__ uoff,
                                                      const int* __restrict__ nlow, int* eblk, int* bmin) {
+  pdl_enter();
   EdgeBlockVisitor vis;
   vis.off = off;
   vis.label = label;
@@ -133,12 +138,14 @@ __global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__
 }
 
 __global__ void k_edge_final(int* eblk, const int* __restrict__ bmin, const int* __restrict__ uoff, int n) {
+  pdl_enter();
   const int E = uoff[n];
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x)
     eblk[e] = __ldg(bmin + eblk[e]);
 }
 
-__global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) { sc->num_edges = uoff[n]; }
+__global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) {
+  pdl_enter(); sc->num_edges = uoff[n]; }
 
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
@@ -147,12 +154,12 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   const int B = 256;
   const int gv = grid_for(n + 1, B);
   // head = -1, cnt = 0, bmin = INF were initialised by the stage-4 kernel
-  k_heads<<<gv, B, 0, st>>>(n, rec, label, head);
+  launch(k_heads, gv, B, 0, st, n, rec, label, head);
   note(K_HEADS);
-  k_count_blocks<<<gv, B, 0, st>>>(n, head, cnt, sc);
+  launch(k_count_blocks, gv, B, 0, st, n, head, cnt, sc);
   note(K_HEADS);
   if (is_ap) {
-    k_ap<<<gv, B, 0, st>>>(n, label, head, cnt, is_ap);
+    launch(k_ap, gv, B, 0, st, n, label, head, cnt, is_ap);
     note(K_AP);
   }
   // edge ids: ud (computed with the chunk table at run start) -> exclusive
@@ -160,14 +167,14 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   int* ud = uoff + (n + 1);
   exclusive_scan(ud, uoff, n + 1, cub_tmp, cub_bytes, st);
   note(K_SCAN);
-  k_set_edges<<<1, 1, 0, st>>>(uoff, n, sc);
+  launch(k_set_edges, 1, 1, 0, st, uoff, n, sc);
   note(K_SET_EDGES);
   if (edge_label && g.m > 0) {
     int64_t nchunks = (g.m + kItems - 1) / kItems;
-    k_edge_blocks<<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow,
+    launch(k_edge_blocks, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow,
                                                           edge_label, bmin);
     note(K_EDGE_BLOCKS);
-    k_edge_final<<<grid_for(g.m / 2, B), B, 0, st>>>(edge_label, bmin, uoff, n);
+    launch(k_edge_final, grid_for(g.m / 2, B), B, 0, st, edge_label, bmin, uoff, n);
     note(K_EDGE_FINAL);
   }
 }
@@ -177,6 +184,7 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
 // ---------------------------------------------------------------------------
 __global__ void k_export(int n, const int4* __restrict__ rec, const int4* __restrict__ AP, int* parent, int* first,
                          int* last, int* w1, int* w2, uint8_t* fence) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
     if (parent) parent[v] = r.z;
@@ -195,7 +203,7 @@ void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* A
                   int* first, int* last, int* w1, int* w2, uint8_t* fence, cudaStream_t st) {
   if (forest) cudaMemcpyAsync(forest, fe, sizeof(int2) * g.n, cudaMemcpyDeviceToDevice, st);
   if (parent || first || last || w1 || w2 || fence)
-    k_export<<<grid_for(g.n, 256), 256, 0, st>>>(g.n, rec, AP, parent, first, last, w1, w2, fence);
+    launch(k_export, grid_for(g.n, 256), 256, 0, st, g.n, rec, AP, parent, first, last, w1, w2, fence);
 }
 
 }  // namespace fbcc

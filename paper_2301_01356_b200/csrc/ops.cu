@@ -35,6 +35,7 @@ __device__ __forceinline__ void raise_err(Scalars* sc, int bit) { atomicOr(&sc->
 // then rank = dist(head) - dist(e).  O(L log L), but this entry point only
 // serves the stand-alone API; the pipeline uses the ruling-set ranking.
 __global__ void k_lr_init(const int* __restrict__ nxt, int64_t L, int* ptr, int* dist, int* indeg, Scalars* sc) {
+  pdl_enter();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < L; e += (int64_t)gridDim.x * blockDim.x) {
     int s = nxt[e];
     if (s >= L || s < -1) { raise_err(sc, E_COVER); s = -1; }
@@ -45,6 +46,7 @@ __global__ void k_lr_init(const int* __restrict__ nxt, int64_t L, int* ptr, int*
 }
 
 __global__ void k_lr_jump(int64_t L, const int* __restrict__ p0, const int* __restrict__ d0, int* p1, int* d1) {
+  pdl_enter();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < L; e += (int64_t)gridDim.x * blockDim.x) {
     int p = p0[e];
     d1[e] = d0[e] + (p != (int)e ? d0[p] : 0);
@@ -54,6 +56,7 @@ __global__ void k_lr_jump(int64_t L, const int* __restrict__ p0, const int* __re
 
 __global__ void k_lr_heads(const int* __restrict__ heads, int64_t H, int64_t L, const int* __restrict__ nxt,
                            const int* __restrict__ ptr, const int* __restrict__ indeg, int* tailhead, Scalars* sc) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H; i += (int64_t)gridDim.x * blockDim.x) {
     int h = heads[i];
     if (h < 0) continue;  // ignored, like the reference
@@ -67,6 +70,7 @@ __global__ void k_lr_heads(const int* __restrict__ heads, int64_t H, int64_t L, 
 
 __global__ void k_lr_ranks(int64_t L, const int* __restrict__ nxt, const int* __restrict__ ptr,
                            const int* __restrict__ dist, const int* __restrict__ tailhead, int* ranks, Scalars* sc) {
+  pdl_enter();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < L; e += (int64_t)gridDim.x * blockDim.x) {
     int t = ptr[e];
     int h = nxt[t] < 0 ? tailhead[t] : -1;
@@ -88,18 +92,18 @@ int op_list_ranking(const int* nxt, int64_t L, const int* heads, int64_t H, int*
   int* d1 = (int*)take(4 * L);
   int* indeg = (int*)take(4 * L);
   cudaMemsetAsync(indeg, 0, 4 * L, st);
-  k_lr_init<<<grid_for(L, B), B, 0, st>>>(nxt, L, p0, d0, indeg, sc);
+  launch(k_lr_init, grid_for(L, B), B, 0, st, nxt, L, p0, d0, indeg, sc);
   int rounds = 1;
   while ((1ll << rounds) < L + 1) rounds++;
   for (int r = 0; r < rounds; r++) {
-    k_lr_jump<<<grid_for(L, B), B, 0, st>>>(L, p0, d0, p1, d1);
+    launch(k_lr_jump, grid_for(L, B), B, 0, st, L, p0, d0, p1, d1);
     int* t = p0; p0 = p1; p1 = t;
     t = d0; d0 = d1; d1 = t;
   }
   int* tailhead = p1;  // reuse
   cudaMemsetAsync(tailhead, 0xFF, 4 * L, st);
-  if (H > 0) k_lr_heads<<<grid_for(H, B), B, 0, st>>>(heads, H, L, nxt, p0, indeg, tailhead, sc);
-  k_lr_ranks<<<grid_for(L, B), B, 0, st>>>(L, nxt, p0, d0, tailhead, ranks, sc);
+  if (H > 0) launch(k_lr_heads, grid_for(H, B), B, 0, st, heads, H, L, nxt, p0, indeg, tailhead, sc);
+  launch(k_lr_ranks, grid_for(L, B), B, 0, st, L, nxt, p0, d0, tailhead, ranks, sc);
   return 0;
 }
 
@@ -107,6 +111,7 @@ int op_list_ranking(const int* nxt, int64_t L, const int* heads, int64_t H, int*
 // build_euler_tour: root a given forest (pairs) at min-id roots
 // ---------------------------------------------------------------------------
 __global__ void k_pairs_check(const int2* __restrict__ pairs, int64_t k, int n, Scalars* sc) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
     int2 e = pairs[i];
     if (e.x < 0 || e.x >= n || e.y < 0 || e.y >= n) raise_err(sc, E_RANGE);
@@ -114,12 +119,14 @@ __global__ void k_pairs_check(const int2* __restrict__ pairs, int64_t k, int n, 
 }
 
 __global__ void k_iota2(int* comp, int n) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) comp[v] = v;
 }
 
 // union the pairs (labels not given): a pair whose ends are already joined
 // closes a cycle -- not a forest
 __global__ void k_union_pairs(const int2* __restrict__ pairs, int64_t k, int n, int* comp, Scalars* sc) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
     int2 e = pairs[i];
     if (e.x < 0 || e.x >= n || e.y < 0 || e.y >= n) continue;  // reported by k_pairs_check
@@ -135,6 +142,7 @@ __global__ void k_union_pairs(const int2* __restrict__ pairs, int64_t k, int n, 
 }
 
 __global__ void k_flatten(int* comp, int n) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int c = comp[v];
     while (comp[c] != c) c = comp[c];
@@ -143,6 +151,7 @@ __global__ void k_flatten(int* comp, int n) {
 }
 
 __global__ void k_nonroot_flags(const int* __restrict__ comp, int n, int* flags) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x)
     flags[v] = v < n ? (comp[v] != v) : 0;
 }
@@ -153,6 +162,7 @@ __global__ void k_nonroot_flags(const int* __restrict__ comp, int n, int* flags)
 __global__ void k_place_pairs(const int2* __restrict__ pairs, int64_t k, const int* __restrict__ comp,
                               const int* __restrict__ nrank, int n, int2* fe, unsigned long long* keys, int* vals,
                               Scalars* sc) {
+  pdl_enter();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     if (comp[x] == x) continue;
     int i = nrank[x];
@@ -170,6 +180,7 @@ __global__ void k_place_pairs(const int2* __restrict__ pairs, int64_t k, const i
 
 __global__ void k_sorted_lists(const unsigned long long* __restrict__ keys, const int* __restrict__ vals, int64_t K2,
                                int* lhead, int* nexto) {
+  pdl_enter();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K2; j += (int64_t)gridDim.x * blockDim.x) {
     unsigned vx = (unsigned)(keys[j] >> 32);
     if (j == 0 || (unsigned)(keys[j - 1] >> 32) != vx) lhead[vx] = vals[j];
@@ -179,12 +190,14 @@ __global__ void k_sorted_lists(const unsigned long long* __restrict__ keys, cons
 
 __global__ void k_check_rooted(const int* __restrict__ comp, const int* __restrict__ lhead, int n,
                                const int* __restrict__ nrank, int64_t k, Scalars* sc) {
+  pdl_enter();
   if (blockIdx.x == 0 && threadIdx.x == 0 && nrank[n] != k) raise_err(sc, E_LABELS);  // #non-roots != #edges
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
     if (comp[v] != v && lhead[v] < 0) raise_err(sc, E_LABELS);  // non-root without a tree edge
 }
 
 __global__ void k_export_forest(const int4* __restrict__ rec, int n, int* parent, int* first, int* last) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
     parent[v] = r.z;
@@ -198,6 +211,7 @@ __global__ void k_export_forest(const int4* __restrict__ rec, int n, int* parent
 // ---------------------------------------------------------------------------
 __global__ void k_rec_ap(const int* __restrict__ parent, const int* __restrict__ first, const int* __restrict__ last,
                          int n, int4* rec, int4* AP) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int f = first[v], l = last[v];
     rec[v] = make_int4(f, l, parent[v], 0);
@@ -211,6 +225,7 @@ __global__ void k_rec_ap(const int* __restrict__ parent, const int* __restrict__
 // ---------------------------------------------------------------------------
 __global__ void k_block_keys(const int* __restrict__ label, const int* __restrict__ head, int n,
                              unsigned long long* keys, int* cnt) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int l = label[v];
     bool member = head[l] != -1;
@@ -224,6 +239,7 @@ __global__ void k_block_keys(const int* __restrict__ label, const int* __restric
 }
 
 __global__ void k_block_bounds(const unsigned long long* __restrict__ keys, int64_t K, int* vtx, int* flags) {
+  pdl_enter();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long k = keys[j];
     bool valid = k != ~0ull;
@@ -234,6 +250,7 @@ __global__ void k_block_bounds(const unsigned long long* __restrict__ keys, int6
 
 __global__ void k_block_offsets(const int* __restrict__ flags, const int* __restrict__ fscan, int64_t K,
                                 const unsigned long long* __restrict__ keys, int* boff, Scalars* sc) {
+  pdl_enter();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
     if (flags[j]) boff[fscan[j]] = (int)j;
     if (keys[j] != ~0ull && (j + 1 == K || keys[j + 1] == ~0ull)) {  // last valid key
@@ -249,6 +266,7 @@ __global__ void k_block_offsets(const int* __restrict__ flags, const int* __rest
 // ---------------------------------------------------------------------------
 __global__ void k_sym_keys(const int64_t* __restrict__ u, const int64_t* __restrict__ v, int64_t k, int64_t n,
                            unsigned long long* keys, Scalars* sc) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t a = u[i], b = v[i];
     if (a < 0 || a >= n || b < 0 || b >= n) { raise_err(sc, E_RANGE); a = b = 0; }
@@ -260,6 +278,7 @@ __global__ void k_sym_keys(const int64_t* __restrict__ u, const int64_t* __restr
 
 __global__ void k_sym_csr(const unsigned long long* __restrict__ ukeys, const int* __restrict__ nuniq, int64_t n,
                           int64_t* off, uint32_t* edges, Scalars* sc) {
+  pdl_enter();
   int64_t m = *nuniq;
   if (m > 0 && ukeys[m - 1] == ~0ull) m--;  // the self-loop sentinel sorts last
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += (int64_t)gridDim.x * blockDim.x) {
@@ -304,11 +323,11 @@ int op_symmetrize(const int64_t* u, const int64_t* v, int64_t k, int64_t n, int6
   void* tmp = take(tmp_bytes);
   cudaMemsetAsync(nuniq, 0, 64, st);
   if (K > 0) {
-    k_sym_keys<<<grid_for(k, B), B, 0, st>>>(u, v, k, n, a, sc);
+    launch(k_sym_keys, grid_for(k, B), B, 0, st, u, v, k, n, a, sc);
     cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, a, b, (int)K, 0, 64, st);
     cub::DeviceSelect::Unique(tmp, tmp_bytes, b, a, nuniq, (int)K, st);
   }
-  k_sym_csr<<<grid_for(n + 1, B), B, 0, st>>>(a, nuniq, n, off, edges, sc);
+  launch(k_sym_csr, grid_for(n + 1, B), B, 0, st, a, nuniq, n, off, edges, sc);
   return 0;
 }
 
@@ -339,12 +358,12 @@ int op_extract_bccs(const int* label, const int* head, int64_t n, int* block_off
   if (sb > tmp_bytes) tmp_bytes = sb;
   void* tmp = take(tmp_bytes);
   if (K == 0) return 0;
-  k_block_keys<<<grid_for(n, B), B, 0, st>>>(label, head, (int)n, a, nullptr);
+  launch(k_block_keys, grid_for(n, B), B, 0, st, label, head, (int)n, a, nullptr);
   cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, a, b, (int)K, 0, 64, st);
-  k_block_bounds<<<grid_for(K, B), B, 0, st>>>(b, K, block_vtx, flags);
+  launch(k_block_bounds, grid_for(K, B), B, 0, st, b, K, block_vtx, flags);
   size_t sbytes = tmp_bytes;
   cub::DeviceScan::ExclusiveSum(tmp, sbytes, flags, fscan, (int)K, st);
-  k_block_offsets<<<grid_for(K, B), B, 0, st>>>(flags, fscan, K, b, block_off, sc);
+  launch(k_block_offsets, grid_for(K, B), B, 0, st, flags, fscan, K, b, block_off, sc);
   return 0;
 }
 
@@ -369,7 +388,6 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   size_t o_comp = L.take(4 * n), o_fe = L.take(8 * n), o_flags = L.take(4 * (n + 1)), o_nrank = L.take(4 * (n + 1));
   size_t o_rootidx = L.take(4 * (n + 1)), o_rlist = L.take(4 * n), o_lhead = L.take(4 * n),
          o_nexto = L.take(4 * N0), o_nxt = L.take(4 * N0), o_own0 = L.take(8 * N0), o_rank0 = L.take(4 * N0),
-         o_j4 = L.take(16 * N0),
          o_rec = L.take(16 * n), o_ap = L.take(16 * (size_t)(N0 + kTile));
   size_t o_keys = L.take(8 * 2 * k + 8), o_keys2 = L.take(8 * 2 * k + 8), o_vals = L.take(4 * 2 * k + 4),
          o_vals2 = L.take(4 * 2 * k + 4);
@@ -409,7 +427,6 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   R.nxt = (int*)at(o_nxt);
   R.own0 = (int2*)at(o_own0);
   R.rank0 = (int*)at(o_rank0);
-  R.J4 = (int4*)at(o_j4);
   R.rec = (int4*)at(o_rec);
   R.nlev = nlev;
   for (int l = 0; l < 8; l++) {
@@ -434,27 +451,27 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   int* vals2 = (int*)at(o_vals2);
 
   const int gv = grid_for(n + 1, B);
-  if (k > 0) k_pairs_check<<<grid_for(k, B), B, 0, st>>>(pairs, k, (int)n, sc);
+  if (k > 0) launch(k_pairs_check, grid_for(k, B), B, 0, st, pairs, k, (int)n, sc);
   if (labels) {
     cudaMemcpyAsync(comp, labels, 4 * n, cudaMemcpyDeviceToDevice, st);
   } else {
-    k_iota2<<<gv, B, 0, st>>>(comp, (int)n);
-    if (k > 0) k_union_pairs<<<grid_for(k, B), B, 0, st>>>(pairs, k, (int)n, comp, sc);
-    k_flatten<<<gv, B, 0, st>>>(comp, (int)n);
+    launch(k_iota2, gv, B, 0, st, comp, (int)n);
+    if (k > 0) launch(k_union_pairs, grid_for(k, B), B, 0, st, pairs, k, (int)n, comp, sc);
+    launch(k_flatten, gv, B, 0, st, comp, (int)n);
   }
   // pair i -> i-th non-root vertex
-  k_nonroot_flags<<<gv, B, 0, st>>>(comp, (int)n, R.flags);
+  launch(k_nonroot_flags, gv, B, 0, st, comp, (int)n, R.flags);
   exclusive_scan(R.flags, nrank, n + 1, R.cub_tmp, R.cub_bytes, st);
   rooting_roots((int)n, comp, R, sc, st);  // rootidx, rlist, c; clears lhead
   if (k > 0) {
-    k_place_pairs<<<gv, B, 0, st>>>(pairs, k, comp, nrank, (int)n, fe, keys, vals, sc);
+    launch(k_place_pairs, gv, B, 0, st, pairs, k, comp, nrank, (int)n, fe, keys, vals, sc);
     size_t sb = R.cub_bytes;
     cub::DeviceRadixSort::SortPairs(R.cub_tmp, sb, keys, keys2, vals, vals2, (int)(2 * k), 0, 64, st);
-    k_sorted_lists<<<grid_for(2 * k, B), B, 0, st>>>(keys2, vals2, 2 * k, R.lhead, R.nexto);
+    launch(k_sorted_lists, grid_for(2 * k, B), B, 0, st, keys2, vals2, 2 * k, R.lhead, R.nexto);
   }
-  k_check_rooted<<<gv, B, 0, st>>>(comp, R.lhead, (int)n, nrank, k, sc);
+  launch(k_check_rooted, gv, B, 0, st, comp, R.lhead, (int)n, nrank, k, sc);
   rooting_tour((int)n, comp, fe, R, AP, sc, st);
-  k_export_forest<<<gv, B, 0, st>>>(R.rec, (int)n, parent, first, last);
+  launch(k_export_forest, gv, B, 0, st, R.rec, (int)n, parent, first, last);
   return 0;
 }
 
@@ -490,7 +507,7 @@ int op_compute_tags(const Graph& g, const int* parent, const int* first, const i
   T.ntile = ntile;
   T.tlev = tlev;
   int* scr = (int*)at(o_scr);
-  k_rec_ap<<<grid_for(n, B), B, 0, st>>>(parent, first, last, (int)n, R.rec, T.AP);
+  launch(k_rec_ap, grid_for(n, B), B, 0, st, parent, first, last, (int)n, R.rec, T.AP);
   stage3_tags(gg, R, T, st, /*exact=*/true);
   stage4_fence(gg, R, T, low, high, scr, scr + n, scr + 2 * n, st);
   export_debug(gg, nullptr, R.rec, T.AP, nullptr, nullptr, nullptr, nullptr, w1, w2, nullptr, st);

@@ -61,6 +61,7 @@ void exclusive_scan(const int* in, int* out, int64_t items, void* tmp, size_t tm
 // ---------------------------------------------------------------------------
 // (also clears the out-arc list heads: same index space, no memset node)
 __global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restrict__ flags, int* __restrict__ lhead) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
     flags[v] = (v < n) ? (__ldg(comp + v) == v) : 0;
     if (v < n) lhead[v] = -1;
@@ -70,6 +71,7 @@ __global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restric
 // rlist[rank among roots] = root;  sc->ncomp = c
 __global__ void k_root_list(const int* __restrict__ comp, const int* __restrict__ rootidx, int n,
                             int* __restrict__ rlist, Scalars* sc) {
+  pdl_enter();
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid == 0) sc->ncomp = rootidx[n];
   for (int r = (int)tid; r < n; r += gridDim.x * blockDim.x)
@@ -79,6 +81,7 @@ __global__ void k_root_list(const int* __restrict__ comp, const int* __restrict_
 // out-arc lists: arc 2x = u->v is an out-arc of u, 2x+1 = v->u of v
 __global__ void k_out_lists(const int* __restrict__ comp, const int2* __restrict__ fe, int n, int* lhead,
                             int* __restrict__ nexto) {
+  pdl_enter();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     if (__ldg(comp + x) == x) continue;
     int2 e = __ldg(fe + x);
@@ -87,10 +90,34 @@ __global__ void k_out_lists(const int* __restrict__ comp, const int2* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// ruling-set list ranking
+// ---------------------------------------------------------------------------
+// splitter of window j (element j*S + hashed offset; window 0 uses element 0,
+// the list head; the last, partial window is clamped into range); S = 1 << sh
+__device__ __forceinline__ int split_elem(int j, int sh, int N) {
+  int e = (j << sh) + (j == 0 ? 0 : (int)(hash32((uint32_t)j * 0x9E3779B1u + 0x7F4A7C15u) & ((1u << sh) - 1)));
+  return e < N ? e : N - 1;
+}
+__device__ __forceinline__ bool is_split(int e, int sh, int N) { return split_elem(e >> sh, sh, N) == e; }
+
+// Successor encoding on every ranking level: s >= 0 is an ordinary next
+// element, -1 ends the list, s <= -2 says the next element ~s is a splitter
+// of the level's windowing (the head, element 0, is nobody's successor, so
+// ~0 = -1 is free).  The producer of the array -- k_link_tour for level 0,
+// the walkers of level l for level l+1 -- tests the target once, so a walker
+// step is one dependent load and a sign test: the walk's critical path is
+// the L2 round trip alone (the hash test and 64-bit division it replaced
+// added ~100 cycles per step, and the slowest walker takes ~S ln K steps).
+__device__ __forceinline__ int flag_succ(int s, int sh, int N) {
+  return (s >= 0 && sh >= 0 && is_split(s, sh, N)) ? ~s : s;
+}
+
 __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict__ fe,
                             const int* __restrict__ lhead, const int* __restrict__ nexto,
                             const int* __restrict__ rootidx, const int* __restrict__ rlist, int n,
-                            int* __restrict__ nxt, const Scalars* sc) {
+                            int* __restrict__ nxt, const Scalars* sc, int sh0) {
+  pdl_enter();
   const int c = sc->ncomp;
   const int64_t N = 2 * (int64_t)n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
@@ -111,89 +138,27 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
       if (nx >= 0) out = nx;
       else out = (__ldg(comp + t) == t) ? 2 * t + 1 : __ldg(lhead + t);
     }
-    nxt[e] = out;
+    nxt[e] = flag_succ(out, sh0, (int)N);
   }
 }
 
-// ---------------------------------------------------------------------------
-// ruling-set list ranking
-// ---------------------------------------------------------------------------
-// splitter of window j (element j*S + hashed offset; window 0 uses element 0,
-// the list head; the last, partial window is clamped into range)
-__device__ __forceinline__ int64_t split_elem(int64_t j, int S, int64_t N) {
-  int64_t e = j * S + (j == 0 ? 0 : (hash32((uint32_t)j * 0x9E3779B1u + 0x7F4A7C15u) & (S - 1)));
-  return e < N ? e : N - 1;
-}
-
 template <bool kWeighted>
-__global__ void __launch_bounds__(256) k_walk(int64_t K, int S, int64_t N, const int* __restrict__ succ,
+__global__ void __launch_bounds__(256) k_walk(int K, int sh, int N, const int* __restrict__ succ,
                                               const int* __restrict__ w, int2* __restrict__ own,
-                                              int* __restrict__ succ_next, int* __restrict__ w_next) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
-    int64_t e = split_elem(j, S, N);
+                                              int* __restrict__ succ_next, int* __restrict__ w_next, int sh_next) {
+  pdl_enter();
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K; j += gridDim.x * blockDim.x) {
+    int e = split_elem(j, sh, N);
     int acc = 0;
-    int nj = -1;
+    int s;
     while (true) {
-      own[e] = make_int2((int)j, acc);
+      own[e] = make_int2(j, acc);
       acc += kWeighted ? __ldg(w + e) : 1;
-      int e2 = __ldg(succ + e);
-      if (e2 < 0) break;
-      int64_t j2 = e2 / S;
-      if (split_elem(j2, S, N) == e2) { nj = (int)j2; break; }
-      e = e2;
+      s = __ldg(succ + e);
+      if (s < 0) break;
+      e = s;
     }
-    succ_next[j] = nj;
-    w_next[j] = acc;
-  }
-}
-
-// Jump tables: each walker step is one DEPENDENT load (an L2 round trip,
-// ~0.3 us), and the last walker of a level needs ~S ln K steps.  J4[e] =
-// the next four elements (two fully parallel gather passes build it), so a
-// walker advances four elements per dependent load; -1 propagates past a
-// list end.
-__global__ void k_jump2(int64_t N, const int* __restrict__ succ, int2* __restrict__ J2) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
-    int s1 = __ldg(succ + e);
-    J2[e] = make_int2(s1, s1 >= 0 ? __ldg(succ + s1) : -1);
-  }
-}
-
-__global__ void k_jump4(int64_t N, const int2* __restrict__ J2, int4* __restrict__ J4) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
-    int2 a = __ldg(J2 + e);
-    int2 b = a.y >= 0 ? __ldg(J2 + a.y) : make_int2(-1, -1);
-    J4[e] = make_int4(a.x, a.y, b.x, b.y);
-  }
-}
-
-template <bool kWeighted>
-__global__ void __launch_bounds__(256) k_walk4(int64_t K, int S, int64_t N, const int4* __restrict__ J4,
-                                               const int* __restrict__ w, int2* __restrict__ own,
-                                               int* __restrict__ succ_next, int* __restrict__ w_next) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
-    int e = (int)split_elem(j, S, N);
-    int acc = 0;
-    int nj = -1;
-    own[e] = make_int2((int)j, acc);
-    acc += kWeighted ? __ldg(w + e) : 1;
-    bool stop = false;
-    while (!stop) {
-      int4 q = __ldg(J4 + e);
-      const int xs[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-      for (int t = 0; t < 4; t++) {
-        if (stop) break;
-        int x = xs[t];
-        if (x < 0) { stop = true; break; }
-        int64_t j2 = x / S;
-        if (split_elem(j2, S, N) == x) { nj = (int)j2; stop = true; break; }
-        own[x] = make_int2((int)j, acc);
-        acc += kWeighted ? __ldg(w + x) : 1;
-      }
-      e = q.w;
-    }
-    succ_next[j] = nj;
+    succ_next[j] = (s == -1) ? -1 : flag_succ((~s) >> sh, sh_next, K);
     w_next[j] = acc;
   }
 }
@@ -210,6 +175,7 @@ constexpr size_t kFinalSmem = 2 * sizeof(int) * kFinalMax + 4 * sizeof(int) * kF
 
 __global__ void __launch_bounds__(kFinalThreads) k_final_rank(int K, const int* __restrict__ succ,
                                                               const int* __restrict__ w, int* __restrict__ offs) {
+  pdl_enter();
   extern __shared__ int fsm[];
   int* S = fsm;                    // succ, then owner walker
   int* W = fsm + kFinalMax;        // weight, then offset inside the walker's segment
@@ -218,29 +184,28 @@ __global__ void __launch_bounds__(kFinalThreads) k_final_rank(int K, const int* 
   int* PS = WS + kFinalThreads;    // walker predecessor
   int* VS = PS + kFinalThreads;    // walker exclusive prefix
   const int t = threadIdx.x;
+  int qs = 0;  // one more ruling level in smem: windows of Q = 1 << qs elements
+  while ((kFinalThreads << qs) < K) qs++;
+  const int nwin = (K + (1 << qs) - 1) >> qs;
   for (int j = t; j < K; j += kFinalThreads) {
-    S[j] = succ[j];
+    S[j] = flag_succ(succ[j], qs, K);
     W[j] = w[j];
   }
-  int Q = 1;
-  while (Q * kFinalThreads < K) Q <<= 1;
-  const int nwin = (K + Q - 1) / Q;
   PS[t] = -1;
   __syncthreads();
   if (t < nwin) {
-    int e = (int)split_elem(t, Q, K);
-    int acc = 0, nj = -1;
+    int e = split_elem(t, qs, K);
+    int acc = 0, s;
     while (true) {
-      int s = S[e], wt = W[e];
+      s = S[e];
+      int wt = W[e];
       S[e] = t;
       W[e] = acc;
       acc += wt;
       if (s < 0) break;
-      int j2 = s / Q;
-      if ((int)split_elem(j2, Q, K) == s) { nj = j2; break; }
       e = s;
     }
-    SS[t] = nj;
+    SS[t] = (s == -1) ? -1 : (~s) >> qs;
     WS[t] = acc;
   }
   __syncthreads();
@@ -265,6 +230,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_final_rank(int K, const int* 
 
 __global__ void k_expand(int64_t K, const int2* __restrict__ own, const int* __restrict__ offs_up,
                          int* __restrict__ offs) {
+  pdl_enter();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
     int2 o = own[j];
     offs[j] = __ldg(offs_up + o.x) + o.y;
@@ -286,6 +252,7 @@ __device__ __forceinline__ void place(int v, int f, int l, int par, int4* rec, i
 // instead of competing with the positions kernel's scattered stores)
 __global__ void k_rank0(int64_t N, const int2* __restrict__ own0, const int* __restrict__ offs1,
                         int* __restrict__ rank0) {
+  pdl_enter();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
     int2 o = __ldg(own0 + e);
     rank0[e] = __ldg(offs1 + o.x) + o.y;
@@ -295,6 +262,7 @@ __global__ void k_rank0(int64_t N, const int2* __restrict__ own0, const int* __r
 __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict__ fe,
                             const int2* __restrict__ rank0, int n, int4* __restrict__ rec,
                             int4* __restrict__ AP) {
+  pdl_enter();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     int2 r = __ldg(rank0 + x);  // ranks of elements 2x and 2x+1, one 8-byte load
     if (__ldg(comp + x) == x) {
@@ -311,11 +279,11 @@ __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict
 void rooting_roots(int n, const int* comp, Rooting& R, Scalars* sc, cudaStream_t st) {
   const int B = 256;
   const int gv = grid_for(n + 1, B);
-  k_root_flags<<<gv, B, 0, st>>>(comp, n, R.flags, R.lhead);
+  launch(k_root_flags, gv, B, 0, st, comp, n, R.flags, R.lhead);
   note(K_ROOT_FLAGS);
   exclusive_scan(R.flags, R.rootidx, n + 1, R.cub_tmp, R.cub_bytes, st);
   note(K_SCAN);
-  k_root_list<<<gv, B, 0, st>>>(comp, R.rootidx, n, R.rlist, sc);
+  launch(k_root_list, gv, B, 0, st, comp, R.rootidx, n, R.rlist, sc);
   note(K_ROOT_LIST);
 }
 
@@ -324,7 +292,7 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
   rooting_roots(g.n, comp, R, sc, st);
   // Euler circuit: out-arc lists in atomicExch order (any order is a valid
   // tour; the final outputs do not depend on it)
-  k_out_lists<<<grid_for(g.n, 256), 256, 0, st>>>(comp, fe, g.n, R.lhead, R.nexto);
+  launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto);
   note(K_TREE_DEGREE);
   rooting_tour(g.n, comp, fe, R, AP, sc, st);
 }
@@ -333,49 +301,35 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
 void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc, cudaStream_t st) {
   const int B = 256;
   const int gv = grid_for(n + 1, B);
-  k_link_tour<<<grid_for(2 * (int64_t)n, B), B, 0, st>>>(comp, fe, R.lhead, R.nexto, R.rootidx, R.rlist, n, R.nxt,
-                                                         sc);
+  const int N0 = 2 * n;
+  auto shift = [](int S) { return __builtin_ctz((unsigned)S); };
+  // levels 1..nlev-1 are walked again (their successors carry splitter flags
+  // for the next windowing); level nlev goes to the one-CTA final kernel
+  auto sh_after = [&](int l) { return l < R.nlev ? shift(R.S[l]) : -1; };
+  launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.nexto, R.rootidx, R.rlist, n, R.nxt, sc,
+                                             shift(R.S[0]));
   note(K_LINK_SLOTS);
   // ruling-set levels
-  const int64_t N0 = 2 * (int64_t)n;
-  const bool jump = g_opt[OPT_JUMP] != 0;
-  if (jump) {  // own0 doubles as the J2 scratch: the walk overwrites it afterwards
-    k_jump2<<<grid_for(N0, B), B, 0, st>>>(N0, R.nxt, R.own0);
-    note(K_JUMP);
-    k_jump4<<<grid_for(N0, B), B, 0, st>>>(N0, R.own0, R.J4);
-    note(K_JUMP);
-    k_walk4<false><<<grid_for(R.K[1], B, 64), B, 0, st>>>(R.K[1], R.S[0], N0, R.J4, nullptr, R.own0, R.succ[1],
-                                                          R.wgt[1]);
-  } else {
-    k_walk<false><<<grid_for(R.K[1], B, 64), B, 0, st>>>(R.K[1], R.S[0], N0, R.nxt, nullptr, R.own0,
-                                                         R.succ[1], R.wgt[1]);
-  }
+  launch(k_walk<false>, grid_for(R.K[1], B, 64), B, 0, st, (int)R.K[1], shift(R.S[0]), N0, R.nxt, nullptr, R.own0,
+                                                       R.succ[1], R.wgt[1], sh_after(1));
   note(K_WALK0);
   for (int l = 1; l < R.nlev; l++) {
-    if (jump) {  // J2 scratch: own[l]; J4 reuses the level-0 table's storage
-      k_jump2<<<grid_for(R.K[l], B), B, 0, st>>>(R.K[l], R.succ[l], R.own[l]);
-      note(K_JUMP);
-      k_jump4<<<grid_for(R.K[l], B), B, 0, st>>>(R.K[l], R.own[l], R.J4);
-      note(K_JUMP);
-      k_walk4<true><<<grid_for(R.K[l + 1], B, 64), B, 0, st>>>(R.K[l + 1], R.S[l], R.K[l], R.J4, R.wgt[l],
-                                                               R.own[l], R.succ[l + 1], R.wgt[l + 1]);
-    } else {
-      k_walk<true><<<grid_for(R.K[l + 1], B, 64), B, 0, st>>>(R.K[l + 1], R.S[l], R.K[l], R.succ[l], R.wgt[l],
-                                                              R.own[l], R.succ[l + 1], R.wgt[l + 1]);
-    }
+    launch(k_walk<true>, grid_for(R.K[l + 1], B, 64), B, 0, st, (int)R.K[l + 1], shift(R.S[l]), (int)R.K[l], R.succ[l],
+                                                            R.wgt[l], R.own[l], R.succ[l + 1], R.wgt[l + 1],
+                                                            sh_after(l + 1));
     note(K_WALKL);
   }
   cudaFuncSetAttribute(k_final_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinalSmem);
-  k_final_rank<<<1, kFinalThreads, kFinalSmem, st>>>((int)R.K[R.nlev], R.succ[R.nlev], R.wgt[R.nlev],
+  launch(k_final_rank, 1, kFinalThreads, kFinalSmem, st, (int)R.K[R.nlev], R.succ[R.nlev], R.wgt[R.nlev],
                                                       R.offs[R.nlev]);
   note(K_FINAL_RANK);
   for (int l = R.nlev - 1; l >= 1; l--) {
-    k_expand<<<grid_for(R.K[l], B), B, 0, st>>>(R.K[l], R.own[l], R.offs[l + 1], R.offs[l]);
+    launch(k_expand, grid_for(R.K[l], B), B, 0, st, R.K[l], R.own[l], R.offs[l + 1], R.offs[l]);
     note(K_EXPAND);
   }
-  k_rank0<<<grid_for(N0, B), B, 0, st>>>(N0, R.own0, R.offs[1], R.rank0);
+  launch(k_rank0, grid_for(N0, B), B, 0, st, N0, R.own0, R.offs[1], R.rank0);
   note(K_EXPAND);
-  k_positions<<<gv, B, 0, st>>>(comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP);
+  launch(k_positions, gv, B, 0, st, comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP);
   note(K_POSITIONS);
 }
 

@@ -44,14 +44,20 @@ __device__ __forceinline__ int2 filler() { return make_int2(kINF, -1); }
 // and every subtree aggregate low/high, unchanged -- only the intermediate
 // w2 of v may grow (SURVEY §8(c) rung 3 checks both forms).  RMAT: 1.05e9
 // gathers from a 134 MB array (mostly L2) instead of a 537 MB one.
-template <bool kExact>
+template <bool kExact, bool kPf = false>
 struct WGatherVisitor {
   const int4* rec;
   const int* firsts;
   int4* AP;
   int fv, pv, m1, m2;
+  int pf[kPf ? kItems : 1];
   // (prefetching all 8 records up front measured slower here: 118 -> 130 us)
-  __device__ __forceinline__ void prefetch(int, const uint32_t*, int) {}
+  __device__ __forceinline__ void prefetch(int, const uint32_t* w, int cnt) {
+    if (kPf) {
+#pragma unroll
+      for (int i = 0; i < kItems; i++) pf[kPf ? i : 0] = (i < cnt) ? __ldg(firsts + w[i]) : 0;
+    }
+  }
   __device__ __forceinline__ void begin(int v, int64_t, int64_t) {
     int4 r = __ldg(rec + v);
     fv = r.x;
@@ -59,7 +65,7 @@ struct WGatherVisitor {
     m1 = kINF;
     m2 = -1;
   }
-  __device__ __forceinline__ void arc(int v, int64_t, int w, int) {
+  __device__ __forceinline__ void arc(int v, int64_t, int w, int i) {
     if (pv == w) return;  // tree edge to the parent
     int f;
     if (kExact) {
@@ -67,7 +73,7 @@ struct WGatherVisitor {
       if (r.z == v) return;  // tree edge to a child
       f = r.x;
     } else {
-      f = __ldg(firsts + w);
+      f = kPf ? pf[kPf ? i : 0] : __ldg(firsts + w);
     }
     m1 = min(m1, f);
     m2 = max(m2, f);
@@ -82,12 +88,13 @@ struct WGatherVisitor {
   }
 };
 
-template <bool kExact>
+template <bool kExact, bool kPf = false>
 __global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                   const int* __restrict__ crow, int n, int64_t m,
                                                   const int4* __restrict__ rec, const int* __restrict__ firsts,
                                                   int4* AP) {
-  WGatherVisitor<kExact> vis;
+  pdl_enter();
+  WGatherVisitor<kExact, kPf> vis;
   vis.rec = rec;
   vis.firsts = firsts;
   vis.AP = AP;
@@ -95,6 +102,7 @@ __global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ of
 }
 
 __global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ firsts) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) firsts[v] = __ldg(&rec[v].x);
 }
 
@@ -144,6 +152,7 @@ struct TileSmem {
 __global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int4* __restrict__ AP,
                                                           int64_t N, int ntile, int2* __restrict__ lh1,
                                                           int2* __restrict__ lh2, int2* __restrict__ table0) {
+  pdl_enter();
   extern __shared__ int2 smem[];
   TileSmem S;
   S.raw = smem;
@@ -209,6 +218,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int4* __restrict
 constexpr int kTableOneCta = 16384;
 
 __global__ void __launch_bounds__(1024) k_table_all(int2* table, int ntile, int tlev) {
+  pdl_enter();
   for (int k = 1; k < tlev; k++) {
     const int2* prev = table + (int64_t)(k - 1) * ntile;
     int2* cur = table + (int64_t)k * ntile;
@@ -222,6 +232,7 @@ __global__ void __launch_bounds__(1024) k_table_all(int2* table, int ntile, int 
 }
 
 __global__ void k_table_level(int2* table, int ntile, int k) {
+  pdl_enter();
   const int2* prev = table + (int64_t)(k - 1) * ntile;
   int2* cur = table + (int64_t)k * ntile;
   const int half = 1 << (k - 1);
@@ -236,28 +247,32 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, boo
   int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (g.m > 0) {
     if (exact) {
-      k_w_gather<true><<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, R.rec, nullptr, T.AP);
+      launch(k_w_gather<true>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, nullptr, T.AP);
     } else {
       // compact first[] lives in lh1 until k_tile overwrites it
       int* firsts = reinterpret_cast<int*>(T.lh1);
-      k_firsts<<<grid_for(g.n, B), B, 0, st>>>(R.rec, g.n, firsts);
+      launch(k_firsts, grid_for(g.n, B), B, 0, st, R.rec, g.n, firsts);
       note(K_W_GATHER);
-      k_w_gather<false><<<grid_for(nchunks, B, 32), B, 0, st>>>(g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts, T.AP);
+      if (g_opt[OPT_GATHER_PREFETCH])
+        launch(k_w_gather<false, true>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts,
+                                                                       T.AP);
+      else
+        launch(k_w_gather<false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts, T.AP);
     }
     note(K_W_GATHER);
   }
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-  k_tile<<<grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st>>>(T.AP, 2 * (int64_t)g.n, T.ntile, T.lh1,
+  launch(k_tile, grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile, T.lh1,
                                                                   T.lh2, T.table);
   note(K_TILE);
   if (T.ntile <= kTableOneCta) {
     if (T.tlev > 1) {
-      k_table_all<<<1, 1024, 0, st>>>(T.table, T.ntile, T.tlev);
+      launch(k_table_all, 1, 1024, 0, st, T.table, T.ntile, T.tlev);
       note(K_TABLE);
     }
   } else {
     for (int k = 1; k < T.tlev; k++) {
-      k_table_level<<<grid_for(T.ntile, B), B, 0, st>>>(T.table, T.ntile, k);
+      launch(k_table_level, grid_for(T.ntile, B), B, 0, st, T.table, T.ntile, k);
       note(K_TABLE);
     }
   }
@@ -269,6 +284,7 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, boo
 __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const int2* __restrict__ lh2,
                         const int2* __restrict__ table, int ntile, int* low_out, int* high_out,
                         int* __restrict__ head, int* __restrict__ cnt, int* __restrict__ bmin) {
+  pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
     int ta = r.x / kTile, tb = r.y / kTile;
@@ -302,7 +318,7 @@ __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const in
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
                   int* bmin, cudaStream_t st) {
   const int B = 256;
-  k_fence<<<grid_for(g.n, B), B, 0, st>>>(g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out, head,
+  launch(k_fence, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out, head,
                                           cnt, bmin);
   note(K_FENCE);
 }

@@ -50,7 +50,7 @@ def test_large_config(name, oracle_mod):
     t0 = time.time()
     off, adj = workloads.make_device(name)
     gen_s = time.time() - t0
-    plan = Plan(off, adj)
+    plan = Plan(off, adj, timing=True)
     plan.run()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ev[0].record()

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--variant", action="append", default=[])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--raw", action="store_true")
+    ap.add_argument("--plan", type=int, default=0, help="time N unprofiled graph replays instead")
     a = ap.parse_args()
     off, adj = workloads.make_device(a.config)
     defaults = {k: _lib.get_option(k) for k in _lib.OPTIONS}
@@ -32,6 +33,27 @@ def main():
         for kv in filter(None, var.split(",")):
             k, v = kv.split("=")
             _lib.set_option(k, int(v))
+        if a.plan:  # unprofiled CUDA-graph replays, L2 flushed before each (as bench.py)
+            import torch
+
+            from paper_2301_01356_b200.bcc import Plan
+
+            pl = Plan(off, adj)
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device=off.device)
+            for _ in range(3):
+                pl.run()
+            ts = []
+            for _ in range(a.plan):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                pl.launch()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            print(f"== variant [{var or 'defaults'}] plan median {np.median(ts):.4f} ms  min {min(ts):.4f} ms")
+            del pl
+            continue
         run_device(off, adj)  # warm
         rows = []
         for _ in range(a.reps):
