@@ -53,17 +53,21 @@ def _peaks():
 def alg_bytes(kind, n, m, T, E, K1=0):
     csr = 8 * (n + 1) + 4 * m
     return {
-        "link_rest": csr + 4 * n + 8 * T,           # one full connectivity pass over the CSR
-        "sample_link": 16 * n + 4 * n + 8 * n,
+        "hook_min": 16 * n + 4 * n + 4 * n + 8 * n,  # off[v..v+1], adj[off[v]], comp + fe out
+        "propose": 16 * n + 4 * n + 8 * n,           # per sampling round
         "compress": 8 * n,
+        "link_rows": csr + 4 * n + 8 * T,            # one full connectivity pass over the CSR
+        "out_lists": n * (4 + 8) + 2 * n * 4,
+        "link_tour": 2 * n * (4 + 4 + 8 + 4),
         "walk0": 2 * n * (4 + 8),                    # read succ, write (segment, offset)
+        "rank0": 2 * n * (8 + 4 + 4),
         "positions": n * (16 + 16 + 8 + 4) + 2 * n * 8 * 2,
-        "w_gather": csr + 8 * m + 16 * n + 8 * n,    # (parent, first) per arc + row record + A
+        "firsts": 16 * n + 4 * n,
+        "w_gather": csr + 4 * m + 16 * n + 8 * n,    # first[w] per arc + row record + (w1, w2) out
         "tile": 2 * n * 16 + 16 * n,                 # A + P in, partials out
         "fence": n * (16 + 16 + 16 + 4),
         "edge_blocks": csr + E * (4 + 4 + 4) + 12 * n,
-        "tree_scatter": n * (16 + 8 + 16) + 4 * 2 * (n - 1) * 2,
-        "link_slots": 2 * n * (4 + 4 + 8 + 4),
+        "edge_final": E * (4 + 4 + 4),
     }.get(kind)
 
 
@@ -275,7 +279,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- e2e: public API, pinned host CSR in, results out -----------------
     gp = Graph(g.offsets, g.edges)
-    gp._pinned = (torch.from_numpy(g.offsets).pin_memory(), torch.from_numpy(g.edges.view(np.int32)).pin_memory())
+    gp.pin()
     for _ in range(max(args.warmup, 3)):  # >= 2 live result sets before the pinned cache is warm
         lab = fast_bcc(gp, device=dev)
     torch.cuda.synchronize()
@@ -306,6 +310,18 @@ def run_ours(args, rank, world, local_rank):
                 traffic = json.loads(prof.read_text()).get(f"config{args.config}", {}).get(dom)
             except Exception:
                 traffic = None
+        # Random 4-byte gathers are bounded by the L1TEX wavefront rate (one
+        # 128 B line per cycle per SM, B300_MICROARCH.md "L1tex wavefront
+        # queue") long before HBM: report the gather rate against that too.
+        gathers = {"w_gather": m, "edge_blocks": E}.get(dom)
+        clocks = clk.summary()
+        gather_bound = None
+        if gathers and clocks.get("sm_mhz"):
+            g_rate = gathers / (kern[dom]["ms_per_launch"] / 1e3)
+            g_peak = 148 * clocks["sm_mhz"] * 1e6
+            gather_bound = {"gathers_per_launch": gathers, "achieved_per_s": g_rate,
+                            "peak_lines_per_s": g_peak, "frac": g_rate / g_peak,
+                            "model": "148 SMs x 1 L1TEX wavefront/cycle x median SM clock"}
         sum_alg = 46 * m + 165 * n + 48 * T + 16  # SURVEY §8(d) end-to-end algorithmic bytes
         ms = total_ms / args.steps
         line = {
@@ -317,7 +333,7 @@ def run_ours(args, rank, world, local_rank):
                     "ms_per_step": 1e3 * e2e_total / args.steps},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
                          "frac": ach / hbm, "traffic": traffic, "peak_source": src,
-                         "alg_bytes_per_launch": b},
+                         "alg_bytes_per_launch": b, "gather_bound": gather_bound},
             "pipeline_roofline": {"alg_bytes": sum_alg, "achieved_gbs": sum_alg / (ms / 1e3) / 1e9,
                                   "frac": sum_alg / (ms / 1e3) / 1e9 / hbm},
             "stage_ms": dict(zip(["forest", "rooting", "tags", "fence", "skeleton_cc", "labelling"],
@@ -325,7 +341,7 @@ def run_ours(args, rank, world, local_rank):
             "kernels": kern,
             "profiled_ms_per_step": prof_total_ms / args.steps,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "num_bccs": int(stats.num_bccs), "num_components": int(stats.num_components),
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -66,6 +66,17 @@ typedef struct {
   int32_t *comp;       /* [n] or NULL: first-pass component labels (min id) */
 } fbcc_outputs;
 
+/* HOST buffers of fbcc_run_host.  Pinned (page-locked) memory lets the
+   copies overlap the kernels; pageable memory works but serialises them. */
+typedef struct {
+  const int64_t *offsets; /* [n+1] symmetric CSR, as fbcc_run                 */
+  const uint32_t *edges;  /* [m]                                              */
+  int32_t *label;         /* [n] or NULL                                      */
+  int32_t *head;          /* [n] or NULL                                      */
+  int32_t *edge_label;    /* capacity m/2 or NULL; the first E entries valid  */
+  uint8_t *is_ap;         /* [n] or NULL                                      */
+} fbcc_host_io;
+
 /* Optional intermediate exports for stage-level parity (DEVICE pointers,
    each may be NULL).  Written after the run, outside the per-stage timers. */
 typedef struct {
@@ -95,6 +106,16 @@ typedef struct {
   int32_t prof_kind[FBCC_MAX_PROFILE];    /* kernel kind (fbcc_kernel_name)  */
   float prof_ms[FBCC_MAX_PROFILE];        /* device time between its events   */
 } fbcc_stats;
+
+/* End to end from host memory (the path behind fast_bcc on a host Graph):
+   copy io->offsets / io->edges into d_offsets / d_edges, run, copy the
+   outputs back into io's host buffers; returns after everything landed.
+   The edge array is copied in arc ranges and Stage 1 links each range as it
+   arrives (the union-find runs under the transfer); label / head / is_ap
+   are copied back while Stage 6 still runs.  Same results as fbcc_run. */
+int fbcc_run_host(const fbcc_host_io *io, int64_t n, int64_t m, int64_t *d_offsets, uint32_t *d_edges,
+                  void *workspace, size_t workspace_bytes, fbcc_outputs *out, fbcc_stats *stats,
+                  void *stream, uint32_t flags);
 
 /* Required workspace bytes for a graph of n vertices and m directed slots. */
 int fbcc_workspace_bytes(int64_t n, int64_t m, size_t *bytes_out);

@@ -23,11 +23,11 @@ FBCC_FLAG_PROFILE = 2
 FBCC_MAX_PROFILE = 512
 
 # every symbol the header declares (checked by tests/test_abi.py)
-EXPORTS = ("fbcc_workspace_bytes", "fbcc_run", "fbcc_strerror", "fbcc_last_cuda_error", "fbcc_version",
+EXPORTS = ("fbcc_workspace_bytes", "fbcc_run", "fbcc_run_host", "fbcc_strerror", "fbcc_last_cuda_error", "fbcc_version",
            "fbcc_kernel_name", "fbcc_plan_create", "fbcc_plan_run", "fbcc_plan_launch", "fbcc_plan_stats", "fbcc_plan_destroy",
            "fbcc_set_option", "fbcc_get_option")
 
-OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "s0": 3, "sl": 4, "compress_mask": 8, "gather_prefetch": 10, "pdl": 11}
+OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "s0": 3, "sl": 4, "compress_mask": 8, "pdl": 11, "stream_chunks": 12}
 
 
 def set_option(name: str, value: int) -> None:
@@ -41,6 +41,10 @@ def get_option(name: str) -> int:
 class FbccOutputs(ctypes.Structure):
     _fields_ = [("label", ctypes.c_void_p), ("head", ctypes.c_void_p), ("edge_label", ctypes.c_void_p),
                 ("is_ap", ctypes.c_void_p), ("comp", ctypes.c_void_p)]
+
+
+class FbccHostIO(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_void_p) for k in ("offsets", "edges", "label", "head", "edge_label", "is_ap")]
 
 
 class FbccDebug(ctypes.Structure):
@@ -77,6 +81,10 @@ def load():
         L.fbcc_run.argtypes = [P, P, ctypes.c_int64, ctypes.c_int64, P, ctypes.c_size_t,
                                ctypes.POINTER(FbccOutputs), ctypes.POINTER(FbccDebug),
                                ctypes.POINTER(FbccStats), P, ctypes.c_uint32]
+        L.fbcc_run_host.restype = ctypes.c_int
+        L.fbcc_run_host.argtypes = [ctypes.POINTER(FbccHostIO), ctypes.c_int64, ctypes.c_int64, P, P, P,
+                                    ctypes.c_size_t, ctypes.POINTER(FbccOutputs), ctypes.POINTER(FbccStats), P,
+                                    ctypes.c_uint32]
         L.fbcc_strerror.restype = ctypes.c_char_p
         L.fbcc_strerror.argtypes = [ctypes.c_int]
         L.fbcc_last_cuda_error.restype = ctypes.c_char_p

@@ -245,37 +245,68 @@ _SESSIONS = {}
 
 
 def _session(g: Graph, dev) -> Plan:
-    """A graph-replay plan bound to device buffers for this input.
-
-    Device-resident inputs bind their own tensors (keyed by pointer); host
-    inputs are copied (from pinned memory when ``g._pinned`` is set) into
-    persistent device buffers of the right size, reused across calls."""
-    import torch
-
-    if g._dev is not None:
-        off, adj, _ = _device_csr(g, dev)
-        key = ("dev", off.data_ptr(), adj.data_ptr(), g.n, g.m)
-        plan = _SESSIONS.get(key)
-        if plan is None:
-            _SESSIONS.clear()
-            plan = _SESSIONS[key] = Plan(off, adj)
-        return plan
-    key = ("host", str(dev), g.n, g.m)
+    """A graph-replay plan bound to a device-resident input (keyed by its
+    buffers), reused across calls."""
+    off, adj, _ = _device_csr(g, dev)
+    key = ("dev", off.data_ptr(), adj.data_ptr(), g.n, g.m)
     plan = _SESSIONS.get(key)
     if plan is None:
         _SESSIONS.clear()
-        off = torch.empty(g.n + 1, dtype=torch.int64, device=dev)
-        adj = torch.empty(max(g.m, 1), dtype=torch.int32, device=dev)[: g.m]
-        plan = _SESSIONS[key] = Plan(off, adj)
-    if g._pinned is not None:
-        off_h, adj_h = g._pinned
-    else:
-        off_h = torch.from_numpy(g.offsets)
-        adj_h = torch.from_numpy(g.edges.view(np.int32))
-    plan.off.copy_(off_h, non_blocking=True)
-    if g.m:
-        plan.adj.copy_(adj_h, non_blocking=True)
+        plan = _SESSIONS[key] = Plan(off, adj, timing=True)
     return plan
+
+
+class _HostRunner:
+    """Persistent device buffers for host-resident inputs of one size;
+    ``run`` is ``fbcc_run_host``: streamed H2D overlapped with Stage 1,
+    early outputs copied back while Stage 6 runs."""
+
+    def __init__(self, n, m, dev):
+        import torch
+
+        self.L = _lib.load()
+        self.n, self.m, self.dev = n, m, dev
+        self.off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.adj = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+        self.ws = torch.empty(max(_lib.workspace_bytes(n, m), 256), dtype=torch.uint8, device=dev)
+        self.label = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.head = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self.is_ap = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        self.edge_label = torch.empty(max(m // 2, 1), dtype=torch.int32, device=dev)
+        self.outs = _lib.FbccOutputs(self.label.data_ptr(), self.head.data_ptr(), self.edge_label.data_ptr(),
+                                     self.is_ap.data_ptr(), None)
+
+    def run(self, g: Graph):
+        import torch
+
+        n, m = self.n, self.m
+        if g._pinned is not None:
+            off_h, adj_h = g._pinned
+            off_p, adj_p = off_h.data_ptr(), adj_h.data_ptr()
+        else:  # pageable: correct, but the copies cannot overlap the kernels
+            off_p, adj_p = g.offsets.ctypes.data, g.edges.ctypes.data
+        h = {"label": torch.empty(n, dtype=torch.int32, pin_memory=True),
+             "head": torch.empty(n, dtype=torch.int32, pin_memory=True),
+             "is_ap": torch.empty(n, dtype=torch.uint8, pin_memory=True),
+             "edge_label": torch.empty(m // 2, dtype=torch.int32, pin_memory=True)}
+        io = _lib.FbccHostIO(off_p, adj_p if m else None, h["label"].data_ptr(), h["head"].data_ptr(),
+                             h["edge_label"].data_ptr() if m // 2 else None, h["is_ap"].data_ptr())
+        st = _lib.FbccStats()
+        s = torch.cuda.current_stream(self.dev)
+        _lib.check(self.L.fbcc_run_host(ctypes.byref(io), n, m, self.off.data_ptr(), self.adj.data_ptr(),
+                                        self.ws.data_ptr(), self.ws.numel(), ctypes.byref(self.outs),
+                                        ctypes.byref(st), ctypes.c_void_p(s.cuda_stream), _lib.FBCC_FLAG_TIMING))
+        E = int(st.num_edges)
+        return st, {k: v.numpy() for k, v in h.items()}, E
+
+
+def _host_session(g: Graph, dev) -> _HostRunner:
+    key = ("host", str(dev), g.n, g.m)
+    r = _SESSIONS.get(key)
+    if r is None:
+        _SESSIONS.clear()
+        r = _SESSIONS[key] = _HostRunner(g.n, g.m, dev)
+    return r
 
 
 def _to_host(res, keys):
@@ -326,13 +357,17 @@ def fast_bcc(g: Graph, *, beta: float | None = None, seed: int = 0, block: int =
         g._dev[0].device if g._dev is not None else torch.device("cuda", torch.cuda.current_device()))
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
+    if g._dev is None and not device_outputs:
+        stats, out, E = _host_session(g, dev).run(g)
+        tim = _timings(stats)
+        return BccLabeling(out["label"], out["head"], int(stats.num_bccs), int(stats.num_components), tim,
+                           out["edge_label"][:E], out["is_ap"].astype(bool))
+    if g._dev is None:  # device outputs from a host graph: upload, then the device path
+        g = Graph.from_device(*[t.to(dev) for t in _pinned_or_numpy(g)])
     plan = _session(g, dev)
     stats = plan.run()
     res = plan.outputs()
-    ms = [float(x) for x in stats.stage_ms]
-    tim = StepTimings(first_cc=ms[0] / 1e3, rooting=ms[1] / 1e3, tagging=ms[2] / 1e3,
-                      last_cc=(ms[3] + ms[4]) / 1e3, labelling=ms[5] / 1e3,
-                      total=float(stats.total_ms) / 1e3, stage_ms=tuple(ms))
+    tim = _timings(stats)
     if device_outputs:  # plan buffers are reused by the next call: hand out copies
         res = {k: (None if v is None else v.clone()) for k, v in res.items()}
         return BccLabeling(res["label"], res["head"], int(stats.num_bccs), int(stats.num_components), tim,
@@ -340,6 +375,21 @@ def fast_bcc(g: Graph, *, beta: float | None = None, seed: int = 0, block: int =
     out = _to_host(res, ("label", "head", "edge_label", "is_ap"))
     return BccLabeling(out["label"], out["head"], int(stats.num_bccs), int(stats.num_components), tim,
                        out["edge_label"], out["is_ap"].astype(bool))
+
+
+def _timings(stats) -> StepTimings:
+    ms = [float(x) for x in stats.stage_ms]
+    return StepTimings(first_cc=ms[0] / 1e3, rooting=ms[1] / 1e3, tagging=ms[2] / 1e3,
+                       last_cc=(ms[3] + ms[4]) / 1e3, labelling=ms[5] / 1e3,
+                       total=float(stats.total_ms) / 1e3, stage_ms=tuple(ms))
+
+
+def _pinned_or_numpy(g: Graph):
+    import torch
+
+    if g._pinned is not None:
+        return g._pinned
+    return torch.from_numpy(g.offsets), torch.from_numpy(g.edges.view(np.int32))
 
 
 def extract_bccs(labeling: BccLabeling) -> list:

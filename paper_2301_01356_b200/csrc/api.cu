@@ -15,10 +15,10 @@ static thread_local char g_cuda_err[256] = "";
 thread_local LaunchLog* g_log = nullptr;
 
 static const char* kKernelNames[K_NUM_KINDS] = {
-    "iota", "sample_link", "compress", "find_giant", "link_rest", "root_flags", "scan", "tree_degree",
-    "tree_scatter", "link_slots", "link_roots", "walk0", "walk_level", "final_rank", "expand", "positions",
-    "w_gather", "tile", "table", "fence", "heads", "ap", "upper_degree", "set_edges", "edge_blocks",
-    "edge_final", "memset", "export", "accept", "chunk_rows", "root_list", "unused"};
+    "chunk_rows", "hook_min", "iota", "propose", "accept", "compress", "find_giant", "link_rows", "link_heavy",
+    "root_flags", "scan", "root_list", "out_lists", "link_tour", "walk0", "walk_level", "final_rank", "expand", "rank0",
+    "positions", "firsts", "w_gather", "tile", "table", "fence", "heads", "count_blocks", "ap", "set_edges",
+    "edge_blocks", "edge_final", "memset", "export"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -27,9 +27,11 @@ static int cuda_fail(cudaError_t e, const char* where) {
 
 int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*retired*/ 0, /*S0*/ 16, /*SL*/ 8,
                       /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last*/ 0,
-                      /*retired*/ 0, /*gather prefetch (measured neutral: off)*/ 0,
-                      /*programmatic dependent launch (measured 5% slower on config 2: off)*/ 0};
+                      /*retired*/ 0, /*retired*/ 0,
+                      /*programmatic dependent launch (measured 5% slower on config 2: off)*/ 0,
+                      /*fbcc_run_host edge-copy chunks*/ 8};
 constexpr int kFinalMaxHost = kFinalMax;
+constexpr int kMaxStreamChunks = 64;
 
 struct Layout {
   size_t total = 0;
@@ -164,29 +166,99 @@ struct Pipeline {
 
   // Enqueue all six stages.  ev (7 events) brackets the stages when given.
   void enqueue(cudaStream_t st, cudaEvent_t* ev, int* low_out, int* high_out, bool capturing = false) {
-    auto mark = [&](int i) {
+    Marks mk{st, ev, capturing};
+    cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
+    note(K_MEMSET);
+    mk(0);
+    build_chunk_rows(g, const_cast<int*>(g.crow), st, uoff + (g.n + 1), nlow);  // + Stage-6 upper degrees
+    stage1_forest(g, comp, fe, prop, sc, st);
+    mk(1);
+    enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
+  }
+
+  struct Marks {
+    cudaStream_t st;
+    cudaEvent_t* ev;
+    bool capturing;
+    void operator()(int i) const {
       if (!ev) return;
       // inside a graph capture the record must become an event-record node
       if (capturing) cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal);
       else cudaEventRecord(ev[i], st);
-    };
+    }
+  };
+
+  // Stages 2-6.  label_done / heads_done (optional) are recorded as soon as
+  // the label array / the head and is_ap arrays are final.
+  void enqueue_rest(cudaStream_t st, const Marks& mk, int* low_out, int* high_out, cudaEvent_t label_done,
+                    cudaEvent_t heads_done) {
+    stage2_rooting(g, comp, fe, R, T.AP, sc, st);
+    mk(2);
+    stage3_tags(g, R, T, st);
+    mk(3);
+    stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st);
+    mk(4);
+    stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st);
+    mk(5);
+    if (label_done) cudaEventRecord(label_done, st);
+    stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, R.cub_tmp,
+                     R.cub_bytes, sc, st, heads_done);
+    mk(6);
+  }
+
+  // Host-resident input and outputs (fbcc_run_host).  The CSR arrives on the
+  // copy stream cs -- offsets, then the edge array in nchunk arc ranges --
+  // and Stage 1 links each range as soon as it lands (stage1_stream_*), so
+  // the union-find hides under the H2D transfer.  label is copied back while
+  // Stage 6 runs, head / is_ap while the per-edge labels are computed; only
+  // the per-edge labels' own D2H trails the last kernel.
+  void enqueue_host(cudaStream_t st, cudaStream_t cs, const fbcc_host_io& io, cudaEvent_t* hev, int nchunk,
+                    cudaEvent_t* ev) {
+    Marks mk{st, ev, false};
+    cudaEvent_t ev_start = hev[0], ev_off = hev[1], ev_label = hev[2], ev_heads = hev[3], ev_copies = hev[4];
+    cudaEvent_t* ev_chunk = hev + 5;
+    const int64_t n = g.n, m = g.m;
+    // the copies must not overwrite inputs a previous run on st still reads
+    cudaEventRecord(ev_start, st);
+    cudaStreamWaitEvent(cs, ev_start, 0);
+    cudaMemcpyAsync(const_cast<int64_t*>(g.off), io.offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, cs);
+    cudaEventRecord(ev_off, cs);
+    const int64_t nq = (m + kItems - 1) / kItems;
+    int64_t qb[kMaxStreamChunks + 1];
+    for (int c = 0; c <= nchunk; c++) qb[c] = nq * c / nchunk;
+    for (int c = 0; c < nchunk; c++) {
+      const int64_t a0 = qb[c] * kItems, a1 = qb[c + 1] * kItems < m ? qb[c + 1] * kItems : m;
+      if (a1 > a0)
+        cudaMemcpyAsync(const_cast<uint32_t*>(g.adj) + a0, io.edges + a0, sizeof(uint32_t) * (a1 - a0),
+                        cudaMemcpyHostToDevice, cs);
+      cudaEventRecord(ev_chunk[c], cs);
+    }
+    cudaStreamWaitEvent(st, ev_off, 0);
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
-    mark(0);
-    build_chunk_rows(g, const_cast<int*>(g.crow), st, uoff + (g.n + 1), nlow);  // + Stage-6 upper degrees
-    stage1_forest(g, comp, fe, prop, sc, st);
-    mark(1);
-    stage2_rooting(g, comp, fe, R, T.AP, sc, st);
-    mark(2);
-    stage3_tags(g, R, T, st);
-    mark(3);
-    stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st);
-    mark(4);
-    stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st);
-    mark(5);
-    stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, R.cub_tmp,
-                     R.cub_bytes, sc, st);
-    mark(6);
+    mk(0);
+    build_chunk_rows(g, const_cast<int*>(g.crow), st);  // offsets only
+    stage1_stream_begin(g, comp, st);
+    for (int c = 0; c < nchunk; c++) {
+      cudaStreamWaitEvent(st, ev_chunk[c], 0);
+      stage1_stream_range(g, qb[c], qb[c + 1], comp, fe, st);
+    }
+    stage1_stream_finish(g, comp, sc, st);
+    upper_degrees(g, uoff + (n + 1), nlow, st);
+    mk(1);
+    enqueue_rest(st, mk, nullptr, nullptr, ev_label, ev_heads);
+    if (io.label) {
+      cudaStreamWaitEvent(cs, ev_label, 0);
+      cudaMemcpyAsync(io.label, out.label, sizeof(int) * n, cudaMemcpyDeviceToHost, cs);
+    }
+    if (io.head || io.is_ap) cudaStreamWaitEvent(cs, ev_heads, 0);
+    if (io.head) cudaMemcpyAsync(io.head, out.head, sizeof(int) * n, cudaMemcpyDeviceToHost, cs);
+    if (io.is_ap && out.is_ap) cudaMemcpyAsync(io.is_ap, out.is_ap, n, cudaMemcpyDeviceToHost, cs);
+    cudaEventRecord(ev_copies, cs);
+    // E <= m/2 labels (exactly m/2 for a loop-free symmetric input)
+    if (io.edge_label && out.edge_label && m / 2 > 0)
+      cudaMemcpyAsync(io.edge_label, out.edge_label, sizeof(int) * (m / 2), cudaMemcpyDeviceToHost, st);
+    cudaStreamWaitEvent(st, ev_copies, 0);
   }
 };
 
@@ -211,6 +283,7 @@ int fbcc_set_option(int key, int value) {
   if (key < 0 || key >= OPT_NUM) return FBCC_ERR_ARG;
   if ((key == OPT_S0 || key == OPT_SL) && (value < 2 || (value & (value - 1)))) return FBCC_ERR_ARG;
   if (key == OPT_SAMPLE_ROUNDS && (value < 0 || value > 8)) return FBCC_ERR_ARG;
+  if (key == OPT_STREAM_CHUNKS && (value < 1 || value > kMaxStreamChunks)) return FBCC_ERR_ARG;
   g_opt[key] = value;
   return FBCC_OK;
 }
@@ -323,6 +396,76 @@ int fbcc_run(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m
     for (int i = 0; i < 7; i++) cudaEventDestroy(ev[i]);
   delete log;
   if (e != cudaSuccess) return cuda_fail(e, "run");
+  return FBCC_OK;
+}
+
+// copy stream + events of fbcc_run_host, per thread and device
+struct HostStreams {
+  int dev = -1;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev[5 + kMaxStreamChunks] = {};
+};
+static thread_local HostStreams g_hs;
+
+static cudaError_t host_streams() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || g_hs.dev == dev) return e;
+  if (g_hs.cs) {  // switched device: the old objects belong to the old one
+    cudaStreamDestroy(g_hs.cs);
+    for (auto& x : g_hs.ev) cudaEventDestroy(x);
+  }
+  g_hs = HostStreams{};
+  e = cudaStreamCreateWithFlags(&g_hs.cs, cudaStreamNonBlocking);
+  for (auto& x : g_hs.ev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  if (e == cudaSuccess) g_hs.dev = dev;
+  return e;
+}
+
+int fbcc_run_host(const fbcc_host_io* io, int64_t n, int64_t m, int64_t* d_offsets, uint32_t* d_edges,
+                  void* workspace, size_t workspace_bytes, fbcc_outputs* out, fbcc_stats* stats, void* stream,
+                  uint32_t flags) {
+  if (!io || !io->offsets || (m > 0 && !io->edges)) return FBCC_ERR_ARG;
+  int rc = check_args(d_offsets, d_edges, n, m, workspace, workspace_bytes, out);
+  if (rc) return rc;
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (n == 0) return FBCC_OK;
+  cudaError_t e = host_streams();
+  if (e != cudaSuccess) return cuda_fail(e, "run_host streams");
+  cudaStream_t st = (cudaStream_t)stream;
+  Pipeline P(d_offsets, d_edges, n, m, workspace, out);
+  const bool timing = (flags & FBCC_FLAG_TIMING) && stats;
+  cudaEvent_t ev[7];
+  if (timing)
+    for (int i = 0; i < 7; i++) cudaEventCreate(&ev[i]);
+  LaunchLog* log = new LaunchLog();
+  log->st = st;
+  log->profile = (flags & FBCC_FLAG_PROFILE) && stats;
+  g_log = log;
+  int nchunk = g_opt[OPT_STREAM_CHUNKS];
+  if (nchunk < 1) nchunk = 1;
+  if (nchunk > kMaxStreamChunks) nchunk = kMaxStreamChunks;
+  P.enqueue_host(st, g_hs.cs, *io, g_hs.ev, nchunk, timing ? ev : nullptr);
+  g_log = nullptr;
+  e = cudaGetLastError();
+  Scalars host;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&host, P.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && stats) {
+    fill_counts(stats, host);
+    stats->launches = log->count;
+    fill_profile(stats, *log);
+    if (timing) {
+      for (int i = 0; i < 6; i++) cudaEventElapsedTime(&stats->stage_ms[i], ev[i], ev[i + 1]);
+      cudaEventElapsedTime(&stats->total_ms, ev[0], ev[6]);
+    }
+  }
+  log->destroy();
+  if (timing)
+    for (int i = 0; i < 7; i++) cudaEventDestroy(ev[i]);
+  delete log;
+  if (e != cudaSuccess) return cuda_fail(e, "run_host");
   return FBCC_OK;
 }
 

@@ -30,11 +30,11 @@ struct Scalars {
 // launch log: counts every launch of ours and, in profile mode, brackets
 // each with CUDA events on the launching stream (per-kernel device time)
 // ---------------------------------------------------------------------------
-enum KernelKind : int {
-  K_IOTA = 0, K_SAMPLE_LINK, K_COMPRESS, K_FIND_GIANT, K_LINK_REST, K_ROOT_FLAGS, K_SCAN, K_TREE_DEGREE,
-  K_TREE_SCATTER, K_LINK_SLOTS, K_LINK_ROOTS, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_POSITIONS,
-  K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_AP, K_UPPER_DEGREE, K_SET_EDGES, K_EDGE_BLOCKS,
-  K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_ACCEPT, K_CHUNK_ROWS, K_ROOT_LIST, K_JUMP, K_NUM_KINDS
+enum KernelKind : int {  // one kind per kernel function (names: api.cu kKernelNames)
+  K_CHUNK_ROWS = 0, K_HOOK_MIN, K_IOTA, K_PROPOSE, K_ACCEPT, K_COMPRESS, K_FIND_GIANT, K_LINK_ROWS, K_LINK_HEAVY,
+  K_ROOT_FLAGS, K_SCAN, K_ROOT_LIST, K_OUT_LISTS, K_LINK_TOUR, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_RANK0,
+  K_POSITIONS, K_FIRSTS, K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_COUNT_BLOCKS, K_AP, K_SET_EDGES,
+  K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_NUM_KINDS
 };
 
 struct LaunchLog {
@@ -71,9 +71,9 @@ enum Option : int {
   OPT_S0 = 3,             // level-0 splitter spacing (power of two)
   OPT_SL = 4,             // spacing on higher ranking levels (power of two)
   OPT_COMPRESS_MASK = 8,  // bitmask: sampling rounds followed by a compress (bit 0 always honoured)
-  OPT_GATHER_PREFETCH = 10,  // relaxed w gather issues all 8 first[] loads of a chunk up front
   OPT_PDL = 11,           // programmatic dependent launch between consecutive kernels
-  // (keys 2, 5, 6, 7, 9: retired experiments -- accepted, ignored)
+  OPT_STREAM_CHUNKS = 12, // fbcc_run_host: arc ranges the edge copy is split into
+  // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 16
 };
 extern int g_opt[OPT_NUM];

@@ -453,15 +453,16 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
   if (kRounds > 0) {
     launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd);  // round 0
+    note(K_HOOK_MIN);
   } else {
     launch(k_iota, gv, B, 0, st, comp, g.n, nullptr);
+    note(K_IOTA);
   }
-  note(K_IOTA);
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
     if (r > 0) {
       launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat);
-      note(K_SAMPLE_LINK);
+      note(K_PROPOSE);
       launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks);
       note(K_ACCEPT);
     }
@@ -479,12 +480,73 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     int* nheavy = sc->nheavy + (slot ? 1 : 0);
     launch(k_link_rows<kPred, kRecord>, grid_for(g.n, B, 32), B, 0, st, g.off, g.adj, g.n, comp, fe, pd, sc, heavy,
                                                                     nheavy);
-    note(K_LINK_REST);
+    note(K_LINK_ROWS);
     launch(k_link_heavy<kPred, kRecord>, grid_for((int64_t)kNumSMs * 2048, B), B, 0, st, g.off, g.adj, comp, fe, pd,
                                                                                      heavy, nheavy);
-    note(K_LINK_REST);
+    note(K_LINK_HEAVY);
   }
   launch(k_compress, gres, B, 0, st, comp, g.n, nroots + 7);  // final root count (= components)
+  note(K_COMPRESS);
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1 on a streamed input (fbcc_run_host): the edge array arrives from
+// host memory in arc ranges, and each range is linked as soon as its copy
+// lands, so the union-find runs under the PCIe transfer instead of after it.
+// Every undirected edge is linked once, from its smaller endpoint (the input
+// is symmetric); no sampling or giant skip (both need the whole graph).  The
+// labels are canonical (root = set minimum) and any spanning forest yields
+// the same final outputs, so the result is identical to stage1_forest's.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_link_range(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                    const int* __restrict__ crow, int n, int64_t m, int64_t q0,
+                                                    int64_t q1, int* comp, int2* fe) {
+  pdl_enter();
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
+  for (int64_t q = q0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < q1; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a0 = q * kItems;
+    const int64_t a1 = a0 + kItems < m ? a0 + kItems : m;
+    uint32_t w[kItems];
+    if (vec_ok && a1 - a0 == kItems) {
+      int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
+      int4 y = ld_stream4(reinterpret_cast<const int4*>(adj + a0 + 4));
+      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+      w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;
+    }
+    int v = __ldg(crow + q);
+    if (v < 0) v = row_of(off, 0, n - 1, a0);
+    int64_t re = __ldg(off + v + 1);
+#pragma unroll
+    for (int i = 0; i < kItems; i++) {
+      const int64_t a = a0 + i;
+      if (a < a1) {
+        if (a >= re) {
+          v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, n - 1, a);
+          re = __ldg(off + v + 1);
+        }
+        if (v < (int)w[i]) link<true>(v, (int)w[i], comp, fe);
+      }
+    }
+  }
+}
+
+void stage1_stream_begin(const Graph& g, int* comp, cudaStream_t st) {
+  launch(k_iota, grid_for(g.n, 256), 256, 0, st, comp, g.n, nullptr);
+  note(K_IOTA);
+}
+
+void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2* fe, cudaStream_t st) {
+  if (q1 <= q0) return;
+  launch(k_link_range, grid_for(q1 - q0, 256, 16), 256, 0, st, g.off, g.adj, g.crow, g.n, g.m, q0, q1, comp, fe);
+  note(K_LINK_ROWS);
+}
+
+void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st) {
+  const int B = 256;
+  launch(k_compress, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7);
   note(K_COMPRESS);
 }
 

@@ -60,6 +60,14 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
 void masked_cc(const Graph& g, const uint8_t* mask, int* comp, int2* fe, unsigned long long* prop, Scalars* sc,
                cudaStream_t st);
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st);
+// Stage 1 over a streamed edge array (fbcc_run_host): identity init, one link
+// pass per arrived chunk range [q0, q1) of kItems-arc chunks, final compress
+void stage1_stream_begin(const Graph& g, int* comp, cudaStream_t st);
+void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2* fe, cudaStream_t st);
+void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st);
+// per-row nlow / upper degree for the edge numbering (when build_chunk_rows
+// ran without the adjacency)
+void upper_degrees(const Graph& g, int* ud, int* nlow, cudaStream_t st);
 void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
                     Scalars* sc, cudaStream_t st);
 // exact: reference w2 (both forest directions excluded); otherwise the
@@ -72,7 +80,7 @@ void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned lo
                         cudaStream_t st);
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
-                      size_t cub_bytes, Scalars* sc, cudaStream_t st);
+                      size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done = nullptr);
 void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* AP, int* forest,
                   int* parent, int* first, int* last, int* w1, int* w2, uint8_t* fence,
                   cudaStream_t st);

@@ -80,6 +80,11 @@ __global__ void k_upper_degree(const int64_t* __restrict__ off, const uint32_t* 
   }
 }
 
+void upper_degrees(const Graph& g, int* ud, int* nlow, cudaStream_t st) {
+  launch(k_upper_degree, grid_for(g.n + 1, 256), 256, 0, st, g.off, g.adj, g.n, ud, nlow);
+  note(K_CHUNK_ROWS);
+}
+
 struct EdgeBlockVisitor {
   const int64_t* off;
   const int* label;
@@ -149,7 +154,7 @@ __global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) {
 
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
-                      size_t cub_bytes, Scalars* sc, cudaStream_t st) {
+                      size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done) {
   const int n = g.n;
   const int B = 256;
   const int gv = grid_for(n + 1, B);
@@ -157,11 +162,12 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   launch(k_heads, gv, B, 0, st, n, rec, label, head);
   note(K_HEADS);
   launch(k_count_blocks, gv, B, 0, st, n, head, cnt, sc);
-  note(K_HEADS);
+  note(K_COUNT_BLOCKS);
   if (is_ap) {
     launch(k_ap, gv, B, 0, st, n, label, head, cnt, is_ap);
     note(K_AP);
   }
+  if (heads_done) cudaEventRecord(heads_done, st);  // head / is_ap final: their D2H may start
   // edge ids: ud (computed with the chunk table at run start) -> exclusive
   // scan -> uoff (uoff[n] = E)
   int* ud = uoff + (n + 1);

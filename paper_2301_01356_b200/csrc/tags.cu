@@ -44,61 +44,118 @@ __device__ __forceinline__ int2 filler() { return make_int2(kINF, -1); }
 // and every subtree aggregate low/high, unchanged -- only the intermediate
 // w2 of v may grow (SURVEY §8(c) rung 3 checks both forms).  RMAT: 1.05e9
 // gathers from a 134 MB array (mostly L2) instead of a 537 MB one.
-template <bool kExact, bool kPf = false>
-struct WGatherVisitor {
-  const int4* rec;
-  const int* firsts;
-  int4* AP;
-  int fv, pv, m1, m2;
-  int pf[kPf ? kItems : 1];
-  // (prefetching all 8 records up front measured slower here: 118 -> 130 us)
-  __device__ __forceinline__ void prefetch(int, const uint32_t* w, int cnt) {
-    if (kPf) {
-#pragma unroll
-      for (int i = 0; i < kItems; i++) pf[kPf ? i : 0] = (i < cnt) ? __ldg(firsts + w[i]) : 0;
-    }
+template <bool kExact>
+__device__ __forceinline__ void w_arc(int v, int pv, int w, const int4* __restrict__ rec,
+                                      const int* __restrict__ firsts, int& m1, int& m2) {
+  if (pv == w) return;  // tree edge to the parent
+  int f;
+  if (kExact) {
+    const int4 r = __ldg(rec + w);
+    if (r.z == v) return;  // tree edge to a child
+    f = r.x;
+  } else {
+    f = __ldg(firsts + w);
   }
-  __device__ __forceinline__ void begin(int v, int64_t, int64_t) {
-    int4 r = __ldg(rec + v);
-    fv = r.x;
-    pv = r.z;
-    m1 = kINF;
-    m2 = -1;
-  }
-  __device__ __forceinline__ void arc(int v, int64_t, int w, int i) {
-    if (pv == w) return;  // tree edge to the parent
-    int f;
-    if (kExact) {
-      const int4 r = __ldg(rec + w);
-      if (r.z == v) return;  // tree edge to a child
-      f = r.x;
-    } else {
-      f = kPf ? pf[kPf ? i : 0] : __ldg(firsts + w);
-    }
-    m1 = min(m1, f);
-    m2 = max(m2, f);
-  }
-  __device__ __forceinline__ void end(int, bool whole) {
-    if (whole) {
-      *reinterpret_cast<int2*>(AP + fv) = make_int2(min(fv, m1), max(fv, m2));
-    } else if (m2 >= 0) {
-      atomicMin(&AP[fv].x, m1);
-      atomicMax(&AP[fv].y, m2);
-    }
-  }
-};
+  m1 = min(m1, f);
+  m2 = max(m2, f);
+}
 
-template <bool kExact, bool kPf = false>
+__device__ __forceinline__ void w_store(int4* AP, int fv, int m1, int m2) {
+  *reinterpret_cast<int2*>(AP + fv) = make_int2(min(fv, m1), max(fv, m2));
+}
+
+__device__ __forceinline__ void w_atomic(int4* AP, int fv, int m1, int m2) {
+  if (m2 < 0) return;  // no contributing arc (AP[fv] already holds (fv, fv))
+  atomicMin(&AP[fv].x, m1);
+  atomicMax(&AP[fv].y, m2);
+}
+
+// Arc-balanced like visit_arc_chunks (8 arcs per thread, the chunk's row from
+// crow), but rows that straddle chunk boundaries are combined inside the warp
+// instead of with two atomics per piece: consecutive lanes hold consecutive
+// chunks, so a row's pieces sit in consecutive lanes.  Each lane ends with at
+// most a "tail" piece (its last row runs past the chunk) and a "head" piece
+// (its first row began before the chunk and ends in it); lane j's head is
+// shuffled to lane j-1, whose tail is the same row, then lanes with equal
+// tail rows reduce with __match_any_sync + __reduce_{min,max}_sync.  A row
+// that begins and ends inside the warp gets one plain store; only rows that
+// cross a warp boundary fall back to atomics.  (Per-piece atomics were ~5 per
+// row at degree 16: a quarter of the kernel's L1 wavefronts.)
+template <bool kExact>
 __global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                   const int* __restrict__ crow, int n, int64_t m,
                                                   const int4* __restrict__ rec, const int* __restrict__ firsts,
                                                   int4* AP) {
   pdl_enter();
-  WGatherVisitor<kExact, kPf> vis;
-  vis.rec = rec;
-  vis.firsts = firsts;
-  vis.AP = AP;
-  visit_arc_chunks(off, adj, crow, n, m, vis);
+  const int64_t nchunks = (m + kItems - 1) / kItems;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the shuffles below need the whole warp)
+  for (int64_t qb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); qb < nchunks; qb += stride) {
+    const int64_t q = qb + lane;
+    int tkey = -1, t1 = kINF, t2 = -1, tfv = 0;  // row running past the chunk end
+    bool tstart = false;                         // ... and starting inside the chunk
+    int hkey = -1, h1 = kINF, h2 = -1, hfv = 0;  // row begun before the chunk, ending in it
+    if (q < nchunks) {
+      const int64_t a0 = q * kItems;
+      const int64_t a1 = a0 + kItems < m ? a0 + kItems : m;
+      uint32_t w[kItems];
+      if (vec_ok && a1 - a0 == kItems) {
+        int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
+        int4 y = ld_stream4(reinterpret_cast<const int4*>(adj + a0 + 4));
+        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+        w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;
+      }
+      int v = __ldg(crow + q);
+      if (v < 0) v = row_of(off, 0, n - 1, a0);
+      int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+      int4 r = __ldg(rec + v);
+      int m1 = kINF, m2 = -1;
+#pragma unroll
+      for (int i = 0; i < kItems; i++) {
+        const int64_t a = a0 + i;
+        if (a < a1) {
+          if (a >= re) {  // row v ends inside the chunk
+            if (rs < a0) { hkey = v; h1 = m1; h2 = m2; hfv = r.x; }
+            else w_store(AP, r.x, m1, m2);
+            v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, n - 1, a);
+            rs = __ldg(off + v);
+            re = __ldg(off + v + 1);
+            r = __ldg(rec + v);
+            m1 = kINF;
+            m2 = -1;
+          }
+          w_arc<kExact>(v, r.z, (int)w[i], rec, firsts, m1, m2);
+        }
+      }
+      if (re > a1) { tkey = v; t1 = m1; t2 = m2; tfv = r.x; tstart = rs >= a0; }
+      else if (rs < a0) { hkey = v; h1 = m1; h2 = m2; hfv = r.x; }
+      else w_store(AP, r.x, m1, m2);
+    }
+    // lane j's head piece belongs to lane j-1's tail row
+    const int nk = __shfl_down_sync(0xffffffffu, hkey, 1);
+    const int n1 = __shfl_down_sync(0xffffffffu, h1, 1);
+    const int n2 = __shfl_down_sync(0xffffffffu, h2, 1);
+    bool tend = false;
+    if (lane < 31 && nk >= 0) {
+      t1 = min(t1, n1);
+      t2 = max(t2, n2);
+      tend = true;
+    }
+    if (lane == 0 && hkey >= 0) w_atomic(AP, hfv, h1, h2);  // began in an earlier warp
+    const unsigned grp = __match_any_sync(0xffffffffu, tkey);
+    const int g1 = __reduce_min_sync(grp, t1);
+    const int g2 = __reduce_max_sync(grp, t2);
+    const unsigned ends = __reduce_or_sync(grp, tend ? 1u : 0u);
+    if (tkey >= 0 && lane == __ffs(grp) - 1) {
+      if (tstart && ends) w_store(AP, tfv, g1, g2);  // whole row inside this warp
+      else w_atomic(AP, tfv, g1, g2);
+    }
+  }
 }
 
 __global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ firsts) {
@@ -252,12 +309,9 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, boo
       // compact first[] lives in lh1 until k_tile overwrites it
       int* firsts = reinterpret_cast<int*>(T.lh1);
       launch(k_firsts, grid_for(g.n, B), B, 0, st, R.rec, g.n, firsts);
-      note(K_W_GATHER);
-      if (g_opt[OPT_GATHER_PREFETCH])
-        launch(k_w_gather<false, true>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts,
-                                                                       T.AP);
-      else
-        launch(k_w_gather<false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts, T.AP);
+      note(K_FIRSTS);
+      launch(k_w_gather<false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts,
+             T.AP);
     }
     note(K_W_GATHER);
   }

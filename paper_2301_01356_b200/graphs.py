@@ -33,6 +33,16 @@ class Graph:
         if validate:
             self.validate()
 
+    def pin(self):
+        """Cache page-locked copies of the CSR: fast_bcc then streams them to
+        the device at full link speed, overlapped with Stage 1."""
+        import torch
+
+        if self._pinned is None and self._dev is None:
+            self._pinned = (torch.from_numpy(self.offsets).pin_memory(),
+                            torch.from_numpy(self.edges.view(np.int32)).pin_memory())
+        return self
+
     @classmethod
     def from_device(cls, offsets_t, edges_t):
         """Wrap device-resident torch tensors (int64 offsets, int32/uint32

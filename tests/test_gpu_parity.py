@@ -184,3 +184,44 @@ def test_repeat_runs_identical():
         b = _run(g, debug=False)
         for k in ("label", "head", "is_ap", "edge_label"):
             assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("name", ["1", "2"])
+def test_public_api_paths_match_reference(name, config_meta):
+    """fast_bcc on a pageable host graph, a pinned one (fbcc_run_host: streamed
+    upload, Stage 1 linked per arrived range, for several range counts), a
+    device-resident one and with device outputs: all equal the reference's
+    digests."""
+    import torch
+
+    import workloads
+    from paper_2301_01356_b200 import Graph, _lib, fast_bcc
+
+    g = workloads.make(name)
+    meta = config_meta[name]
+
+    def check(lab):
+        host = {k: (v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v))
+                for k, v in (("label", lab.label), ("head", lab.head), ("edge_label", lab.edge_label),
+                             ("is_ap", lab.is_ap))}
+        assert lab.num_bccs == meta["num_bccs"]
+        assert lab.num_components == meta["num_components"]
+        assert host["edge_label"].size == meta["E"]
+        assert _sha(host["label"]) == meta["label_sha256"]
+        assert _sha(host["head"]) == meta["head_sha256"]
+        assert _sha(host["edge_label"]) == meta["edge_label_sha256"]
+        assert _sha(host["is_ap"].astype(np.uint8)) == meta["is_ap_sha256"]
+
+    check(fast_bcc(g))  # pageable
+    gp = Graph(g.offsets, g.edges).pin()
+    old = _lib.get_option("stream_chunks")
+    try:
+        for chunks in (1, 3, 8, 64):
+            _lib.set_option("stream_chunks", chunks)
+            check(fast_bcc(gp))
+    finally:
+        _lib.set_option("stream_chunks", old)
+    check(fast_bcc(gp, device_outputs=True))
+    gd = Graph.from_device(torch.from_numpy(g.offsets).cuda(), torch.from_numpy(g.edges.view(np.int32)).cuda())
+    check(fast_bcc(gd))
+    check(fast_bcc(gd, device_outputs=True))

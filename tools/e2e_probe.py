@@ -1,4 +1,6 @@
-"""Break down fast_bcc's end-to-end time (pinned H2D, graph replay, D2H)."""
+"""Break down fast_bcc's end-to-end time on a host graph (fbcc_run_host):
+raw link speeds, the run itself, its per-stage events, and the Python-side
+overhead around it."""
 import sys
 import time
 from pathlib import Path
@@ -12,12 +14,12 @@ def main():
     import torch
 
     import workloads
-    from paper_2301_01356_b200 import Graph, fast_bcc
-    from paper_2301_01356_b200.bcc import _session, _to_host
+    from paper_2301_01356_b200 import Graph, _lib, fast_bcc
+    from paper_2301_01356_b200.bcc import _host_session
 
-    g = workloads.make("2")
-    gp = Graph(g.offsets, g.edges)
-    gp._pinned = (torch.from_numpy(g.offsets).pin_memory(), torch.from_numpy(g.edges.view(np.int32)).pin_memory())
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "2"
+    g = workloads.make(cfg)
+    gp = Graph(g.offsets, g.edges).pin()
     dev = torch.device("cuda", 0)
     for _ in range(3):
         fast_bcc(gp, device=dev)
@@ -33,16 +35,22 @@ def main():
             ts.append(time.perf_counter() - t0)
         return 1e3 * float(np.median(ts))
 
-    plan = _session(gp, dev)
-    print("h2d+session ms", t(lambda: _session(gp, dev)))
-    print("plan.run ms", t(lambda: plan.run()))
-    res = plan.outputs()
-    print("d2h (to_host) ms", t(lambda: _to_host(res, ("label", "head", "edge_label", "is_ap"))))
+    h2d = 8 * (g.n + 1) + 4 * g.m
+    d2h = 9 * g.n + 4 * (g.m // 2)
+    x = torch.empty(h2d, dtype=torch.uint8).pin_memory()
+    y = torch.empty(h2d, dtype=torch.uint8, device=dev)
+    print(f"raw h2d {h2d / 1e6:.1f} MB ms", t(lambda: y.copy_(x, non_blocking=True)))
+    print(f"raw d2h {d2h / 1e6:.1f} MB ms", t(lambda: x[:d2h].copy_(y[:d2h], non_blocking=True)))
+    r = _host_session(gp, dev)
+    print("run_host ms", t(lambda: r.run(gp)))
+    st, _, _ = r.run(gp)
+    print("run_host stage ms", [round(float(v), 3) for v in st.stage_ms], "total", round(float(st.total_ms), 3))
     print("fast_bcc ms", t(lambda: fast_bcc(gp, device=dev)))
-    x = torch.empty(75 << 20, dtype=torch.uint8).pin_memory()
-    y = torch.empty(75 << 20, dtype=torch.uint8, device=dev)
-    print("raw h2d 75MB ms", t(lambda: y.copy_(x, non_blocking=True)))
-    print("raw d2h 75MB ms", t(lambda: x.copy_(y, non_blocking=True)))
+    old = _lib.get_option("stream_chunks")
+    for c in (1, 2, 4, 16, 32):
+        _lib.set_option("stream_chunks", c)
+        print(f"run_host chunks={c} ms", t(lambda: r.run(gp)))
+    _lib.set_option("stream_chunks", old)
 
 
 if __name__ == "__main__":

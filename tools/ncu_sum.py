@@ -17,7 +17,7 @@ def rows(path):
     r = list(csv.reader(out.splitlines()))
     h, units = r[0], r[1]
     for v in r[2:]:
-        d = {"kernel": v[h.index("Kernel Name")][:40]}
+        d = {"kernel": v[h.index("Kernel Name")][:80]}
         for m, short in WANT:
             if m in h:
                 x = v[h.index(m)]
