@@ -73,6 +73,7 @@ enum Option : int {
   OPT_COMPRESS_MASK = 8,  // bitmask: sampling rounds followed by a compress (bit 0 always honoured)
   OPT_PDL = 11,           // programmatic dependent launch between consecutive kernels
   OPT_STREAM_CHUNKS = 12, // fbcc_run_host: arc ranges the edge copy is split into
+  OPT_SKEL_PARENT = 13,   // Stage 5 sampling: bit r = round r samples the plain parent edge
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 16
 };

@@ -174,7 +174,7 @@ void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st, int* ud, int* 
 // Also resets the proposal words for the later rounds.
 template <int kPred, bool kRecord>
 __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int* comp,
-                           int2* fe, unsigned long long* __restrict__ prop, PredData pd) {
+                           int2* fe, unsigned long long* __restrict__ prop, PredData pd, bool skel_parent) {
   pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t s = __ldg(off + v);
@@ -186,6 +186,10 @@ __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __re
       if (w < v && keep<kPred>(pd, v, rv, w, s)) {
         c = w;
         if (kRecord) fe[v] = make_int2(v, w);
+      }
+      // skeleton: the plain tree edge to the parent is always kept
+      if (kPred == PRED_SKEL && skel_parent) {
+        if (rv.z >= 0 && rv.w == 0 && rv.z < c) c = rv.z;
       }
     }
     comp[v] = c;
@@ -210,7 +214,7 @@ constexpr int kPerRoot = 32;
 template <int kPred>
 __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round,
                           int* comp, unsigned long long* prop, PredData pd, const int* __restrict__ nroots,
-                          const int* __restrict__ hooks, bool flat) {
+                          const int* __restrict__ hooks, bool flat, bool skel_parent) {
   pdl_enter();
   // participate iff hash < thr / 2^24, thr = min(1, kPerRoot * roots / n);
   // roots at round start = roots counted after round 0 minus later hooks
@@ -223,12 +227,19 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
   }
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     if (thr < (1u << 24) && (hash32((uint32_t)v * 0x9E3779B1u + (uint32_t)round) >> 8) >= thr) continue;
+    int w;
     int64_t s = __ldg(off + v) + round;
-    if (s >= __ldg(off + v + 1)) continue;
-    int w = (int)__ldg(adj + s);
     int4 rv;
     if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
-    if (!keep<kPred>(pd, v, rv, w, s)) continue;
+    if (kPred == PRED_SKEL && skel_parent) {  // this round samples the plain parent edge
+      if (rv.z < 0 || rv.w != 0) continue;
+      w = rv.z;
+      s = -1;
+    } else {
+      if (s >= __ldg(off + v + 1)) continue;
+      w = (int)__ldg(adj + s);
+      if (!keep<kPred>(pd, v, rv, w, s)) continue;
+    }
     // flat after a compress; otherwise (rounds >= 1 hook root -> root only,
     // so trees stay shallow) find with halving
     int ru = flat ? ldp(comp + v) : find_halve(comp, v);
@@ -452,7 +463,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   int cmask = g_opt[OPT_COMPRESS_MASK];
   if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
   if (kRounds > 0) {
-    launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd);  // round 0
+    const int sp = g_opt[OPT_SKEL_PARENT];
+    launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd, (sp & 1) != 0);  // round 0
     note(K_HOOK_MIN);
   } else {
     launch(k_iota, gv, B, 0, st, comp, g.n, nullptr);
@@ -461,7 +473,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
     if (r > 0) {
-      launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat);
+      launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat,
+             ((g_opt[OPT_SKEL_PARENT] >> r) & 1) != 0);
       note(K_PROPOSE);
       launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks);
       note(K_ACCEPT);

@@ -12,7 +12,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 
 def main():
-    import torch
+    import torch  # noqa: F401
 
     import workloads
     from paper_2301_01356_b200 import _lib
@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--variant", action="append", default=[])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--raw", action="store_true")
+    ap.add_argument("--scalars", action="store_true", help="print the sampling-round counters")
     ap.add_argument("--plan", type=int, default=0, help="time N unprofiled graph replays instead")
     a = ap.parse_args()
     off, adj = workloads.make_device(a.config)
@@ -55,6 +56,14 @@ def main():
             del pl
             continue
         run_device(off, adj)  # warm
+        if a.scalars:  # device counters at the head of the workspace (common.cuh Scalars)
+            from paper_2301_01356_b200 import bcc as _bcc
+
+            ws = next(iter(_bcc._WS.values()))
+            sc = ws[:4 * 64].view(torch.int32).cpu().numpy()
+            print(f"   ncomp {sc[0]} giant {sc[1]} nbccs {sc[2]} err {sc[3]} E {sc[4]}")
+            print(f"   S1 roots after rounds {sc[5:13].tolist()} hooks {sc[21:29].tolist()}")
+            print(f"   S5 roots after rounds {sc[13:21].tolist()} hooks {sc[29:37].tolist()} heavy {sc[37:39].tolist()}")
         rows = []
         for _ in range(a.reps):
             res, st = run_device(off, adj, profile=True)
