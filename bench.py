@@ -63,7 +63,7 @@ def alg_bytes(kind, n, m, T, E, K1=0):
         "rank0": 2 * n * (8 + 4 + 4),
         "positions": n * (16 + 16 + 8 + 4) + 2 * n * 8 * 2,
         "firsts": 16 * n + 4 * n,
-        "w_gather": csr + 4 * m + 16 * n + 8 * n,    # first[w] per arc + row record + (w1, w2) out
+        "w_gather": csr + 4 * m + 16 * n + 12 * n,   # first[w] per arc + row record + (w1, w2) + nlow out
         "tile": 2 * n * 16 + 16 * n,                 # A + P in, partials out
         "fence": n * (16 + 16 + 16 + 4),
         "edge_blocks": csr + E * (4 + 4 + 4) + 12 * n,

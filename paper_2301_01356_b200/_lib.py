@@ -5,11 +5,13 @@ present, every entry point raises.
 """
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libfastbcc_b200.so"
+# FBCC_LIB: an experiment build (tools/build_variant.py); default the in-tree library
+LIB_PATH = Path(os.environ["FBCC_LIB"]) if os.environ.get("FBCC_LIB") else _HERE / "libfastbcc_b200.so"
 
 FBCC_OK = 0
 FBCC_ERR_ARG = 1

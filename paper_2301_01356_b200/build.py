@@ -43,29 +43,34 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out: Path | None = None) -> Path:
+    """extra / out: experiment builds (tools/build_variant.py) -- extra nvcc
+    flags, a separate object directory and library path."""
+    lib = out or LIB
+    bdir = BUILD if out is None else BUILD.parent / "_build_variants" / lib.stem
+    if out is None and not force and not _stale():
         return LIB
     nvcc = _nvcc()
-    BUILD.mkdir(exist_ok=True)
+    bdir.mkdir(parents=True, exist_ok=True)
     objs = []
     for src in sources():
-        obj = BUILD / (src.stem + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = bdir / (src.stem + ".o")
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src.name}:\n{r.stderr}")
-        (BUILD / (src.stem + ".ptxas.txt")).write_text(r.stderr)
+        (bdir / (src.stem + ".ptxas.txt")).write_text(r.stderr)
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -66,6 +66,7 @@ struct Layout {
     tlev = 1;
     while ((1 << tlev) <= ntile) tlev++;
     cub_bytes = scan_temp_bytes(n + 1);
+    if (scan_upper_temp_bytes((int)n) > cub_bytes) cub_bytes = scan_upper_temp_bytes((int)n);
 
     sc = take(sizeof(Scalars));
     crow = take(4 * ((m + kItems - 1) / kItems + 1));
@@ -92,7 +93,7 @@ struct Layout {
     lh2 = take(8 * n);
     table = take(8 * (size_t)ntile * tlev);
     cnt = take(4 * n);
-    uoff = take(4 * 2 * (n + 1));
+    uoff = take(4 * (n + 1));
     nlow = take(4 * n);
     bmin = take(4 * n);
     cub = take(cub_bytes);
@@ -170,7 +171,7 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    build_chunk_rows(g, const_cast<int*>(g.crow), st, uoff + (g.n + 1), nlow);  // + Stage-6 upper degrees
+    build_chunk_rows(g, const_cast<int*>(g.crow), st);
     stage1_forest(g, comp, fe, prop, sc, st);
     mk(1);
     enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
@@ -194,7 +195,7 @@ struct Pipeline {
                     cudaEvent_t heads_done) {
     stage2_rooting(g, comp, fe, R, T.AP, sc, st);
     mk(2);
-    stage3_tags(g, R, T, st);
+    stage3_tags(g, R, T, st, nlow);
     mk(3);
     stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st);
     mk(4);
@@ -237,14 +238,13 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    build_chunk_rows(g, const_cast<int*>(g.crow), st);  // offsets only
+    build_chunk_rows(g, const_cast<int*>(g.crow), st);
     stage1_stream_begin(g, comp, st);
     for (int c = 0; c < nchunk; c++) {
       cudaStreamWaitEvent(st, ev_chunk[c], 0);
       stage1_stream_range(g, qb[c], qb[c + 1], comp, fe, st);
     }
     stage1_stream_finish(g, comp, sc, st);
-    upper_degrees(g, uoff + (n + 1), nlow, st);
     mk(1);
     enqueue_rest(st, mk, nullptr, nullptr, ev_label, ev_heads);
     if (io.label) {

@@ -129,24 +129,10 @@ __device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
 // chunk -> row table (see visit_arc_chunks): row v owns the chunks whose
 // first arc lies in it
 // ---------------------------------------------------------------------------
-// Also (ud != nullptr) the per-row input facts Stage 6 needs for edge ids:
-// nlow[v] = #neighbours < v (rows are sorted, graphs.py:36-41) and the upper
-// degree ud[v] = deg - nlow[v], scanned later into the edge numbering.
-__global__ void k_chunk_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
-                             int* __restrict__ crow, int* __restrict__ ud, int* __restrict__ nlow) {
+__global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow) {
   pdl_enter();
-  if (ud && blockIdx.x == 0 && threadIdx.x == 0) ud[n] = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
-    if (ud) {
-      int64_t a = rs, b = re;  // first slot with target > v
-      while (a < b) {
-        int64_t mid = (a + b) >> 1;
-        if ((int)__ldg(adj + mid) < v) a = mid + 1; else b = mid;
-      }
-      nlow[v] = (int)(a - rs);
-      ud[v] = (int)(re - a);
-    }
     int64_t q0 = (rs + kItems - 1) / kItems;
     int64_t q1 = (re + kItems - 1) / kItems;
     if (q1 - q0 > kRowChunks) continue;  // hub row: consumers binary-search
@@ -154,16 +140,13 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, const uint32_t* __
   }
 }
 
-void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st, int* ud, int* nlow) {
+void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st) {
   int64_t nchunks = (g.m + kItems - 1) / kItems;
-  if (nchunks > 0) {
-    cudaMemsetAsync(crow, 0xFF, sizeof(int) * nchunks, st);
-    note(K_MEMSET);
-  }
-  if (nchunks > 0 || ud) {
-    launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.adj, g.n, crow, ud, nlow);
-    note(K_CHUNK_ROWS);
-  }
+  if (nchunks == 0) return;
+  cudaMemsetAsync(crow, 0xFF, sizeof(int) * nchunks, st);
+  note(K_MEMSET);
+  launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow);
+  note(K_CHUNK_ROWS);
 }
 
 // Sampling round 0 without atomics.  With every vertex its own root, the

@@ -16,7 +16,7 @@ struct Graph {
   const int* crow;       // [ceil(m/kItems)] chunk -> row table (build_chunk_rows)
 };
 
-void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st, int* ud = nullptr, int* nlow = nullptr);
+void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st);
 
 // Device arrays for the rooting / tags stages (see api.cu for the layout).
 constexpr int kFinalMax = 16384;  // list-ranking level finished in one CTA
@@ -65,14 +65,13 @@ void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop
 void stage1_stream_begin(const Graph& g, int* comp, cudaStream_t st);
 void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2* fe, cudaStream_t st);
 void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st);
-// per-row nlow / upper degree for the edge numbering (when build_chunk_rows
-// ran without the adjacency)
-void upper_degrees(const Graph& g, int* ud, int* nlow, cudaStream_t st);
+
 void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
                     Scalars* sc, cudaStream_t st);
-// exact: reference w2 (both forest directions excluded); otherwise the
-// relaxed gather of tags.cu (same w1/low/high)
-void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, bool exact = false);
+// nlow == nullptr: the reference's exact w2 (both forest directions
+// excluded, stand-alone op); otherwise the pipeline's relaxed gather (same
+// w1/low/high), which also counts each row's lower neighbours into nlow
+void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow);
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
                   int* bmin,
                   cudaStream_t st);
@@ -86,6 +85,10 @@ void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* A
                   cudaStream_t st);
 
 size_t scan_temp_bytes(int64_t items);
+// uoff[v] = sum over u < v of (deg(u) - nlow[u]), v in [0, n] (uoff[n] = E)
+size_t scan_upper_temp_bytes(int n);
+void scan_upper_degrees(const int64_t* off, const int* nlow, int n, int* uoff, void* tmp, size_t tmp_bytes,
+                        cudaStream_t st);
 void exclusive_scan(const int* in, int* out, int64_t items, void* tmp, size_t tmp_bytes,
                     cudaStream_t st);
 

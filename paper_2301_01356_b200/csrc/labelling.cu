@@ -63,28 +63,6 @@ __global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict
   }
 }
 
-// upper degree (neighbours > v) of each row; rows are sorted (graphs.py:36-41)
-__global__ void k_upper_degree(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
-                               int* __restrict__ ud, int* __restrict__ nlow) {
-  pdl_enter();
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
-    if (v == n) { ud[n] = 0; continue; }
-    int64_t lo = __ldg(off + v), hi = __ldg(off + v + 1);
-    int64_t a = lo, b = hi;  // first slot with target > v
-    while (a < b) {
-      int64_t mid = (a + b) >> 1;
-      if ((int)__ldg(adj + mid) < v) a = mid + 1; else b = mid;
-    }
-    nlow[v] = (int)(a - lo);
-    ud[v] = (int)(hi - a);
-  }
-}
-
-void upper_degrees(const Graph& g, int* ud, int* nlow, cudaStream_t st) {
-  launch(k_upper_degree, grid_for(g.n + 1, 256), 256, 0, st, g.off, g.adj, g.n, ud, nlow);
-  note(K_CHUNK_ROWS);
-}
-
 struct EdgeBlockVisitor {
   const int64_t* off;
   const int* label;
@@ -168,10 +146,9 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
     note(K_AP);
   }
   if (heads_done) cudaEventRecord(heads_done, st);  // head / is_ap final: their D2H may start
-  // edge ids: ud (computed with the chunk table at run start) -> exclusive
-  // scan -> uoff (uoff[n] = E)
-  int* ud = uoff + (n + 1);
-  exclusive_scan(ud, uoff, n + 1, cub_tmp, cub_bytes, st);
+  // edge ids: exclusive scan of the upper degrees deg - nlow (nlow counted
+  // by the Stage-3 gather) -> uoff (uoff[n] = E)
+  scan_upper_degrees(g.off, nlow, n, uoff, cub_tmp, cub_bytes, st);
   note(K_SCAN);
   launch(k_set_edges, 1, 1, 0, st, uoff, n, sc);
   note(K_SET_EDGES);

@@ -508,7 +508,7 @@ int op_compute_tags(const Graph& g, const int* parent, const int* first, const i
   T.tlev = tlev;
   int* scr = (int*)at(o_scr);
   launch(k_rec_ap, grid_for(n, B), B, 0, st, parent, first, last, (int)n, R.rec, T.AP);
-  stage3_tags(gg, R, T, st, /*exact=*/true);
+  stage3_tags(gg, R, T, st, /*nlow=*/nullptr);
   stage4_fence(gg, R, T, low, high, scr, scr + n, scr + 2 * n, st);
   export_debug(gg, nullptr, R.rec, T.AP, nullptr, nullptr, nullptr, nullptr, w1, w2, nullptr, st);
   return 0;

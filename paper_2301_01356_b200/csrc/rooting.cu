@@ -36,6 +36,8 @@
 //    tag stage reads, one 16-byte record per position (AP: (first, first) at
 //    entry, filler at exit; vertex id + partner position).
 #include <cub/device/device_scan.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -54,6 +56,30 @@ size_t scan_temp_bytes(int64_t items) {
 void exclusive_scan(const int* in, int* out, int64_t items, void* tmp, size_t tmp_bytes, cudaStream_t st) {
   size_t bytes = tmp_bytes;
   cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int)items, st);
+}
+
+struct UpperDegree {
+  const int64_t* off;
+  const int* nlow;
+  int n;
+  __host__ __device__ int operator()(int v) const {
+    return v < n ? (int)(off[v + 1] - off[v]) - nlow[v] : 0;
+  }
+};
+using UpperIt = cub::TransformInputIterator<int, UpperDegree, cub::CountingInputIterator<int>>;
+
+size_t scan_upper_temp_bytes(int n) {
+  size_t bytes = 0;
+  UpperIt it(cub::CountingInputIterator<int>(0), UpperDegree{nullptr, nullptr, n});
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (int*)nullptr, n + 1);
+  return bytes;
+}
+
+void scan_upper_degrees(const int64_t* off, const int* nlow, int n, int* uoff, void* tmp, size_t tmp_bytes,
+                        cudaStream_t st) {
+  size_t bytes = tmp_bytes;
+  UpperIt it(cub::CountingInputIterator<int>(0), UpperDegree{off, nlow, n});
+  cub::DeviceScan::ExclusiveSum(tmp, bytes, it, uoff, n + 1, st);
 }
 
 // ---------------------------------------------------------------------------

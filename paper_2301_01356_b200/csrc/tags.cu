@@ -81,25 +81,34 @@ __device__ __forceinline__ void w_atomic(int4* AP, int fv, int m1, int m2) {
 // that begins and ends inside the warp gets one plain store; only rows that
 // cross a warp boundary fall back to atomics.  (Per-piece atomics were ~5 per
 // row at degree 16: a quarter of the kernel's L1 wavefronts.)
+#ifndef FBCC_WG_MIN_BLOCKS
+#define FBCC_WG_MIN_BLOCKS 8  // 32 registers: full occupancy for the gathers (measured: 46 regs -> 133 us, 32 -> 111 us on config 2)
+#endif
+constexpr int kWGatherMinBlocks = FBCC_WG_MIN_BLOCKS;
+
 template <bool kExact>
-__global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+__global__ void __launch_bounds__(256, kWGatherMinBlocks) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                   const int* __restrict__ crow, int n, int64_t m,
                                                   const int4* __restrict__ rec, const int* __restrict__ firsts,
-                                                  int4* AP) {
+                                                  int4* AP, int* __restrict__ nlow) {
   pdl_enter();
+  // the pipeline variant also counts each row's lower neighbours (w < v) for
+  // Stage 6's edge numbering (k_upper_degree's binary searches, folded into
+  // this pass over the same arcs)
+  constexpr bool kCount = !kExact;
   const int64_t nchunks = (m + kItems - 1) / kItems;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // warp-uniform trip count (the shuffles below need the whole warp)
   for (int64_t qb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); qb < nchunks; qb += stride) {
-    const int64_t q = qb + lane;
-    int tkey = -1, t1 = kINF, t2 = -1, tfv = 0;  // row running past the chunk end
-    bool tstart = false;                         // ... and starting inside the chunk
-    int hkey = -1, h1 = kINF, h2 = -1, hfv = 0;  // row begun before the chunk, ending in it
+    const int q = (int)qb + lane;  // arc indices fit 32 bits (check_sizes: m < 2^31)
+    int tkey = -1, t1 = kINF, t2 = -1, tfv = 0, tc = 0;  // row running past the chunk end
+    bool tstart = false;                                 // ... and starting inside the chunk
+    int hkey = -1, h1 = kINF, h2 = -1, hfv = 0, hc = 0;  // row begun before the chunk, ending in it
     if (q < nchunks) {
-      const int64_t a0 = q * kItems;
-      const int64_t a1 = a0 + kItems < m ? a0 + kItems : m;
+      const int a0 = q * kItems;
+      const int a1 = a0 + kItems < (int)m ? a0 + kItems : (int)m;
       uint32_t w[kItems];
       if (vec_ok && a1 - a0 == kItems) {
         int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
@@ -112,55 +121,79 @@ __global__ void __launch_bounds__(256) k_w_gather(const int64_t* __restrict__ of
       }
       int v = __ldg(crow + q);
       if (v < 0) v = row_of(off, 0, n - 1, a0);
-      int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+      int rs = (int)__ldg(off + v), re = (int)__ldg(off + v + 1);
       int4 r = __ldg(rec + v);
-      int m1 = kINF, m2 = -1;
+      int m1 = kINF, m2 = -1, c = 0;
 #pragma unroll
       for (int i = 0; i < kItems; i++) {
-        const int64_t a = a0 + i;
+        const int a = a0 + i;
         if (a < a1) {
           if (a >= re) {  // row v ends inside the chunk
-            if (rs < a0) { hkey = v; h1 = m1; h2 = m2; hfv = r.x; }
-            else w_store(AP, r.x, m1, m2);
+            if (rs < a0) { hkey = v; h1 = m1; h2 = m2; hfv = r.x; hc = c; }
+            else {
+              w_store(AP, r.x, m1, m2);
+              if (kCount) nlow[v] = c;
+            }
             v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, n - 1, a);
-            rs = __ldg(off + v);
-            re = __ldg(off + v + 1);
+            rs = (int)__ldg(off + v);
+            re = (int)__ldg(off + v + 1);
             r = __ldg(rec + v);
             m1 = kINF;
             m2 = -1;
+            c = 0;
           }
+          if (kCount) c += (int)w[i] < v;
           w_arc<kExact>(v, r.z, (int)w[i], rec, firsts, m1, m2);
         }
       }
-      if (re > a1) { tkey = v; t1 = m1; t2 = m2; tfv = r.x; tstart = rs >= a0; }
-      else if (rs < a0) { hkey = v; h1 = m1; h2 = m2; hfv = r.x; }
-      else w_store(AP, r.x, m1, m2);
+      if (re > a1) { tkey = v; t1 = m1; t2 = m2; tfv = r.x; tc = c; tstart = rs >= a0; }
+      else if (rs < a0) { hkey = v; h1 = m1; h2 = m2; hfv = r.x; hc = c; }
+      else {
+        w_store(AP, r.x, m1, m2);
+        if (kCount) nlow[v] = c;
+      }
     }
     // lane j's head piece belongs to lane j-1's tail row
     const int nk = __shfl_down_sync(0xffffffffu, hkey, 1);
     const int n1 = __shfl_down_sync(0xffffffffu, h1, 1);
     const int n2 = __shfl_down_sync(0xffffffffu, h2, 1);
+    const int nc = kCount ? __shfl_down_sync(0xffffffffu, hc, 1) : 0;
     bool tend = false;
     if (lane < 31 && nk >= 0) {
       t1 = min(t1, n1);
       t2 = max(t2, n2);
+      tc += nc;
       tend = true;
     }
-    if (lane == 0 && hkey >= 0) w_atomic(AP, hfv, h1, h2);  // began in an earlier warp
+    if (lane == 0 && hkey >= 0) {  // began in an earlier warp
+      w_atomic(AP, hfv, h1, h2);
+      if (kCount && hc) atomicAdd(nlow + hkey, hc);
+    }
     const unsigned grp = __match_any_sync(0xffffffffu, tkey);
     const int g1 = __reduce_min_sync(grp, t1);
     const int g2 = __reduce_max_sync(grp, t2);
+    const int gc = kCount ? (int)__reduce_add_sync(grp, (unsigned)tc) : 0;
     const unsigned ends = __reduce_or_sync(grp, tend ? 1u : 0u);
     if (tkey >= 0 && lane == __ffs(grp) - 1) {
-      if (tstart && ends) w_store(AP, tfv, g1, g2);  // whole row inside this warp
-      else w_atomic(AP, tfv, g1, g2);
+      if (tstart && ends) {  // whole row inside this warp
+        w_store(AP, tfv, g1, g2);
+        if (kCount) nlow[tkey] = gc;
+      } else {
+        w_atomic(AP, tfv, g1, g2);
+        if (kCount && gc) atomicAdd(nlow + tkey, gc);
+      }
     }
   }
 }
 
-__global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ firsts) {
+// compact first[] for the relaxed gather; zeroes the lower-degree counters
+// the gather accumulates into (rows split across warps add atomically)
+__global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ firsts, int* __restrict__ nlow) {
   pdl_enter();
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) firsts[v] = __ldg(&rec[v].x);
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    firsts[v] = __ldg(&rec[v].x);
+    nlow[v] = 0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -299,20 +332,23 @@ __global__ void k_table_level(int2* table, int ntile, int k) {
   }
 }
 
-void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, bool exact) {
+void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow) {
   const int B = 256;
   int64_t nchunks = (g.m + kItems - 1) / kItems;
-  if (g.m > 0) {
-    if (exact) {
-      launch(k_w_gather<true>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, nullptr, T.AP);
-    } else {
-      // compact first[] lives in lh1 until k_tile overwrites it
-      int* firsts = reinterpret_cast<int*>(T.lh1);
-      launch(k_firsts, grid_for(g.n, B), B, 0, st, R.rec, g.n, firsts);
-      note(K_FIRSTS);
+  if (!nlow) {  // stand-alone compute_tags: the reference's exact w2
+    if (g.m > 0)
+      launch(k_w_gather<true>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, nullptr, T.AP,
+             nullptr);
+  } else {
+    // compact first[] lives in lh1 until k_tile overwrites it
+    int* firsts = reinterpret_cast<int*>(T.lh1);
+    launch(k_firsts, grid_for(g.n, B), B, 0, st, R.rec, g.n, firsts, nlow);
+    note(K_FIRSTS);
+    if (g.m > 0)
       launch(k_w_gather<false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts,
-             T.AP);
-    }
+             T.AP, nlow);
+  }
+  if (g.m > 0) {
     note(K_W_GATHER);
   }
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
