@@ -160,3 +160,14 @@ def test_fast_bcc_on_device_graph():
     b = fast_bcc(hg)
     assert np.array_equal(a.label, b.label) and np.array_equal(a.head, b.head)
     assert np.array_equal(a.edge_label, b.edge_label) and a.num_bccs == b.num_bccs
+
+
+def test_rmat_device_generator_matches_numpy():
+    """The GPU RMAT generator (bench/test input only) reproduces the numpy
+    PCG64 stream bit for bit, across chunk boundaries."""
+    import workloads
+
+    u0, v0 = workloads._rmat_pairs(scale=12, edge_factor=16, seed=0, chunk=5000)
+    u1, v1 = workloads.rmat_pairs_device(scale=12, edge_factor=16, seed=0, chunk=5000)
+    assert np.array_equal(u0, u1.cpu().numpy())
+    assert np.array_equal(v0, v1.cpu().numpy())

@@ -148,6 +148,51 @@ def _rmat_pairs(scale=25, edge_factor=16, seed=0, chunk=1 << 24):
     return np.concatenate(us), np.concatenate(vs)
 
 
+def _rmat_lib():
+    """tools/librmat_pcg.so (built here on first use when nvcc is present)."""
+    import ctypes
+    import subprocess
+    from pathlib import Path
+
+    tools = Path(__file__).resolve().parent / "tools"
+    so = tools / "librmat_pcg.so"
+    src = tools / "rmat_pcg.cu"
+    if not so.exists() or so.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared", "-Xcompiler",
+                        "-fPIC", "-cudart", "static", "-o", str(so), str(src)], check=True)
+    lib = ctypes.CDLL(str(so))
+    lib.rmat_pairs_chunk.restype = ctypes.c_int
+    lib.rmat_pairs_chunk.argtypes = [ctypes.c_uint64] * 5 + [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                                             ctypes.c_void_p, ctypes.c_void_p]
+    return lib
+
+
+def rmat_pairs_device(scale=25, edge_factor=16, seed=0, chunk=1 << 24, device="cuda"):
+    """_rmat_pairs on the GPU, bit-identical (same PCG64 stream, jumped to each
+    chunk/level offset; tools/rmat_pcg.cu).  Returns int64 device tensors."""
+    import ctypes
+
+    import torch
+
+    lib = _rmat_lib()
+    st = np.random.PCG64(seed).state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    total = edge_factor * (1 << scale)
+    u = torch.empty(total, dtype=torch.int64, device=device)
+    v = torch.empty(total, dtype=torch.int64, device=device)
+    stream = torch.cuda.current_stream(u.device).cuda_stream
+    done = 0
+    while done < total:
+        k = min(chunk, total - done)
+        rc = lib.rmat_pairs_chunk(s >> 64, s & m64, inc >> 64, inc & m64, done * scale, k, scale,
+                                  u[done:].data_ptr(), v[done:].data_ptr(), ctypes.c_void_p(stream))
+        if rc:
+            raise RuntimeError(f"rmat kernel failed ({rc})")
+        done += k
+    return u, v
+
+
 def symmetrize_device(u, v, n, device="cuda"):
     """symmetrize() on the GPU; returns (offsets int64[n+1], edges int32[m]) tensors."""
     import torch
@@ -174,6 +219,9 @@ def make_device(name, device="cuda"):
 
         g = make(name)
         return (torch.from_numpy(g.offsets).to(device), torch.from_numpy(g.edges.view(np.int32)).to(device))
+    if name == "5":  # the host generator takes minutes; the GPU one is bit-identical
+        u, v = rmat_pairs_device(device=device)
+        return symmetrize_device(u, v, 1 << 25, device)
     u, v, n = _pairs(name)
     return symmetrize_device(u, v, n, device)
 
