@@ -172,11 +172,27 @@ __device__ __forceinline__ int row_of(const int64_t* __restrict__ off, int lo, i
   return lo;
 }
 
+// Row after v that holds arc a (a >= off[v+1]): galloping from v+1, so the
+// usual case (the next row) costs the one probe of off[v+2], and runs of
+// empty rows (RMAT: half the vertices are isolated) cost O(log run) probes
+// instead of a binary search over all n rows.
+__device__ __forceinline__ int next_row(const int64_t* __restrict__ off, int v, int n, int64_t a) {
+  int lo = v + 1;  // off[lo] <= a
+  int step = 1;
+  while (true) {
+    const int probe = lo + step;
+    if (probe > n - 1) return row_of(off, lo, n - 1, a);
+    if (__ldg(off + probe) > a) return row_of(off, lo, probe - 1, a);
+    lo = probe;
+    step <<= 1;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Arc-balanced CSR traversal.  Every thread owns kItems consecutive arcs
 // (one 32-byte sector of targets, loaded as two 128-bit vectors) and reads
 // the row of its first arc from the per-run chunk->row table (crow, built by
-// k_chunk_rows; hub rows fall back to a binary search).  The visitor sees
+// k_chunk_rows, every chunk).  The visitor sees
 // rows in order:
 //   begin(v, row_start, row_end)  arc(v, a, w)  end(v, whole)
 // where ``whole`` says the row lies entirely inside this thread's chunk (no
@@ -220,7 +236,7 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
       if (a < a1) {
         if (a >= re) {
           vis.end(v, rs >= a0);
-          v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, n - 1, a);
+          v = next_row(off, v, n, a);
           rs = __ldg(off + v);
           re = __ldg(off + v + 1);
           vis.begin(v, rs, re);
@@ -233,10 +249,10 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
 }
 
 // chunk -> row table for visit_arc_chunks: crow[q] = row holding arc q*kItems,
-// written by the row itself (one thread per row) for rows spanning at most
-// kRowChunks chunks; chunks inside longer (hub) rows keep -1 from the memset
-// and fall back to a binary search.  One pass of n threads replaces a binary
-// search per chunk in each of the four arc-balanced kernels of a run.
+// written by the row itself -- one lane for rows spanning at most kRowChunks
+// chunks, the whole warp for longer (hub) rows.  One pass of n threads
+// replaces a binary search per chunk in each arc-balanced kernel of a run
+// (consumers keep a row_of fallback for a negative entry).
 constexpr int kRowChunks = 64;
 
 // Block-reduced counter add: every thread of the block must call it (after

@@ -129,22 +129,38 @@ __device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
 // chunk -> row table (see visit_arc_chunks): row v owns the chunks whose
 // first arc lies in it
 // ---------------------------------------------------------------------------
+// Every chunk q (first arc 8q) belongs to exactly one non-empty row, which
+// writes it -- no memset.  Rows of up to kRowChunks chunks are written by
+// their own lane; longer (hub) rows by the whole warp, so a 600k-arc RMAT hub
+// costs 2.3k warp stores instead of one thread's 75k (consumers used to
+// binary-search hub chunks over all n rows: half of RMAT's gather passes).
 __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow) {
   pdl_enter();
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
-    int64_t q0 = (rs + kItems - 1) / kItems;
-    int64_t q1 = (re + kItems - 1) / kItems;
-    if (q1 - q0 > kRowChunks) continue;  // hub row: consumers binary-search
-    for (int64_t q = q0; q < q1; q++) crow[q] = v;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n; base += warps * 32) {
+    const int v = (int)base + lane;
+    int q0 = 0, q1 = 0;
+    if (v < n) {
+      q0 = (int)((__ldg(off + v) + kItems - 1) / kItems);
+      q1 = (int)((__ldg(off + v + 1) + kItems - 1) / kItems);
+    }
+    const bool hub = q1 - q0 > kRowChunks;
+    if (!hub)
+      for (int q = q0; q < q1; q++) crow[q] = v;
+    unsigned hb = __ballot_sync(0xffffffffu, hub);
+    while (hb) {
+      const int src = __ffs(hb) - 1;
+      hb &= hb - 1;
+      const int hv = __shfl_sync(0xffffffffu, v, src);
+      const int h0 = __shfl_sync(0xffffffffu, q0, src), h1 = __shfl_sync(0xffffffffu, q1, src);
+      for (int q = h0 + lane; q < h1; q += 32) crow[q] = hv;
+    }
   }
 }
 
 void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st) {
-  int64_t nchunks = (g.m + kItems - 1) / kItems;
-  if (nchunks == 0) return;
-  cudaMemsetAsync(crow, 0xFF, sizeof(int) * nchunks, st);
-  note(K_MEMSET);
+  if (g.m == 0) return;
   launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow);
   note(K_CHUNK_ROWS);
 }
@@ -520,7 +536,7 @@ __global__ void __launch_bounds__(256) k_link_range(const int64_t* __restrict__ 
       const int64_t a = a0 + i;
       if (a < a1) {
         if (a >= re) {
-          v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, n - 1, a);
+          v = next_row(off, v, n, a);
           re = __ldg(off + v + 1);
         }
         if (v < (int)w[i]) link<true>(v, (int)w[i], comp, fe);

@@ -14,11 +14,13 @@
 //    tree child of the head: `head[l] = parent[v]` is an idempotent store
 //    (no packed-min over first[] like the reference).  A second per-label
 //    pass counts blocks and bumps the heads' saturating headed-counts.
-//  * edge ids: upper-degree via binary search in the sorted row + CUB scan.
-//  * per-block minimum edge id: arc-balanced pass, run-length aggregated per
-//    thread, and an L2 read before each atomicMin (ids only decrease, so a
-//    stale read can only cause a redundant atomic) -- config 2 has one block
-//    with 8.4 M edges that would otherwise serialise on one address.
+//  * edge ids: CUB scan of the upper degrees deg - nlow (nlow counted by the
+//    Stage-3 gather pass over the same arcs).
+//  * per-block minimum edge id: only the arcs of each block's minimum vertex
+//    can hold it (see EdgeBlockVisitor), so only those rows issue atomicMin
+//    -- one uncontended address per block instead of an atomic per run
+//    (config 2's giant block has 8.4 M edges, RMAT hubs change block on
+//    almost every arc).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -63,6 +65,15 @@ __global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict
   }
 }
 
+// Per-block minimum edge id without a per-run atomic: edge ids grow with the
+// row (u < w, CSR order), so a block's minimum edge is the FIRST upper arc in
+// the row of the block's minimum vertex u0 = min(l, head[l]) (every block
+// vertex has a block edge; u0's all go upward).  Only arcs of u0 rows feed
+// bmin: for an arc in its own component's block (blk == label[v]) that means
+// v == label[v] < head[label[v]]; for an arc into a child block headed by v
+// (blk == label[w]) it means v < label[w].  Those atomics hit distinct
+// addresses (one row per block) -- the old run-length scheme issued a
+// read + atomicMin per block change, i.e. per arc of an RMAT hub.
 struct EdgeBlockVisitor {
   const int64_t* off;
   const int* label;
@@ -72,6 +83,7 @@ struct EdgeBlockVisitor {
   int* eblk;
   int* bmin;
   int lu, ebase;
+  bool row_u0;
   int run_blk, run_min;
   int pl[kItems];
   // label[w] for every arc that can be an upper arc (w > first row of the chunk)
@@ -80,20 +92,34 @@ struct EdgeBlockVisitor {
     for (int i = 0; i < kItems; i++) pl[i] = (i < cnt && (int)w[i] > v0) ? __ldg(label + w[i]) : -1;
   }
   __device__ __forceinline__ void flush() {
-    if (run_blk >= 0 && run_min < ld_relaxed(bmin + run_blk)) atomicMin(bmin + run_blk, run_min);
+    if (run_blk >= 0) atomicMin(bmin + run_blk, run_min);
     run_blk = -1;
   }
   __device__ __forceinline__ void begin(int v, int64_t rs, int64_t) {
     lu = __ldg(label + v);
     ebase = __ldg(uoff + v) - (int)(rs + __ldg(nlow + v));  // e = ebase + a for upper arcs
+    // head[v] >= 0 only for label vertices (v == label[v]): no dependent load
+    const int hv = __ldg(head + v);
+    row_u0 = hv >= 0 && v < hv;
   }
   __device__ __forceinline__ void arc(int v, int64_t a, int w, int i) {
     if (w <= v) return;
     int e = ebase + (int)a;
     int lw = pl[i];
-    int blk = (lu == lw) ? lu : (__ldg(head + lw) == v ? lw : lu);
+    bool mine;
+    int blk;
+    if (lu == lw) {
+      blk = lu;
+      mine = row_u0;
+    } else if (__ldg(head + lw) == v) {  // w's component hangs off v: its block
+      blk = lw;
+      mine = v < lw;
+    } else {
+      blk = lu;
+      mine = row_u0;
+    }
     eblk[e] = blk;
-    if (blk != run_blk) {
+    if (mine && blk != run_blk) {
       flush();
       run_blk = blk;
       run_min = e;

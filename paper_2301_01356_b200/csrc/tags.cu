@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256, kWGatherMinBlocks) k_w_gather(const int64
               w_store(AP, r.x, m1, m2);
               if (kCount) nlow[v] = c;
             }
-            v = (a < __ldg(off + v + 2)) ? v + 1 : row_of(off, v + 1, n - 1, a);
+            v = next_row(off, v, n, a);
             rs = (int)__ldg(off + v);
             re = (int)__ldg(off + v + 1);
             r = __ldg(rec + v);
