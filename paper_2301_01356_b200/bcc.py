@@ -361,7 +361,7 @@ def fast_bcc(g: Graph, *, beta: float | None = None, seed: int = 0, block: int =
         stats, out, E = _host_session(g, dev).run(g)
         tim = _timings(stats)
         return BccLabeling(out["label"], out["head"], int(stats.num_bccs), int(stats.num_components), tim,
-                           out["edge_label"][:E], out["is_ap"].astype(bool))
+                           out["edge_label"][:E], out["is_ap"].view(np.bool_))
     if g._dev is None:  # device outputs from a host graph: upload, then the device path
         g = Graph.from_device(*[t.to(dev) for t in _pinned_or_numpy(g)])
     plan = _session(g, dev)
@@ -374,7 +374,7 @@ def fast_bcc(g: Graph, *, beta: float | None = None, seed: int = 0, block: int =
                            res["edge_label"], res["is_ap"])
     out = _to_host(res, ("label", "head", "edge_label", "is_ap"))
     return BccLabeling(out["label"], out["head"], int(stats.num_bccs), int(stats.num_components), tim,
-                       out["edge_label"], out["is_ap"].astype(bool))
+                       out["edge_label"], out["is_ap"].view(np.bool_))
 
 
 def _timings(stats) -> StepTimings:

@@ -35,7 +35,7 @@ constexpr int kMaxStreamChunks = 64;
 
 struct Layout {
   size_t total = 0;
-  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
+  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, hsub, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
       nlow, bmin, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
@@ -77,6 +77,7 @@ struct Layout {
     rootidx = take(4 * (n + 1));
     rlist = take(4 * n);
     lhead = take(4 * n);
+    hsub = take(4 * (m / 16 + 64));
     nexto = take(4 * N0);
     nxt = take(4 * N0);
     own0 = take(8 * N0);
@@ -131,6 +132,8 @@ struct Pipeline {
     R.rootidx = (int*)at(lay.rootidx);
     R.rlist = (int*)at(lay.rlist);
     R.lhead = (int*)at(lay.lhead);
+    R.hsub = (int*)at(lay.hsub);
+    R.hoff = offsets;
     R.nexto = (int*)at(lay.nexto);
     R.nxt = (int*)at(lay.nxt);
     R.own0 = (int2*)at(lay.own0);
@@ -171,7 +174,7 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    build_chunk_rows(g, const_cast<int*>(g.crow), st);
+    build_chunk_rows(g, const_cast<int*>(g.crow), sc, st);
     stage1_forest(g, comp, fe, prop, sc, st);
     mk(1);
     enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
@@ -238,7 +241,7 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    build_chunk_rows(g, const_cast<int*>(g.crow), st);
+    build_chunk_rows(g, const_cast<int*>(g.crow), sc, st);
     stage1_stream_begin(g, comp, st);
     for (int c = 0; c < nchunk; c++) {
       cudaStreamWaitEvent(st, ev_chunk[c], 0);

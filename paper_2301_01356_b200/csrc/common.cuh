@@ -23,7 +23,8 @@ struct Scalars {
   int nroots[16];  // roots after each sampling round's compress (stage 1: 0..7, stage 5: 8..15)
   int hooks[16];   // hooks accepted per sampling round (same split)
   int nheavy[2];   // super-heavy rows deferred by k_link_rows (stage 1 / stage 5 slot)
-  int pad[25];
+  int has_hubs;    // some row has >= kHubDeg slots (set by k_chunk_rows)
+  int pad[24];
 };
 
 // ---------------------------------------------------------------------------
@@ -254,6 +255,11 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
 // replaces a binary search per chunk in each arc-balanced kernel of a run
 // (consumers keep a row_of fallback for a negative entry).
 constexpr int kRowChunks = 64;
+
+// rows of at least kHubDeg slots get kHubWays out-list heads in rooting
+// (see k_root_flags)
+constexpr int kHubDeg = 1024;
+constexpr int kHubWays = 32;
 
 // Block-reduced counter add: every thread of the block must call it (after
 // its grid-stride loop) with its private count; one atomic per block.

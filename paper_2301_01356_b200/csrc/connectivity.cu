@@ -134,7 +134,7 @@ __device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
 // their own lane; longer (hub) rows by the whole warp, so a 600k-arc RMAT hub
 // costs 2.3k warp stores instead of one thread's 75k (consumers used to
 // binary-search hub chunks over all n rows: half of RMAT's gather passes).
-__global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow) {
+__global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow, Scalars* sc) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -146,6 +146,7 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
       q1 = (int)((__ldg(off + v + 1) + kItems - 1) / kItems);
     }
     const bool hub = q1 - q0 > kRowChunks;
+    if (hub && (int64_t)(q1 - q0) * kItems >= kHubDeg) sc->has_hubs = 1;
     if (!hub)
       for (int q = q0; q < q1; q++) crow[q] = v;
     unsigned hb = __ballot_sync(0xffffffffu, hub);
@@ -159,9 +160,9 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
   }
 }
 
-void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st) {
+void build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st) {
   if (g.m == 0) return;
-  launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow);
+  launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow, sc);
   note(K_CHUNK_ROWS);
 }
 

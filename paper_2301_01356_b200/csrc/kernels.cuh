@@ -16,7 +16,7 @@ struct Graph {
   const int* crow;       // [ceil(m/kItems)] chunk -> row table (build_chunk_rows)
 };
 
-void build_chunk_rows(const Graph& g, int* crow, cudaStream_t st);
+void build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st);
 
 // Device arrays for the rooting / tags stages (see api.cu for the layout).
 constexpr int kFinalMax = 16384;  // list-ranking level finished in one CTA
@@ -25,7 +25,9 @@ struct Rooting {
   int* flags;      // [n+1] comp[v] == v
   int* rootidx;    // [n+1] exclusive scan of flags (rank among roots)
   int* rlist;      // [n]   roots in id order
-  int* lhead;      // [n]   first out-arc of each vertex (-1: none)
+  int* lhead;      // [n]   first out-arc of each vertex (-1: none; <= -2: hub, see rooting.cu)
+  int* hsub;       // [m/16 + 64] hub sub-list heads (nullptr: no hub split)
+  const int64_t* hoff;  // CSR offsets the hubs are chosen from (nullptr: no hub split)
   int* nexto;      // [2n]  next out-arc of the same vertex
   int* nxt;        // [2n]  unified tour list successor
   int2* own0;      // [2n]  (segment, offset) per list element

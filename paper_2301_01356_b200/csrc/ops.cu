@@ -423,6 +423,8 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   R.rootidx = (int*)at(o_rootidx);
   R.rlist = (int*)at(o_rlist);
   R.lhead = (int*)at(o_lhead);
+  R.hsub = nullptr;  // pairs input: no CSR, no hub split
+  R.hoff = nullptr;
   R.nexto = (int*)at(o_nexto);
   R.nxt = (int*)at(o_nxt);
   R.own0 = (int2*)at(o_own0);
@@ -486,7 +488,7 @@ int op_compute_tags(const Graph& g, const int* parent, const int* first, const i
   while ((1 << tlev) <= ntile) tlev++;
   size_t o_rec = L.take(16 * n), o_ap = L.take(16 * (size_t)ntile * kTile), o_lh1 = L.take(8 * n),
          o_lh2 = L.take(8 * n), o_table = L.take(8 * (size_t)ntile * tlev), o_scr = L.take(3 * 4 * n),
-         o_crow = L.take(4 * ((g.m + kItems - 1) / kItems + 1));
+         o_crow = L.take(4 * ((g.m + kItems - 1) / kItems + 1)), o_sc = L.take(sizeof(Scalars));
   if (dry) {
     *need = L.total;
     return 0;
@@ -496,7 +498,7 @@ int op_compute_tags(const Graph& g, const int* parent, const int* first, const i
   auto at = [&](size_t o) { return (void*)(w + o); };
   Graph gg = g;
   gg.crow = (const int*)at(o_crow);
-  build_chunk_rows(gg, (int*)at(o_crow), st);
+  build_chunk_rows(gg, (int*)at(o_crow), (Scalars*)at(o_sc), st);  // (hub flag unused here)
   Rooting R{};
   R.rec = (int4*)at(o_rec);
   Tags T;

@@ -86,11 +86,33 @@ void scan_upper_degrees(const int64_t* off, const int* nlow, int n, int* uoff, v
 // roots in id order
 // ---------------------------------------------------------------------------
 // (also clears the out-arc list heads: same index space, no memset node)
-__global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restrict__ flags, int* __restrict__ lhead) {
+//
+// Hub split: every forest edge inserts its two arcs at the heads of its
+// endpoints' lists with atomicExch, so a vertex of tree degree d serialises d
+// returning atomics on one address (RMAT hubs: ~1e5, 2 ms).  Vertices of
+// CSR degree >= kHubDeg instead get 32 sub-lists (the inserting edge x picks
+// x & 31), whose heads live at hsub[(off[v] >> 4) + j] -- disjoint for rows
+// of >= 527 slots -- and lhead[v] = -2 - (off[v] >> 4) marks the vertex.
+// The tour walks a hub's sub-lists in order (k_link_tour).
+
+__global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restrict__ flags, int* __restrict__ lhead,
+                             const int64_t* __restrict__ off, int* __restrict__ hsub, const Scalars* sc) {
   pdl_enter();
+  if (off && !sc->has_hubs) off = nullptr;  // (k_chunk_rows saw no row that long)
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
     flags[v] = (v < n) ? (__ldg(comp + v) == v) : 0;
-    if (v < n) lhead[v] = -1;
+    if (v < n) {
+      int h = -1;
+      if (off) {
+        const int64_t rs = __ldg(off + v);
+        if (__ldg(off + v + 1) - rs >= kHubDeg) {
+          const int base = (int)(rs >> 4);
+          for (int j = 0; j < kHubWays; j++) hsub[base + j] = -1;
+          h = -2 - base;
+        }
+      }
+      lhead[v] = h;
+    }
   }
 }
 
@@ -105,15 +127,33 @@ __global__ void k_root_list(const int* __restrict__ comp, const int* __restrict_
 }
 
 // out-arc lists: arc 2x = u->v is an out-arc of u, 2x+1 = v->u of v
+__device__ __forceinline__ int* list_head(int* lhead, int* hsub, int t, int x, bool split) {
+  if (split) {
+    const int h = ld_relaxed(lhead + t);  // concurrent exchanges leave non-hubs >= -1
+    if (h <= -2) return hsub + (-2 - h) + (x & (kHubWays - 1));
+  }
+  return lhead + t;
+}
+
 __global__ void k_out_lists(const int* __restrict__ comp, const int2* __restrict__ fe, int n, int* lhead,
-                            int* __restrict__ nexto) {
+                            int* __restrict__ nexto, int* hsub, const Scalars* sc) {
   pdl_enter();
+  const bool split = hsub != nullptr && sc->has_hubs;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     if (__ldg(comp + x) == x) continue;
     int2 e = __ldg(fe + x);
-    nexto[2 * x] = atomicExch(lhead + e.x, 2 * x);
-    nexto[2 * x + 1] = atomicExch(lhead + e.y, 2 * x + 1);
+    nexto[2 * x] = atomicExch(list_head(lhead, hsub, e.x, x, split), 2 * x);
+    nexto[2 * x + 1] = atomicExch(list_head(lhead, hsub, e.y, x, split), 2 * x + 1);
   }
+}
+
+// first non-empty hub sub-list head at or after way j (-1: none)
+__device__ __forceinline__ int hub_next(const int* __restrict__ hsub, int base, int j) {
+  for (; j < kHubWays; j++) {
+    const int h = __ldg(hsub + base + j);
+    if (h >= 0) return h;
+  }
+  return -1;
 }
 
 // ---------------------------------------------------------------------------
@@ -140,7 +180,7 @@ __device__ __forceinline__ int flag_succ(int s, int sh, int N) {
 }
 
 __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict__ fe,
-                            const int* __restrict__ lhead, const int* __restrict__ nexto,
+                            const int* __restrict__ lhead, const int* __restrict__ hsub, const int* __restrict__ nexto,
                             const int* __restrict__ rootidx, const int* __restrict__ rlist, int n,
                             int* __restrict__ nxt, const Scalars* sc, int sh0) {
   pdl_enter();
@@ -152,6 +192,7 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
     if (__ldg(comp + x) == x) {  // enter(x) / exit(x)
       if ((e & 1) == 0) {
         int h = __ldg(lhead + x);
+        if (h <= -2) h = hub_next(hsub, -2 - h, 0);
         out = h >= 0 ? h : (int)e + 1;
       } else {
         int ri = __ldg(rootidx + x);
@@ -161,8 +202,15 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
       int2 uv = __ldg(fe + x);
       int t = (e & 1) ? uv.x : uv.y;
       int nx = __ldg(nexto + (e ^ 1));
-      if (nx >= 0) out = nx;
-      else out = (__ldg(comp + t) == t) ? 2 * t + 1 : __ldg(lhead + t);
+      if (nx >= 0) {
+        out = nx;
+      } else {  // end of t's list (of a hub's sub-list: the next non-empty one)
+        const int h = __ldg(lhead + t);
+        if (h <= -2) nx = hub_next(hsub, -2 - h, (x & (kHubWays - 1)) + 1);
+        if (nx >= 0) out = nx;
+        else if (__ldg(comp + t) == t) out = 2 * t + 1;
+        else out = h <= -2 ? hub_next(hsub, -2 - h, 0) : h;
+      }
     }
     nxt[e] = flag_succ(out, sh0, (int)N);
   }
@@ -319,7 +367,7 @@ __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict
 void rooting_roots(int n, const int* comp, Rooting& R, Scalars* sc, cudaStream_t st) {
   const int B = 256;
   const int gv = grid_for(n + 1, B);
-  launch(k_root_flags, gv, B, 0, st, comp, n, R.flags, R.lhead);
+  launch(k_root_flags, gv, B, 0, st, comp, n, R.flags, R.lhead, R.hoff, R.hoff ? R.hsub : nullptr, sc);
   note(K_ROOT_FLAGS);
   exclusive_scan(R.flags, R.rootidx, n + 1, R.cub_tmp, R.cub_bytes, st);
   note(K_SCAN);
@@ -332,7 +380,7 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
   rooting_roots(g.n, comp, R, sc, st);
   // Euler circuit: out-arc lists in atomicExch order (any order is a valid
   // tour; the final outputs do not depend on it)
-  launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto);
+  launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto, R.hoff ? R.hsub : nullptr, sc);
   note(K_OUT_LISTS);
   rooting_tour(g.n, comp, fe, R, AP, sc, st);
 }
@@ -346,7 +394,7 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
   // levels 1..nlev-1 are walked again (their successors carry splitter flags
   // for the next windowing); level nlev goes to the one-CTA final kernel
   auto sh_after = [&](int l) { return l < R.nlev ? shift(R.S[l]) : -1; };
-  launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.nexto, R.rootidx, R.rlist, n, R.nxt, sc,
+  launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.hsub, R.nexto, R.rootidx, R.rlist, n, R.nxt, sc,
                                              shift(R.S[0]));
   note(K_LINK_TOUR);
   // ruling-set levels

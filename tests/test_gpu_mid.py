@@ -23,6 +23,17 @@ def _star(k):
     return symmetrize(np.column_stack([np.zeros(k, np.int64), i]), k + 1)
 
 
+def _star_at(n, c):
+    i = np.setdiff1d(np.arange(n), [c])
+    return symmetrize(np.column_stack([np.full(i.size, c), i]), n)
+
+
+def _wheel_at(n, c):
+    i = np.setdiff1d(np.arange(n), [c])
+    rim = np.column_stack([i, np.roll(i, -1)])
+    return symmetrize(np.concatenate([np.column_stack([np.full(i.size, c), i]), rim]), n)
+
+
 def _with_isolated(g, extra):
     p = g.edge_pairs()
     p = p[p[:, 0] < p[:, 1]]
@@ -35,6 +46,9 @@ GRAPHS = {
     "chain_300k": lambda: workloads.chain(300_000),
     "cycle_50k": lambda: symmetrize(np.column_stack([np.arange(50_000), (np.arange(50_000) + 1) % 50_000]), 50_000),
     "star_100k": lambda: _star(100_000),
+    # hubs that are not the tree root (rooting's split out-lists, kHubDeg)
+    "star_mid_20k": lambda: _star_at(20_000, 7_777),
+    "wheel_mid_30k": lambda: _wheel_at(30_000, 12_345),
     "grid_300": lambda: workloads.grid(300, 300),
     "torus_200_p07": lambda: workloads.grid(200, 200, circular=True, keep_prob=0.7, seed=5),
     "uniform_64k_d3": lambda: workloads.uniform(1 << 16, 3, seed=1),
