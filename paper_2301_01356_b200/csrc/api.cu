@@ -29,7 +29,8 @@ int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*retired*/ 0, /*S0
                       /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last*/ 0,
                       /*retired*/ 0, /*retired*/ 0,
                       /*programmatic dependent launch (measured 5% slower on config 2: off)*/ 0,
-                      /*fbcc_run_host edge-copy chunks*/ 8, /*skeleton parent-edge rounds (hook_min + round 1)*/ 3};
+                      /*fbcc_run_host edge-copy chunks*/ 8, /*skeleton parent-edge rounds (hook_min + round 1)*/ 3,
+                      /*giant pick folded into the last compress*/ 1};
 constexpr int kFinalMaxHost = kFinalMax;
 constexpr int kMaxStreamChunks = 64;
 

@@ -24,7 +24,8 @@ struct Scalars {
   int hooks[16];   // hooks accepted per sampling round (same split)
   int nheavy[2];   // super-heavy rows deferred by k_link_rows (stage 1 / stage 5 slot)
   int has_hubs;    // some row has >= kHubDeg slots (set by k_chunk_rows)
-  int pad[24];
+  unsigned ticket; // last-block detection (k_compress; reset by the last block)
+  int pad[23];
 };
 
 // ---------------------------------------------------------------------------
@@ -75,6 +76,7 @@ enum Option : int {
   OPT_PDL = 11,           // programmatic dependent launch between consecutive kernels
   OPT_STREAM_CHUNKS = 12, // fbcc_run_host: arc ranges the edge copy is split into
   OPT_SKEL_PARENT = 13,   // Stage 5 sampling: bit r = round r samples the plain parent edge
+  OPT_GIANT_FOLD = 14,    // the last sampling compress also picks the giant (no k_find_giant)
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 16
 };

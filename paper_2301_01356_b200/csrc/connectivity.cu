@@ -294,7 +294,11 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
 // (doubling), for the deep chains of path-like graphs.
 constexpr int kL1Steps = 8;
 
-__global__ void k_compress(int* comp, int n, int* nroots) {
+__device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable);
+
+// giant_sc != nullptr: the last block to finish also picks the sampled giant
+// root (Afforest skip) -- one launch instead of a separate 1-block kernel.
+__global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable) {
   pdl_enter();
   int roots = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
@@ -316,31 +320,54 @@ __global__ void k_compress(int* comp, int n, int* nroots) {
     __stcg(comp + v, c);
   }
   if (nroots) block_count_add(nroots, roots);
+  if (giant_sc) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(&giant_sc->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      giant_of_block(comp, n, giant_sc, giant_enable);
+      if (threadIdx.x == 0) giant_sc->ticket = 0;  // ready for the next stage
+    }
+  }
 }
 
-// Most frequent root among 1024 sampled vertices (one block of 1024):
-// shared-memory open-addressing histogram, then a block argmax.
-__global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, bool enable) {
-  pdl_enter();
-  constexpr int H = 2048;
+// Most frequent root among 1024 sampled vertices, computed by ONE block
+// (any size dividing 1024) once comp is final: shared-memory open-addressing
+// histogram, then a block argmax (ties -> smaller root, deterministic).
+__device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable) {
+  constexpr int H = 2048, kSamples = 1024;
   __shared__ int key[H], num[H];
   __shared__ int bestc[32], bestv[32];
-  int t = threadIdx.x;
-  for (int i = t; i < H; i += 1024) { key[i] = -1; num[i] = 0; }
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int i = t; i < H; i += nt) { key[i] = -1; num[i] = 0; }
   __syncthreads();
-  int v = (int)(hash32(0x9E3779B9u * (uint32_t)(t + 1)) % (uint32_t)n);
-  int mine = comp[v];  // comp may not be flat here: climb to the root
-  for (int up = comp[mine]; up != mine; up = comp[mine]) mine = up;
-  int slot = hash32((uint32_t)mine) & (H - 1);
-  while (true) {
-    int k = atomicCAS(&key[slot], -1, mine);
-    if (k == -1 || k == mine) break;
-    slot = (slot + 1) & (H - 1);
+  int cnt = 0, mine = 0x7fffffff;
+  int slots[kSamples / 32];
+  const int per = kSamples / nt;
+  for (int k = 0; k < per; k++) {
+    const int s = t + k * nt;
+    const int v = (int)(hash32(0x9E3779B9u * (uint32_t)(s + 1)) % (uint32_t)n);
+    int r = __ldcg(comp + v);  // comp may not be flat here: climb to the root
+    for (int up = __ldcg(comp + r); up != r; up = __ldcg(comp + r)) r = up;
+    int slot = hash32((uint32_t)r) & (H - 1);
+    while (true) {
+      int kk = atomicCAS(&key[slot], -1, r);
+      if (kk == -1 || kk == r) break;
+      slot = (slot + 1) & (H - 1);
+    }
+    atomicAdd(&num[slot], 1);
+    slots[k] = slot;
   }
-  atomicAdd(&num[slot], 1);
   __syncthreads();
-  int cnt = num[slot];
-  // argmax (ties -> smaller root id, deterministic)
+  for (int k = 0; k < per; k++) {
+    const int c = num[slots[k]], r = key[slots[k]];
+    if (c > cnt || (c == cnt && r < mine)) { cnt = c; mine = r; }
+  }
   for (int o = 16; o > 0; o >>= 1) {
     int oc = __shfl_down_sync(0xffffffffu, cnt, o);
     int ov = __shfl_down_sync(0xffffffffu, mine, o);
@@ -349,7 +376,8 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, b
   if ((t & 31) == 0) { bestc[t >> 5] = cnt; bestv[t >> 5] = mine; }
   __syncthreads();
   if (t < 32) {
-    cnt = bestc[t]; mine = bestv[t];
+    cnt = t < (nt >> 5) ? bestc[t] : -1;
+    mine = t < (nt >> 5) ? bestv[t] : 0x7fffffff;
     for (int o = 16; o > 0; o >>= 1) {
       int oc = __shfl_down_sync(0xffffffffu, cnt, o);
       int ov = __shfl_down_sync(0xffffffffu, mine, o);
@@ -357,6 +385,11 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, b
     }
     if (t == 0) sc->giant = enable ? mine : -1;
   }
+}
+
+__global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, bool enable) {
+  pdl_enter();
+  giant_of_block(comp, n, sc, enable);
 }
 
 // Remaining arcs, row-filtered: each warp takes 32 consecutive rows and drops
@@ -480,12 +513,17 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       note(K_ACCEPT);
     }
     if ((cmask >> r) & 1) {
-      launch(k_compress, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr);
+      // the last sampling round's compress also picks the giant
+      const bool last_round = r == kRounds - 1 && g_opt[OPT_GIANT_FOLD];
+      launch(k_compress, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr, last_round ? sc : nullptr,
+             g_opt[OPT_GIANT_SKIP] != 0);
       note(K_COMPRESS);
     }
   }
-  launch(k_find_giant, 1, 1024, 0, st, comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
-  note(K_FIND_GIANT);
+  if (!g_opt[OPT_GIANT_FOLD] || kRounds == 0 || !((cmask >> (kRounds - 1)) & 1)) {  // not folded
+    launch(k_find_giant, 1, 1024, 0, st, comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
+    note(K_FIND_GIANT);
+  }
   if (g.m > 0) {
     // the proposal words are dead after the last accept: reuse them as the
     // super-heavy row list
@@ -498,7 +536,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
                                                                                      heavy, nheavy);
     note(K_LINK_HEAVY);
   }
-  launch(k_compress, gres, B, 0, st, comp, g.n, nroots + 7);  // final root count (= components)
+  launch(k_compress, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false);  // final root count (= components)
   note(K_COMPRESS);
 }
 
@@ -559,7 +597,7 @@ void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2
 
 void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st) {
   const int B = 256;
-  launch(k_compress, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7);
+  launch(k_compress, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false);
   note(K_COMPRESS);
 }
 

@@ -11,9 +11,10 @@
 //  * heads without a min pass: by the BCC tree-connectivity lemma
 //     a block is tree-connected through its head, so
 //    every member v of skeleton component l with label[parent[v]] != l is a
-//    tree child of the head: `head[l] = parent[v]` is an idempotent store
-//    (no packed-min over first[] like the reference).  A second per-label
-//    pass counts blocks and bumps the heads' saturating headed-counts.
+//    tree child of the head: all of them would store the same head[l] =
+//    parent[v] (no packed-min over first[] like the reference); the one
+//    member whose CAS claims head[l] also counts the block and bumps the
+//    head's saturating headed-count.
 //  * edge ids: CUB scan of the upper degrees deg - nlow (nlow counted by the
 //    Stage-3 gather pass over the same arcs).
 //  * per-block minimum edge id: only the arcs of each block's minimum vertex
@@ -28,29 +29,25 @@ namespace fbcc {
 
 // Every member of component l whose tree parent lies outside l has that
 // parent equal to the block's head (all such members are children of the
-// head: the block is tree-connected through its head),
-// so the concurrent stores are idempotent.
-__global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restrict__ label, int* head) {
+// head: the block is tree-connected through its head).
+// The first of them to CAS head[l] from -1 also counts the block and bumps
+// the head's saturating headed-count for the articulation rule of
+// bcc.py:229-234 -- heads and the block count in one pass.
+__global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restrict__ label, int* head, int* cnt,
+                        Scalars* sc) {
   pdl_enter();
+  int blocks = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int p = __ldg(&rec[v].z);
     if (p >= 0) {
       int l = __ldg(label + v);
-      if (l != __ldg(label + p)) head[l] = p;
+      // (read first: the children of one head inside one component -- RMAT
+      // hubs -- would otherwise serialise their CAS on one word)
+      if (l != __ldg(label + p) && ld_relaxed(head + l) == -1 && atomicCAS(head + l, -1, p) == -1) {
+        blocks++;
+        if (ld_relaxed(cnt + p) < 2) atomicAdd(cnt + p, 1);
+      }
     }
-  }
-}
-
-// one thread per label: count the block and bump its head's (saturating)
-// headed-count for the articulation rule of bcc.py:229-234
-__global__ void k_count_blocks(int n, const int* __restrict__ head, int* cnt, Scalars* sc) {
-  pdl_enter();
-  int blocks = 0;
-  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
-    int h = __ldg(head + l);
-    if (h < 0) continue;
-    blocks++;
-    if (ld_relaxed(cnt + h) < 2) atomicAdd(cnt + h, 1);
   }
   block_count_add(&sc->nbccs, blocks);
 }
@@ -163,10 +160,8 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   const int B = 256;
   const int gv = grid_for(n + 1, B);
   // head = -1, cnt = 0, bmin = INF were initialised by the stage-4 kernel
-  launch(k_heads, gv, B, 0, st, n, rec, label, head);
+  launch(k_heads, gv, B, 0, st, n, rec, label, head, cnt, sc);
   note(K_HEADS);
-  launch(k_count_blocks, gv, B, 0, st, n, head, cnt, sc);
-  note(K_COUNT_BLOCKS);
   if (is_ap) {
     launch(k_ap, gv, B, 0, st, n, label, head, cnt, is_ap);
     note(K_AP);
