@@ -129,7 +129,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(g, runs=3):
+def cpu_baseline(g, config, runs=3):
     """The reference algorithm on the host cores (golden-pinned C port)."""
     import oracle
 
@@ -143,7 +143,7 @@ def cpu_baseline(g, runs=3):
         secs.append(time.perf_counter() - t0)
     s = statistics.median(secs)
     return {"value": E / s, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port",
-            "sample": f"full config-2 graph ({E} edges), median of {runs} runs after 1 warm-up, "
+            "sample": f"full config-{config} graph ({E} edges), median of {runs} runs after 1 warm-up, "
                       f"{s:.3f} s/run", "seconds_per_run": s}
 
 
@@ -345,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
             "num_bccs": int(stats.num_bccs), "num_components": int(stats.num_components),
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(g)
+            line["cpu_baseline"] = cpu_baseline(g, args.config)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -82,7 +82,7 @@ __device__ __forceinline__ bool keep(const PredData& pd, int v, const int4& rv, 
 // ---------------------------------------------------------------------------
 // Root of x with path halving.  Only non-roots are rewritten, always to an
 // ancestor (ancestors stay ancestors: sets only merge), and roots change only
-// through the hooking CAS -- so the concurrent plain stores are benign.
+// through the hooking CAS -- so the concurrent rewrites are benign.
 //
 // Parent reads are L1-cacheable (ld.global.ca).  Every value comp[x] ever
 // held is an ancestor of x, so a stale line can only (a) make two endpoints
@@ -98,7 +98,10 @@ __device__ __forceinline__ int find_halve(int* comp, int x) {
   while (p != x) {
     int gp = ldp(comp + p);
     if (gp == p) return p;
-    comp[x] = gp;
+    // non-returning atomicMin (RED) rather than a store: ancestors have
+    // smaller ids, so a shortcut another thread made (or a fresher value
+    // than our possibly stale L1 copy) is never undone (config 3: -13%)
+    atomicMin(comp + x, gp);
     x = gp;
     p = ldp(comp + x);
   }
