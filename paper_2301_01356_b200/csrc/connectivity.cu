@@ -111,8 +111,10 @@ __device__ __forceinline__ int find_halve(int* comp, int x) {
 // Hook the larger root under the smaller.  A successful CAS hooks root `hi`
 // under `lo`, whose set holds the other endpoint (root(lo) <= lo < hi), so
 // (u, w) is a spanning-forest edge joining two distinct sets.
+// Returns the root the two sets were joined under (an ancestor of u, for the
+// caller's next comparison).
 template <bool kRecord>
-__device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
+__device__ __forceinline__ int link(int u, int w, int* comp, int2* fe) {
   int ru = find_halve(comp, u);
   int rw = find_halve(comp, w);
   while (ru != rw) {
@@ -121,11 +123,12 @@ __device__ __forceinline__ void link(int u, int w, int* comp, int2* fe) {
     int prev = atomicCAS(comp + hi, hi, lo);
     if (prev == hi) {
       if (kRecord) fe[hi] = make_int2(u, w);
-      return;
+      return lo;
     }
     ru = find_halve(comp, prev);  // hi was hooked meanwhile: climb on
     rw = find_halve(comp, lo);
   }
+  return ru;
 }
 
 // ---------------------------------------------------------------------------
@@ -403,8 +406,18 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, b
 // striding over the arcs (a non-giant hub cannot serialise one thread).
 constexpr int kSuperRow = 8192;
 
+// 4-arc batches at 32 registers (full occupancy) measured best across
+// configs 2/3/4b/4c/5 (8-arc batches at 64 registers: 4b/4c +4 %)
+#ifndef FBCC_LR_BATCH
+#define FBCC_LR_BATCH 4
+#endif
+#ifndef FBCC_LR_MINB
+#define FBCC_LR_MINB 8
+#endif
+constexpr int kLinkBatch = FBCC_LR_BATCH;
+
 template <int kPred, bool kRecord>
-__global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+__global__ void __launch_bounds__(256, FBCC_LR_MINB) k_link_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                    int n, int* comp, int2* fe, PredData pd, const Scalars* sc,
                                                    int* heavy_list, int* nheavy) {
   pdl_enter();
@@ -431,10 +444,35 @@ __global__ void __launch_bounds__(256) k_link_rows(const int64_t* __restrict__ o
     if (!heavy && re > rs) {
       int4 rv;
       if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
-      for (int64_t a = rs; a < re; a++) {
-        int w = (int)__ldg(adj + a);
-        if (!keep<kPred>(pd, v, rv, w, a)) continue;
-        link<kRecord>(v, w, comp, fe);
+      // A row's links would be a chain of dependent finds; most targets are
+      // already in v's set, so test kLinkBatch arcs at a time with independent loads
+      // of comp[w] (and its parent) against v's current root and link only
+      // the rest (config 2: one surviving degree-16 row no longer holds its
+      // warp for 16 serial links).
+      int root = -1;  // found lazily: under a predicate most rows keep no arc
+      const int r0 = (int)rs, r1 = (int)re;  // slot indices fit 32 bits (check_sizes)
+      for (int a0 = r0; a0 < r1; a0 += kLinkBatch) {
+        const int cnt = r1 - a0 < kLinkBatch ? r1 - a0 : kLinkBatch;
+        int w[kLinkBatch], c[kLinkBatch];
+        bool k[kLinkBatch];
+#pragma unroll
+        for (int i = 0; i < kLinkBatch; i++) w[i] = i < cnt ? (int)__ldg(adj + a0 + i) : v;
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < kLinkBatch; i++) {
+          k[i] = i < cnt && keep<kPred>(pd, v, rv, w[i], a0 + i);
+          any |= k[i];
+        }
+        if (!any) continue;
+        if (root < 0) root = find_halve(comp, v);
+#pragma unroll
+        for (int i = 0; i < kLinkBatch; i++) c[i] = k[i] ? ldp(comp + w[i]) : root;
+#pragma unroll
+        for (int i = 0; i < kLinkBatch; i++)
+          if (k[i] && c[i] != root) c[i] = ldp(comp + c[i]);
+#pragma unroll
+        for (int i = 0; i < kLinkBatch; i++)  // (root moves with each link: test k[i] again)
+          if (k[i] && c[i] != root) root = link<kRecord>(v, w[i], comp, fe);
       }
     }
     unsigned hb = __ballot_sync(0xffffffffu, heavy);
