@@ -30,14 +30,15 @@ int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*retired*/ 0, /*S0
                       /*retired*/ 0, /*retired*/ 0,
                       /*programmatic dependent launch (measured 5% slower on config 2: off)*/ 0,
                       /*fbcc_run_host edge-copy chunks*/ 8, /*skeleton parent-edge rounds (hook_min + round 1)*/ 3,
-                      /*giant pick folded into the last compress*/ 1};
+                      /*giant pick folded into the last compress*/ 1,
+                      /*warp-staged edge-block pass with the giant bitmap*/ 1};
 constexpr int kFinalMaxHost = kFinalMax;
 constexpr int kMaxStreamChunks = 64;
 
 struct Layout {
   size_t total = 0;
   size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, hsub, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
-      nlow, bmin, cub;
+      nlow, bmin, gbits, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
   int64_t K[8] = {0};
@@ -98,6 +99,7 @@ struct Layout {
     uoff = take(4 * (n + 1));
     nlow = take(4 * n);
     bmin = take(4 * n);
+    gbits = take(4 * ((n + 31) / 32 + 4));
     cub = take(cub_bytes);
   }
 };
@@ -117,6 +119,7 @@ struct Pipeline {
   int* uoff;
   int* nlow;
   int* bmin;
+  uint32_t* gbits;  // [ceil(n/32)] Stage 6: bit v = v in the giant skeleton component
 
   Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
            const fbcc_outputs* o)
@@ -167,6 +170,7 @@ struct Pipeline {
     uoff = (int*)at(lay.uoff);
     nlow = (int*)at(lay.nlow);
     bmin = (int*)at(lay.bmin);
+    gbits = (uint32_t*)at(lay.gbits);
   }
 
   // Enqueue all six stages.  ev (7 events) brackets the stages when given.
@@ -206,7 +210,7 @@ struct Pipeline {
     stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st);
     mk(5);
     if (label_done) cudaEventRecord(label_done, st);
-    stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, R.cub_tmp,
+    stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, gbits, R.cub_tmp,
                      R.cub_bytes, sc, st, heads_done);
     mk(6);
   }

@@ -77,6 +77,7 @@ enum Option : int {
   OPT_STREAM_CHUNKS = 12, // fbcc_run_host: arc ranges the edge copy is split into
   OPT_SKEL_PARENT = 13,   // Stage 5 sampling: bit r = round r samples the plain parent edge
   OPT_GIANT_FOLD = 14,    // the last sampling compress also picks the giant (no k_find_giant)
+  OPT_EB_STAGED = 15,     // Stage 6 edge blocks: warp-staged rows + giant bitmap (0: plain arc visitor)
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 16
 };

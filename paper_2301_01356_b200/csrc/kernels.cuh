@@ -80,7 +80,7 @@ void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out,
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
                         cudaStream_t st);
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
-                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
+                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, uint32_t* gbits, void* cub_tmp,
                       size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done = nullptr);
 void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* AP, int* forest,
                   int* parent, int* first, int* last, int* w1, int* w2, uint8_t* fence,

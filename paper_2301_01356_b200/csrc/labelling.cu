@@ -33,21 +33,37 @@ namespace fbcc {
 // The first of them to CAS head[l] from -1 also counts the block and bumps
 // the head's saturating headed-count for the articulation rule of
 // bcc.py:229-234 -- heads and the block count in one pass.
+// Label of the giant skeleton component (Stage 5's sampled giant root, now
+// under its final label), or -1.  Every kernel recomputes it from the same
+// two words, so the bitmap and its readers agree.
+__device__ __forceinline__ int giant_label(const int* label, const Scalars* sc) {
+  const int gi = sc->giant;
+  return gi >= 0 ? __ldg(label + gi) : -1;
+}
+
 __global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restrict__ label, int* head, int* cnt,
-                        Scalars* sc) {
+                        uint32_t* __restrict__ gbits, Scalars* sc) {
   pdl_enter();
+  const int G = giant_label(label, sc);
+  const int lane = threadIdx.x & 31;
   int blocks = 0;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    int p = __ldg(&rec[v].z);
-    if (p >= 0) {
-      int l = __ldg(label + v);
+  // warp-uniform trip count: the warp also writes one word of the giant bitmap
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)base + lane;
+    int l = -1;
+    if (v < n) {
+      l = __ldg(label + v);
+      int p = __ldg(&rec[v].z);
       // (read first: the children of one head inside one component -- RMAT
       // hubs -- would otherwise serialise their CAS on one word)
-      if (l != __ldg(label + p) && ld_relaxed(head + l) == -1 && atomicCAS(head + l, -1, p) == -1) {
+      if (p >= 0 && l != __ldg(label + p) && ld_relaxed(head + l) == -1 && atomicCAS(head + l, -1, p) == -1) {
         blocks++;
         if (ld_relaxed(cnt + p) < 2) atomicAdd(cnt + p, 1);
       }
     }
+    const unsigned bits = __ballot_sync(0xffffffffu, l == G && G >= 0);
+    if (lane == 0) gbits[base >> 5] = bits;
   }
   block_count_add(&sc->nbccs, blocks);
 }
@@ -143,6 +159,134 @@ __global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__
   vis.flush();
 }
 
+// Warp-staged variant.  Each warp owns 256 consecutive arcs (8 per lane, as
+// visit_arc_chunks); the per-row words every arc needs -- row end, label,
+// edge-id base, "block minimum row" flag -- are loaded ONCE per row, coalesced,
+// by the lane whose index is the row's offset from the warp's first row, into
+// a per-warp shared-memory window of kEBRows rows (rows beyond it fall back to
+// global loads).  label[w] is replaced, for the common case, by one bit of the
+// giant-component bitmap (bit w = label[w] == G; k_heads), held in shared
+// memory (configs 2/3: 128 KB per CTA, one 1024-thread CTA per SM).  Only
+// arcs leaving the giant gather label[w] / head[label[w]].  Used when the
+// bitmap fits (n <= 1.6M); larger graphs run k_edge_blocks (a global bitmap
+// measured 13% slower than the label gather on RMAT, whose hubs keep label
+// lines L1-resident).
+constexpr int kEBRows = 64;
+constexpr int kEBThreads = 1024;
+constexpr int kEBMaxSmemBytes = 227 * 1024;
+
+__host__ __device__ constexpr size_t eb_rows_bytes(int threads) { return sizeof(int4) * kEBRows * (threads / 32); }
+
+__device__ __forceinline__ int4 eb_row(const int64_t* __restrict__ off, const int* __restrict__ label,
+                                       const int* __restrict__ head, const int* __restrict__ uoff,
+                                       const int* __restrict__ nlow, int r) {
+  const int64_t rs = __ldg(off + r);
+  const int re = (int)__ldg(off + r + 1);
+  const int h = __ldg(head + r);
+  return make_int4(re, __ldg(label + r), __ldg(uoff + r) - (int)(rs + __ldg(nlow + r)), (h >= 0 && r < h) ? 1 : 0);
+}
+
+__global__ void __launch_bounds__(kEBThreads, 1)
+    k_edge_blocks_ws(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
+                     int n, int64_t m, const int* __restrict__ label, const int* __restrict__ head,
+                     const int* __restrict__ uoff, const int* __restrict__ nlow, const uint32_t* __restrict__ gbits,
+                     const Scalars* sc, int* __restrict__ eblk, int* bmin) {
+  pdl_enter();
+  extern __shared__ int4 ebsm[];
+  constexpr int kThreads = kEBThreads;
+  int4* rows = ebsm + (threadIdx.x >> 5) * kEBRows;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(ebsm + kEBRows * (kThreads / 32));
+  const int nw4 = ((n + 31) / 32 + 3) / 4;
+  for (int i = threadIdx.x; i < nw4; i += kThreads)
+    reinterpret_cast<uint4*>(bits)[i] = __ldg(reinterpret_cast<const uint4*>(gbits) + i);
+  __syncthreads();
+  const int G = giant_label(label, sc);
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunks = (m + kItems - 1) / kItems;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  int run_blk = -1, run_min = 0;
+  for (int64_t qb = (int64_t)blockIdx.x * kThreads + (threadIdx.x & ~31); qb < nchunks; qb += stride) {
+    const int64_t q = qb + lane;
+    const bool live = q < nchunks;
+    int v = 0;
+    uint32_t w[kItems];
+    int64_t a0 = q * kItems, a1 = a0;
+    if (live) {
+      a1 = a0 + kItems < m ? a0 + kItems : m;
+      if (vec_ok && a1 - a0 == kItems) {
+        int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
+        int4 y = ld_stream4(reinterpret_cast<const int4*>(adj + a0 + 4));
+        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+        w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;
+      }
+      v = __ldg(crow + q);
+      if (v < 0) v = row_of(off, 0, n - 1, a0);
+    }
+    const int vf = __shfl_sync(0xffffffffu, v, 0);  // lane 0 is live whenever the warp is
+    __syncwarp();  // the previous iteration's readers of the window are done
+#pragma unroll
+    for (int k = 0; k < kEBRows; k += 32) {
+      const int r = vf + k + lane;
+      if (r < n) rows[k + lane] = eb_row(off, label, head, uoff, nlow, r);
+    }
+    __syncwarp();
+    if (live) {
+      int vi = v - vf;
+      int4 R = vi < kEBRows ? rows[vi] : eb_row(off, label, head, uoff, nlow, v);
+#pragma unroll
+      for (int i = 0; i < kItems; i++) {
+        const int a = (int)(a0 + i);
+        if (a < (int)a1) {
+          while (a >= R.x) {  // next non-empty row (empty rows share the end)
+            if (vi + 1 < kEBRows) {
+              vi++;
+              v++;
+              R = rows[vi];
+            } else {
+              v = next_row(off, v, n, a);
+              vi = kEBRows;
+              R = eb_row(off, label, head, uoff, nlow, v);
+            }
+          }
+          const int x = (int)w[i];
+          if (x > v) {
+            int blk;
+            bool mine;
+            if (R.y == G && ((bits[x >> 5] >> (x & 31)) & 1u)) {
+              blk = G;
+              mine = R.w != 0;
+            } else {
+              const int lw = __ldg(label + x);
+              if (R.y == lw) {
+                blk = lw;
+                mine = R.w != 0;
+              } else if (__ldg(head + lw) == v) {  // x's component hangs off v: its block
+                blk = lw;
+                mine = v < lw;
+              } else {
+                blk = R.y;
+                mine = R.w != 0;
+              }
+            }
+            const int e = R.z + a;
+            eblk[e] = blk;
+            if (mine && blk != run_blk) {
+              if (run_blk >= 0) atomicMin(bmin + run_blk, run_min);
+              run_blk = blk;
+              run_min = e;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (run_blk >= 0) atomicMin(bmin + run_blk, run_min);
+}
+
 __global__ void k_edge_final(int* eblk, const int* __restrict__ bmin, const int* __restrict__ uoff, int n) {
   pdl_enter();
   const int E = uoff[n];
@@ -154,13 +298,13 @@ __global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) {
   pdl_enter(); sc->num_edges = uoff[n]; }
 
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
-                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, void* cub_tmp,
+                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, uint32_t* gbits, void* cub_tmp,
                       size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done) {
   const int n = g.n;
   const int B = 256;
   const int gv = grid_for(n + 1, B);
   // head = -1, cnt = 0, bmin = INF were initialised by the stage-4 kernel
-  launch(k_heads, gv, B, 0, st, n, rec, label, head, cnt, sc);
+  launch(k_heads, gv, B, 0, st, n, rec, label, head, cnt, gbits, sc);
   note(K_HEADS);
   if (is_ap) {
     launch(k_ap, gv, B, 0, st, n, label, head, cnt, is_ap);
@@ -175,8 +319,15 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   note(K_SET_EDGES);
   if (edge_label && g.m > 0) {
     int64_t nchunks = (g.m + kItems - 1) / kItems;
-    launch(k_edge_blocks, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow,
-                                                          edge_label, bmin);
+    const size_t smem = eb_rows_bytes(kEBThreads) + 16 * (size_t)(((n + 31) / 32 + 3) / 4);
+    if (g_opt[OPT_EB_STAGED] && smem <= (size_t)kEBMaxSmemBytes) {
+      cudaFuncSetAttribute(k_edge_blocks_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      launch(k_edge_blocks_ws, grid_for(nchunks, kEBThreads, 1), kEBThreads, smem, st, g.off, g.adj, g.crow, n, g.m,
+             label, head, uoff, nlow, (const uint32_t*)gbits, (const Scalars*)sc, edge_label, bmin);
+    } else {
+      launch(k_edge_blocks, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow,
+             edge_label, bmin);
+    }
     note(K_EDGE_BLOCKS);
     launch(k_edge_final, grid_for(g.m / 2, B), B, 0, st, edge_label, bmin, uoff, n);
     note(K_EDGE_FINAL);

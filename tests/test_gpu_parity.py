@@ -186,7 +186,7 @@ def test_repeat_runs_identical():
             assert np.array_equal(a[k], b[k]), k
 
 
-@pytest.mark.parametrize("name", ["1", "2"])
+@pytest.mark.parametrize("name", ["1", "2", "3"])
 def test_public_api_paths_match_reference(name, config_meta):
     """fast_bcc on a pageable host graph, a pinned one (fbcc_run_host: streamed
     upload, Stage 1 linked per arrived range, for several range counts), a
