@@ -71,6 +71,21 @@ def alg_bytes(kind, n, m, T, E, K1=0):
     }.get(kind)
 
 
+def measured_gather_peak(n, gathers):
+    """Streamed-index random-gather rate measured by tools/gather_peak.py for
+    the gathered-array size closest to n 4-byte words (and gather count)."""
+    import math
+
+    try:
+        d = json.loads((ROOT / "profiles" / "r1_gather_peak.json").read_text())
+        best = min(d["gather"], key=lambda r: (abs(math.log2(r["elements"]) - math.log2(max(n, 2))),
+                                               abs(math.log2(r["gathers"]) - math.log2(max(gathers, 2)))))
+        return best["streamed_idx_per_s"], (f"profiles/r1_gather_peak.json: {best['array']}, "
+                                            f"{best['gathers']} gathers ({d.get('device', '')})")
+    except Exception:
+        return None, "unavailable"
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -310,18 +325,20 @@ def run_ours(args, rank, world, local_rank):
                 traffic = json.loads(prof.read_text()).get(f"config{args.config}", {}).get(dom)
             except Exception:
                 traffic = None
-        # Random 4-byte gathers are bounded by the L1TEX wavefront rate (one
-        # 128 B line per cycle per SM, B300_MICROARCH.md "L1tex wavefront
-        # queue") long before HBM: report the gather rate against that too.
+        # Random 4-byte gathers are bounded by the L1TEX line rate (one 128 B
+        # wavefront per cycle per SM) long before HBM: report the kernel's
+        # gather rate against the rate measured for the same access pattern
+        # on this B200 (tools/gather_peak.py: streamed 16 B index loads, 8
+        # random 4-byte gathers per thread, gathered array of the same size).
         gathers = {"w_gather": m, "edge_blocks": E}.get(dom)
         clocks = clk.summary()
         gather_bound = None
-        if gathers and clocks.get("sm_mhz"):
+        if gathers:
             g_rate = gathers / (kern[dom]["ms_per_launch"] / 1e3)
-            g_peak = 148 * clocks["sm_mhz"] * 1e6
-            gather_bound = {"gathers_per_launch": gathers, "achieved_per_s": g_rate,
-                            "peak_lines_per_s": g_peak, "frac": g_rate / g_peak,
-                            "model": "148 SMs x 1 L1TEX wavefront/cycle x median SM clock"}
+            g_peak, g_src = measured_gather_peak(n, gathers)
+            gather_bound = {"gathers_per_launch": gathers, "achieved_per_s": g_rate, "peak_per_s": g_peak,
+                            "frac": g_rate / g_peak if g_peak else None, "peak_source": g_src,
+                            "l1tex_model_per_s": 148 * (clocks.get("sm_mhz") or 1965.0) * 1e6}
         sum_alg = 46 * m + 165 * n + 48 * T + 16  # SURVEY §8(d) end-to-end algorithmic bytes
         ms = total_ms / args.steps
         line = {

@@ -93,9 +93,14 @@ extern int g_opt[OPT_NUM];
 // programmatic edges).  No kernel touches global memory before the wait, so
 // write-after-read across kernels is ordered as with plain launches.
 // ---------------------------------------------------------------------------
+#ifndef FBCC_PDL_EARLY_TRIGGER
+#define FBCC_PDL_EARLY_TRIGGER 1
+#endif
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if FBCC_PDL_EARLY_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 template <typename... KArgs, typename... Args>

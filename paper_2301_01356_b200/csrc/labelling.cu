@@ -227,28 +227,31 @@ __global__ void __launch_bounds__(kEBThreads, 1)
       if (v < 0) v = row_of(off, 0, n - 1, a0);
     }
     const int vf = __shfl_sync(0xffffffffu, v, 0);  // lane 0 is live whenever the warp is
+    // rows the warp can touch: up to the last live lane's row plus the rows
+    // its 8 arcs may still enter
+    const int vl = __reduce_max_sync(0xffffffffu, live ? v : vf);
+    const int rend = min(min(vf + kEBRows, vl + kItems + 1), n);
     __syncwarp();  // the previous iteration's readers of the window are done
 #pragma unroll
     for (int k = 0; k < kEBRows; k += 32) {
       const int r = vf + k + lane;
-      if (r < n) rows[k + lane] = eb_row(off, label, head, uoff, nlow, r);
+      if (r < rend) rows[k + lane] = eb_row(off, label, head, uoff, nlow, r);
     }
     __syncwarp();
     if (live) {
       int vi = v - vf;
-      int4 R = vi < kEBRows ? rows[vi] : eb_row(off, label, head, uoff, nlow, v);
+      int4 R = v < rend ? rows[vi] : eb_row(off, label, head, uoff, nlow, v);
 #pragma unroll
       for (int i = 0; i < kItems; i++) {
         const int a = (int)(a0 + i);
         if (a < (int)a1) {
           while (a >= R.x) {  // next non-empty row (empty rows share the end)
-            if (vi + 1 < kEBRows) {
+            if (v + 1 < rend) {
               vi++;
               v++;
               R = rows[vi];
             } else {
               v = next_row(off, v, n, a);
-              vi = kEBRows;
               R = eb_row(off, label, head, uoff, nlow, v);
             }
           }
