@@ -28,7 +28,7 @@ static int cuda_fail(cudaError_t e, const char* where) {
 int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*retired*/ 0, /*S0*/ 16, /*SL*/ 8,
                       /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last*/ 0,
                       /*retired*/ 0, /*retired*/ 0,
-                      /*programmatic dependent launch (measured 5% slower on config 2: off)*/ 0,
+                      /*programmatic dependent launch (dependents launch as the previous grid exits)*/ 1,
                       /*fbcc_run_host edge-copy chunks*/ 8, /*skeleton parent-edge rounds (hook_min + round 1)*/ 3,
                       /*giant pick folded into the last compress*/ 1,
                       /*warp-staged edge-block pass with the giant bitmap*/ 1};
@@ -179,8 +179,8 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    build_chunk_rows(g, const_cast<int*>(g.crow), sc, st);
-    stage1_forest(g, comp, fe, prop, sc, st);
+    const bool round0 = build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, comp, fe, prop);
+    stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args());
     mk(1);
     enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
   }
@@ -199,9 +199,20 @@ struct Pipeline {
 
   // Stages 2-6.  label_done / heads_done (optional) are recorded as soon as
   // the label array / the head and is_ap arrays are final.
+  // Stage 1's final compress writes Stage 2's root flags and list heads
+  RootInit root_init_args() const {
+    RootInit ri;
+    ri.flags = R.flags;
+    ri.lhead = R.lhead;
+    ri.hsub = R.hsub;
+    ri.off = R.hoff;
+    ri.sc = sc;
+    return ri;
+  }
+
   void enqueue_rest(cudaStream_t st, const Marks& mk, int* low_out, int* high_out, cudaEvent_t label_done,
                     cudaEvent_t heads_done) {
-    stage2_rooting(g, comp, fe, R, T.AP, sc, st);
+    stage2_rooting_fused(g, comp, fe, R, T.AP, sc, st);
     mk(2);
     stage3_tags(g, R, T, st, nlow);
     mk(3);
@@ -252,7 +263,7 @@ struct Pipeline {
       cudaStreamWaitEvent(st, ev_chunk[c], 0);
       stage1_stream_range(g, qb[c], qb[c + 1], comp, fe, st);
     }
-    stage1_stream_finish(g, comp, sc, st);
+    stage1_stream_finish(g, comp, sc, st, root_init_args());
     mk(1);
     enqueue_rest(st, mk, nullptr, nullptr, ev_label, ev_heads);
     if (io.label) {

@@ -94,7 +94,7 @@ extern int g_opt[OPT_NUM];
 // write-after-read across kernels is ordered as with plain launches.
 // ---------------------------------------------------------------------------
 #ifndef FBCC_PDL_EARLY_TRIGGER
-#define FBCC_PDL_EARLY_TRIGGER 1
+#define FBCC_PDL_EARLY_TRIGGER 0
 #endif
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");

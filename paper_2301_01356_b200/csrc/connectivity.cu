@@ -140,7 +140,13 @@ __device__ __forceinline__ int link(int u, int w, int* comp, int2* fe) {
 // their own lane; longer (hub) rows by the whole warp, so a 600k-arc RMAT hub
 // costs 2.3k warp stores instead of one thread's 75k (consumers used to
 // binary-search hub chunks over all n rows: half of RMAT's gather passes).
-__global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow, Scalars* sc) {
+//
+// The pipeline's Stage 1 also folds its sampling round 0 (k_hook_min<NONE>:
+// comp[v] = min(v, first neighbour), the forest edge, the proposal reset)
+// into this pass over the offsets (comp != nullptr).
+__global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow, Scalars* sc,
+                             const uint32_t* __restrict__ adj, int* __restrict__ comp, int2* __restrict__ fe,
+                             unsigned long long* __restrict__ prop) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -148,8 +154,21 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
     const int v = (int)base + lane;
     int q0 = 0, q1 = 0;
     if (v < n) {
-      q0 = (int)((__ldg(off + v) + kItems - 1) / kItems);
-      q1 = (int)((__ldg(off + v + 1) + kItems - 1) / kItems);
+      const int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+      q0 = (int)((rs + kItems - 1) / kItems);
+      q1 = (int)((re + kItems - 1) / kItems);
+      if (comp) {  // sampling round 0 (see k_hook_min)
+        int c = v;
+        if (rs < re) {
+          const int w = (int)__ldg(adj + rs);
+          if (w < v) {
+            c = w;
+            fe[v] = make_int2(v, w);
+          }
+        }
+        comp[v] = c;
+        prop[v] = ~0ull;
+      }
     }
     const bool hub = q1 - q0 > kRowChunks;
     if (hub && (int64_t)(q1 - q0) * kItems >= kHubDeg) sc->has_hubs = 1;
@@ -166,10 +185,13 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
   }
 }
 
-void build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st) {
-  if (g.m == 0) return;
-  launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow, sc);
+bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp, int2* fe,
+                      unsigned long long* prop) {
+  if (g.m == 0) return false;
+  const bool fold = comp != nullptr && g_opt[OPT_SAMPLE_ROUNDS] > 0;
+  launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow, sc, g.adj, fold ? comp : nullptr, fe, prop);
   note(K_CHUNK_ROWS);
+  return fold;
 }
 
 // Sampling round 0 without atomics.  With every vertex its own root, the
@@ -304,12 +326,15 @@ __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable)
 
 // giant_sc != nullptr: the last block to finish also picks the sampled giant
 // root (Afforest skip) -- one launch instead of a separate 1-block kernel.
-__global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable) {
+__global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable, RootInit ri) {
   pdl_enter();
   int roots = 0;
+  const int64_t* hoff = (ri.flags && ri.off && ri.sc->has_hubs) ? ri.off : nullptr;
+  if (ri.flags && blockIdx.x == 0 && threadIdx.x == 0) ri.flags[n] = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int c = __ldcg(comp + v);
     roots += (c == v);
+    if (ri.flags) root_init(ri, hoff, v, c == v);
     if (c == v) continue;
     bool done = false;
     for (int i = 0; i < kL1Steps; i++) {
@@ -519,9 +544,11 @@ __global__ void __launch_bounds__(256) k_link_heavy(const int64_t* __restrict__ 
 // The schedule shared by Stage 1 (no predicate, forest recorded), Stage 5
 // (skeleton predicate) and the masked stand-alone op.  `slot` picks the
 // sampling counters (0 / 8) in Scalars.
+// round0_done: k_chunk_rows already ran sampling round 0 (Stage 1);
+// ri: the final compress also writes Stage 2's root flags / list heads.
 template <int kPred, bool kRecord>
 static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop, PredData pd, Scalars* sc,
-                   int slot, cudaStream_t st) {
+                   int slot, cudaStream_t st, bool round0_done = false, RootInit ri = RootInit{}) {
   const int B = 256;
   const int kRounds = g_opt[OPT_SAMPLE_ROUNDS];
   const int gv = grid_for(g.n, B);
@@ -536,7 +563,9 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   // between only hook roots under roots and their proposers find() instead
   int cmask = g_opt[OPT_COMPRESS_MASK];
   if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
-  if (kRounds > 0) {
+  if (kRounds > 0 && round0_done) {
+    // (k_chunk_rows)
+  } else if (kRounds > 0) {
     const int sp = g_opt[OPT_SKEL_PARENT];
     launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd, (sp & 1) != 0);  // round 0
     note(K_HOOK_MIN);
@@ -557,7 +586,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       // the last sampling round's compress also picks the giant
       const bool last_round = r == kRounds - 1 && g_opt[OPT_GIANT_FOLD];
       launch(k_compress, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr, last_round ? sc : nullptr,
-             g_opt[OPT_GIANT_SKIP] != 0);
+             g_opt[OPT_GIANT_SKIP] != 0, RootInit{});
       note(K_COMPRESS);
     }
   }
@@ -577,7 +606,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
                                                                                      heavy, nheavy);
     note(K_LINK_HEAVY);
   }
-  launch(k_compress, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false);  // final root count (= components)
+  launch(k_compress, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri);  // final root count (= components)
   note(K_COMPRESS);
 }
 
@@ -636,14 +665,15 @@ void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2
   note(K_LINK_ROWS);
 }
 
-void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st) {
+void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st, RootInit ri) {
   const int B = 256;
-  launch(k_compress, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false);
+  launch(k_compress, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri);
   note(K_COMPRESS);
 }
 
-void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st) {
-  run_cc<PRED_NONE, true>(g, comp, fe, prop, PredData{}, sc, 0, st);
+void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st,
+                   bool round0_done, RootInit ri) {
+  run_cc<PRED_NONE, true>(g, comp, fe, prop, PredData{}, sc, 0, st, round0_done, ri);
 }
 
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,

@@ -16,7 +16,35 @@ struct Graph {
   const int* crow;       // [ceil(m/kItems)] chunk -> row table (build_chunk_rows)
 };
 
-void build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st);
+// (comp/fe/prop given: also Stage 1's sampling round 0; returns whether it ran)
+bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp = nullptr,
+                      int2* fe = nullptr, unsigned long long* prop = nullptr);
+
+// Stage 2 initial state written by Stage 1's final compress (one pass over
+// the vertices instead of a separate k_root_flags): flags[v] = v is a root
+// (flags[n] = 0, the scan's tail), lhead[v] = empty out-list (-1) or the hub
+// sub-list marker, hub sub-list heads cleared (see rooting.cu).
+struct RootInit {
+  int* flags = nullptr;
+  int* lhead = nullptr;
+  int* hsub = nullptr;
+  const int64_t* off = nullptr;  // hub split source (nullptr: none)
+  const Scalars* sc = nullptr;
+};
+
+__device__ __forceinline__ void root_init(const RootInit& ri, const int64_t* hoff, int v, bool root) {
+  ri.flags[v] = root ? 1 : 0;
+  int h = -1;
+  if (hoff) {
+    const int64_t rs = __ldg(hoff + v);
+    if (__ldg(hoff + v + 1) - rs >= kHubDeg) {
+      const int base = (int)(rs >> 4);
+      for (int j = 0; j < kHubWays; j++) ri.hsub[base + j] = -1;
+      h = -2 - base;
+    }
+  }
+  ri.lhead[v] = h;
+}
 
 // Device arrays for the rooting / tags stages (see api.cu for the layout).
 constexpr int kFinalMax = 16384;  // list-ranking level finished in one CTA
@@ -61,15 +89,20 @@ void rooting_roots(int n, const int* comp, Rooting& R, Scalars* sc, cudaStream_t
 void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc, cudaStream_t st);
 void masked_cc(const Graph& g, const uint8_t* mask, int* comp, int2* fe, unsigned long long* prop, Scalars* sc,
                cudaStream_t st);
-void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st);
+void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st,
+                   bool round0_done = false, RootInit ri = RootInit{});
 // Stage 1 over a streamed edge array (fbcc_run_host): identity init, one link
 // pass per arrived chunk range [q0, q1) of kItems-arc chunks, final compress
 void stage1_stream_begin(const Graph& g, int* comp, cudaStream_t st);
 void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2* fe, cudaStream_t st);
-void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st);
+void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st, RootInit ri = RootInit{});
 
 void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP,
                     Scalars* sc, cudaStream_t st);
+// the pipeline's Stage 2 after a RootInit compress: scan of the flags, then
+// out-lists (which also place the roots in id order) and the tour
+void stage2_rooting_fused(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc,
+                          cudaStream_t st);
 // nlow == nullptr: the reference's exact w2 (both forest directions
 // excluded, stand-alone op); otherwise the pipeline's relaxed gather (same
 // w1/low/high), which also counts each row's lower neighbours into nlow

@@ -144,8 +144,10 @@ struct EdgeBlockVisitor {
 __global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
                                                      int n, int64_t m, const int* __restrict__ label,
                                                      const int* __restrict__ head, const int* __restrict__ uoff,
-                                                     const int* __restrict__ nlow, int* eblk, int* bmin) {
+                                                     const int* __restrict__ nlow, int* eblk, int* bmin,
+                                                     Scalars* sc) {
   pdl_enter();
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->num_edges = uoff[n];  // (k_set_edges' job)
   EdgeBlockVisitor vis;
   vis.off = off;
   vis.label = label;
@@ -190,8 +192,9 @@ __global__ void __launch_bounds__(kEBThreads, 1)
     k_edge_blocks_ws(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
                      int n, int64_t m, const int* __restrict__ label, const int* __restrict__ head,
                      const int* __restrict__ uoff, const int* __restrict__ nlow, const uint32_t* __restrict__ gbits,
-                     const Scalars* sc, int* __restrict__ eblk, int* bmin) {
+                     Scalars* sc, int* __restrict__ eblk, int* bmin) {
   pdl_enter();
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->num_edges = uoff[n];  // (k_set_edges' job)
   extern __shared__ int4 ebsm[];
   constexpr int kThreads = kEBThreads;
   int4* rows = ebsm + (threadIdx.x >> 5) * kEBRows;
@@ -318,18 +321,19 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   // by the Stage-3 gather) -> uoff (uoff[n] = E)
   scan_upper_degrees(g.off, nlow, n, uoff, cub_tmp, cub_bytes, st);
   note(K_SCAN);
-  launch(k_set_edges, 1, 1, 0, st, uoff, n, sc);
-  note(K_SET_EDGES);
-  if (edge_label && g.m > 0) {
+  if (!edge_label || g.m == 0) {
+    launch(k_set_edges, 1, 1, 0, st, uoff, n, sc);
+    note(K_SET_EDGES);
+  } else {
     int64_t nchunks = (g.m + kItems - 1) / kItems;
     const size_t smem = eb_rows_bytes(kEBThreads) + 16 * (size_t)(((n + 31) / 32 + 3) / 4);
     if (g_opt[OPT_EB_STAGED] && smem <= (size_t)kEBMaxSmemBytes) {
       cudaFuncSetAttribute(k_edge_blocks_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       launch(k_edge_blocks_ws, grid_for(nchunks, kEBThreads, 1), kEBThreads, smem, st, g.off, g.adj, g.crow, n, g.m,
-             label, head, uoff, nlow, (const uint32_t*)gbits, (const Scalars*)sc, edge_label, bmin);
+             label, head, uoff, nlow, (const uint32_t*)gbits, sc, edge_label, bmin);
     } else {
       launch(k_edge_blocks, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow,
-             edge_label, bmin);
+             edge_label, bmin, sc);
     }
     note(K_EDGE_BLOCKS);
     launch(k_edge_final, grid_for(g.m / 2, B), B, 0, st, edge_label, bmin, uoff, n);

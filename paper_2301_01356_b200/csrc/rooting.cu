@@ -135,12 +135,19 @@ __device__ __forceinline__ int* list_head(int* lhead, int* hsub, int t, int x, b
   return lhead + t;
 }
 
+// (rootidx != nullptr: also k_root_list's work -- roots placed in id order,
+// c published -- in the same pass over the vertices)
 __global__ void k_out_lists(const int* __restrict__ comp, const int2* __restrict__ fe, int n, int* lhead,
-                            int* __restrict__ nexto, int* hsub, const Scalars* sc) {
+                            int* __restrict__ nexto, int* hsub, Scalars* sc, const int* __restrict__ rootidx,
+                            int* __restrict__ rlist) {
   pdl_enter();
   const bool split = hsub != nullptr && sc->has_hubs;
+  if (rootidx && blockIdx.x == 0 && threadIdx.x == 0) sc->ncomp = rootidx[n];
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-    if (__ldg(comp + x) == x) continue;
+    if (__ldg(comp + x) == x) {
+      if (rootidx) rlist[__ldg(rootidx + x)] = x;
+      continue;
+    }
     int2 e = __ldg(fe + x);
     nexto[2 * x] = atomicExch(list_head(lhead, hsub, e.x, x, split), 2 * x);
     nexto[2 * x + 1] = atomicExch(list_head(lhead, hsub, e.y, x, split), 2 * x + 1);
@@ -380,7 +387,19 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
   rooting_roots(g.n, comp, R, sc, st);
   // Euler circuit: out-arc lists in atomicExch order (any order is a valid
   // tour; the final outputs do not depend on it)
-  launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto, R.hoff ? R.hsub : nullptr, sc);
+  launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto, R.hoff ? R.hsub : nullptr, sc,
+         (const int*)nullptr, (int*)nullptr);
+  note(K_OUT_LISTS);
+  rooting_tour(g.n, comp, fe, R, AP, sc, st);
+}
+
+void stage2_rooting_fused(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc,
+                          cudaStream_t st) {
+  // R.flags / R.lhead / R.hsub were written by Stage 1's final compress
+  exclusive_scan(R.flags, R.rootidx, g.n + 1, R.cub_tmp, R.cub_bytes, st);
+  note(K_SCAN);
+  launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto, R.hoff ? R.hsub : nullptr, sc,
+         (const int*)R.rootidx, R.rlist);
   note(K_OUT_LISTS);
   rooting_tour(g.n, comp, fe, R, AP, sc, st);
 }
