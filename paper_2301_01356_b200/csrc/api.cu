@@ -31,7 +31,8 @@ int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*retired*/ 0, /*S0
                       /*programmatic dependent launch (dependents launch as the previous grid exits)*/ 1,
                       /*fbcc_run_host edge-copy chunks*/ 8, /*skeleton parent-edge rounds (hook_min + round 1)*/ 3,
                       /*giant pick folded into the last compress*/ 1,
-                      /*warp-staged edge-block pass with the giant bitmap*/ 1};
+                      /*warp-staged edge-block pass with the giant bitmap*/ 1,
+                      /*adaptive sampling rounds up to*/ 3, 0, 0, 0};
 constexpr int kFinalMaxHost = kFinalMax;
 constexpr int kMaxStreamChunks = 64;
 

@@ -78,8 +78,9 @@ enum Option : int {
   OPT_SKEL_PARENT = 13,   // Stage 5 sampling: bit r = round r samples the plain parent edge
   OPT_GIANT_FOLD = 14,    // the last sampling compress also picks the giant (no k_find_giant)
   OPT_EB_STAGED = 15,     // Stage 6 edge blocks: warp-staged rows + giant bitmap (0: plain arc visitor)
+  OPT_MAX_ROUNDS = 16,    // adaptive sampling rounds beyond OPT_SAMPLE_ROUNDS, up to this many (see skip_round)
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
-  OPT_NUM = 16
+  OPT_NUM = 20
 };
 extern int g_opt[OPT_NUM];
 

@@ -30,6 +30,8 @@
 //   5. final compress -> comp[v] = min id of v's component
 // In Stage 1 each successful hook records the arc that merged the two sets
 // at fe[hooked root]: exactly n - c records, an acyclic spanning forest.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -239,11 +241,24 @@ __global__ void k_iota(int* __restrict__ comp, int n, unsigned long long* __rest
 // ---------------------------------------------------------------------------
 constexpr int kPerRoot = 32;
 
+// Rounds at or past rbase are adaptive: they run only while the previous
+// round still hooked >= 5% as many roots as the one before it and >= n/8192
+// (high-diameter graphs -- config 3: 114k, 28k, 3.4k, 0.6k hooks in rounds
+// 1-4 -- keep merging, which leaves k_link_rows far fewer components; a
+// low-diameter graph's round 2 hooks < 1% of round 1's and the extra rounds
+// exit at once).
+__device__ __forceinline__ bool skip_round(const int* hooks, int round, int rbase, int n) {
+  if (round < rbase || round < 2) return false;
+  const int h1 = hooks[round - 1], h2 = hooks[round - 2];
+  return (int64_t)h1 * 20 < (int64_t)h2 || (int64_t)h1 * 8192 < (int64_t)n;
+}
+
 template <int kPred>
 __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round,
                           int* comp, unsigned long long* prop, PredData pd, const int* __restrict__ nroots,
-                          const int* __restrict__ hooks, bool flat, bool skel_parent) {
+                          const int* __restrict__ hooks, bool flat, bool skel_parent, int rbase) {
   pdl_enter();
+  if (skip_round(hooks, round, rbase, n)) return;
   // participate iff hash < thr / 2^24, thr = min(1, kPerRoot * roots / n);
   // roots at round start = roots counted after round 0 minus later hooks
   uint32_t thr = 1u << 24;
@@ -285,8 +300,9 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
 
 template <bool kRecord>
 __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
-                         unsigned long long* prop, int2* fe, int* hooks) {
+                         unsigned long long* prop, int2* fe, int* hooks, int rbase) {
   pdl_enter();
+  if (skip_round(hooks, round, rbase, n)) return;
   int hooked = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     unsigned long long key = prop[v];
@@ -550,7 +566,9 @@ template <int kPred, bool kRecord>
 static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop, PredData pd, Scalars* sc,
                    int slot, cudaStream_t st, bool round0_done = false, RootInit ri = RootInit{}) {
   const int B = 256;
-  const int kRounds = g_opt[OPT_SAMPLE_ROUNDS];
+  const int kBase = g_opt[OPT_SAMPLE_ROUNDS];
+  // adaptive rounds kBase .. kRounds-1 (skip_round)
+  const int kRounds = g_opt[OPT_MAX_ROUNDS] > kBase ? std::min(g_opt[OPT_MAX_ROUNDS], 8) : kBase;
   const int gv = grid_for(g.n, B);
   // k_compress relies on concurrent threads advancing each other's pointers:
   // its grid must be fully resident (2048 threads/SM), or grid-stride
@@ -577,9 +595,9 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
     if (r > 0) {
       launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat,
-             ((g_opt[OPT_SKEL_PARENT] >> r) & 1) != 0);
+             ((g_opt[OPT_SKEL_PARENT] >> r) & 1) != 0, kBase);
       note(K_PROPOSE);
-      launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks);
+      launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase);
       note(K_ACCEPT);
     }
     if ((cmask >> r) & 1) {
