@@ -16,7 +16,7 @@ ROOT = Path(__file__).resolve().parent.parent
 def kind_of(name):
     if "DeviceScan" in name:
         return "scan"
-    m = re.search(r"fbcc::k_(\w+)(<[^>]*>)?", name)
+    m = re.search(r"(?:fbcc::|\b)k_(\w+)(<[^>]*>)?", name)
     if not m:
         return None
     k, targs = m.group(1), m.group(2) or ""
@@ -24,6 +24,8 @@ def kind_of(name):
         return "walk0" if ("false" in targs or "0>" in targs) else "walk_level"
     if k.startswith("table"):
         return "table"
+    if k == "edge_blocks_ws":
+        return "edge_blocks"
     return k
 
 
