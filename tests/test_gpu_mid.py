@@ -88,3 +88,33 @@ def test_mid_graph_rungs(name, oracle_mod):
     assert r["num_components"] == ref["num_components"] == ncomp
     assert np.array_equal(r["is_ap"], ref["is_ap"]), "rung 6: is_ap"
     assert np.array_equal(r["edge_label"], ref["edge_label"]), "rung 6: edge labels"
+
+
+# Alternative kernel paths and tunables: every one must give the reference's
+# outputs (the edge-block pass without the bitmap is what graphs with
+# n > 1.6M run; max_rounds runs the adaptive sampling rounds and their skips)
+OPTION_VARIANTS = [{"eb_staged": 0}, {"max_rounds": 6}, {"max_rounds": 8, "sample_rounds": 2}, {"pdl": 0},
+                   {"sample_rounds": 1}, {"giant_skip": 0}, {"s0": 8, "sl": 4}]
+
+
+@pytest.mark.parametrize("name", ["rmat_s16", "isolated_mix", "star_mid_20k", "uniform_64k_d3", "chain_300k",
+                                  "torus_200_p07"])
+def test_mid_graph_option_paths(name, oracle_mod):
+    from paper_2301_01356_b200 import _lib
+
+    g = GRAPHS[name]()
+    ref = oracle_mod.fast_bcc(g.offsets, g.edges)
+    defaults = {k: _lib.get_option(k) for k in _lib.OPTIONS}
+    try:
+        for var in OPTION_VARIANTS:
+            for k, v in var.items():
+                _lib.set_option(k, v)
+            r = _run(g, debug=False)
+            for k in ("label", "head", "is_ap", "edge_label"):
+                assert np.array_equal(r[k], ref[k]), (name, var, k)
+            assert r["num_bccs"] == ref["num_bccs"] and r["num_components"] == ref["num_components"], (name, var)
+            for k in var:
+                _lib.set_option(k, defaults[k])
+    finally:
+        for k, v in defaults.items():
+            _lib.set_option(k, v)
