@@ -137,6 +137,38 @@ __device__ __forceinline__ int link(int u, int w, int* comp, int2* fe) {
 // chunk -> row table (see visit_arc_chunks): row v owns the chunks whose
 // first arc lies in it
 // ---------------------------------------------------------------------------
+// Sampling round 0's hook target for v (rows sorted, every vertex its own
+// root): a smaller neighbour, so comp[v] = w < v keeps parents below children.
+// Prefer the LARGEST smaller neighbour when it lies within kNear ids and the
+// row is short enough to scan in its first sector (deg <= 8); otherwise the
+// minimum neighbour (the minimum proposal v would receive, Borůvka-style).
+// On meshes with id locality (tori, grids: configs 1, 4a, 4b) the near rule
+// hooks each vertex to its left neighbour, so the spanning forest -- and the
+// Euler tour built from it -- follows the id order: the tour positions of
+// consecutive vertices are consecutive, and Stage 2/3's position-indexed
+// scatters (k_positions, the w gather's AP stores, the tile pass's partials)
+// become coalesced instead of random.  Random-id graphs (configs 2, 3, 5)
+// almost never have a smaller neighbour within kNear ids and keep the minimum.
+#ifndef FBCC_NEAR
+#define FBCC_NEAR 64
+#endif
+constexpr int kNear = FBCC_NEAR;
+
+__device__ __forceinline__ int round0_target(const uint32_t* __restrict__ adj, int v, int64_t rs, int64_t re) {
+  const int w0 = (int)__ldg(adj + rs);
+  if (w0 >= v) return v;  // no smaller neighbour
+  if (re - rs <= kItems) {
+    int best = w0;
+    for (int64_t a = rs + 1; a < re; a++) {
+      const int w = (int)__ldg(adj + a);
+      if (w >= v) break;
+      best = w;
+    }
+    if (v - best <= kNear) return best;
+  }
+  return w0;
+}
+
 // Every chunk q (first arc 8q) belongs to exactly one non-empty row, which
 // writes it -- no memset.  Rows of up to kRowChunks chunks are written by
 // their own lane; longer (hub) rows by the whole warp, so a 600k-arc RMAT hub
@@ -144,7 +176,7 @@ __device__ __forceinline__ int link(int u, int w, int* comp, int2* fe) {
 // binary-search hub chunks over all n rows: half of RMAT's gather passes).
 //
 // The pipeline's Stage 1 also folds its sampling round 0 (k_hook_min<NONE>:
-// comp[v] = min(v, first neighbour), the forest edge, the proposal reset)
+// comp[v] = round0_target, the forest edge, the proposal reset)
 // into this pass over the offsets (comp != nullptr).
 __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow, Scalars* sc,
                              const uint32_t* __restrict__ adj, int* __restrict__ comp, int2* __restrict__ fe,
@@ -162,11 +194,8 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
       if (comp) {  // sampling round 0 (see k_hook_min)
         int c = v;
         if (rs < re) {
-          const int w = (int)__ldg(adj + rs);
-          if (w < v) {
-            c = w;
-            fe[v] = make_int2(v, w);
-          }
+          c = round0_target(adj, v, rs, re);
+          if (c < v) fe[v] = make_int2(v, c);
         }
         comp[v] = c;
         prop[v] = ~0ull;
@@ -196,12 +225,12 @@ bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, i
   return fold;
 }
 
-// Sampling round 0 without atomics.  With every vertex its own root, the
-// minimum proposal a vertex v receives is its own smallest neighbour w0
-// (any u < v proposing to v is a neighbour of v, hence u >= w0), so round 0
-// is exactly comp[v] = min(v, w0) and the forest edge (v, w0).  Under a
-// predicate only v's own arc 0 is used (best effort: k_link_rows re-covers).
-// Also resets the proposal words for the later rounds.
+// Sampling round 0 without atomics.  With every vertex its own root, v can
+// hook under any smaller neighbour (round0_target: the minimum one -- the
+// minimum proposal v would receive -- or a near one on meshes) with the
+// forest edge (v, w).  Under a predicate only v's own arc 0 is used (best
+// effort: k_link_rows re-covers).  Also resets the proposal words for the
+// later rounds.
 template <int kPred, bool kRecord>
 __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int* comp,
                            int2* fe, unsigned long long* __restrict__ prop, PredData pd, bool skel_parent) {
@@ -209,8 +238,9 @@ __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __re
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t s = __ldg(off + v);
     int c = v;
-    if (s < __ldg(off + v + 1)) {
-      int w = (int)__ldg(adj + s);
+    const int64_t e = __ldg(off + v + 1);
+    if (s < e) {
+      int w = kPred == PRED_NONE ? round0_target(adj, v, s, e) : (int)__ldg(adj + s);
       int4 rv;
       if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
       if (w < v && keep<kPred>(pd, v, rv, w, s)) {
