@@ -372,16 +372,45 @@ __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable)
 
 // giant_sc != nullptr: the last block to finish also picks the sampled giant
 // root (Afforest skip) -- one launch instead of a separate 1-block kernel.
+template <bool kJump>
 __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable, RootInit ri) {
   pdl_enter();
   int roots = 0;
   const int64_t* hoff = (ri.flags && ri.off && ri.sc->has_hubs) ? ri.off : nullptr;
   if (ri.flags && blockIdx.x == 0 && threadIdx.x == 0) ri.flags[n] = 0;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    int c = __ldcg(comp + v);
-    roots += (c == v);
-    if (ri.flags) root_init(ri, hoff, v, c == v);
-    if (c == v) continue;
+  __shared__ int sp[kJump ? 1024 : 1];
+  // block-uniform trip count (kJump): each step the block owns blockDim.x
+  // consecutive vertices and may first shorten their chains in shared memory
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)base + threadIdx.x;
+    int c = v < n ? __ldcg(comp + v) : v;
+    const bool root = c == v;
+    if (kJump) {
+      // Pointer jumping inside the block's id range (after sampling round 0
+      // only): chains of consecutive ids -- round 0's left-neighbour hooks on
+      // meshes, a path's v -> v-1 -- then leave the block in one step instead
+      // of up to blockDim global climbs (config 4a: 10^4-vertex row chains,
+      // S1 5.6 -> 3.9 ms).  A block with no in-range pointer pays one
+      // barrier.  Every value is an ancestor, so the climb below stays exact.
+      sp[threadIdx.x] = c;
+      int rel = c - (int)base;
+      if (__syncthreads_or(!root && rel >= 0 && rel < (int)blockDim.x)) {
+        for (int r = 0; r < 10; r++) {
+          const int nc = (rel >= 0 && rel < (int)blockDim.x) ? sp[rel] : c;
+          const bool moved = nc != c;
+          __syncthreads();
+          sp[threadIdx.x] = nc;
+          c = nc;
+          rel = c - (int)base;
+          if (!__syncthreads_or(moved)) break;
+        }
+      }
+      __syncthreads();  // sp is rewritten next step
+    }
+    if (v >= n) continue;
+    roots += root;
+    if (ri.flags) root_init(ri, hoff, v, root);
+    if (root) continue;
     bool done = false;
     for (int i = 0; i < kL1Steps; i++) {
       int x = __ldca(comp + c);
@@ -633,8 +662,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     if ((cmask >> r) & 1) {
       // the last sampling round's compress also picks the giant
       const bool last_round = r == kRounds - 1 && g_opt[OPT_GIANT_FOLD];
-      launch(k_compress, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr, last_round ? sc : nullptr,
-             g_opt[OPT_GIANT_SKIP] != 0, RootInit{});
+      launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
+             last_round ? sc : nullptr, g_opt[OPT_GIANT_SKIP] != 0, RootInit{});
       note(K_COMPRESS);
     }
   }
@@ -654,7 +683,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
                                                                                      heavy, nheavy);
     note(K_LINK_HEAVY);
   }
-  launch(k_compress, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri);  // final root count (= components)
+  launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri);  // final root count (= components)
   note(K_COMPRESS);
 }
 
@@ -715,7 +744,7 @@ void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2
 
 void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st, RootInit ri) {
   const int B = 256;
-  launch(k_compress, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri);
+  launch(k_compress<true>, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri);
   note(K_COMPRESS);
 }
 
