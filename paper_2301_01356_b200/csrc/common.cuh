@@ -25,7 +25,8 @@ struct Scalars {
   int nheavy[2];   // super-heavy rows deferred by k_link_rows (stage 1 / stage 5 slot)
   int has_hubs;    // some row has >= kHubDeg slots (set by k_chunk_rows)
   unsigned ticket; // last-block detection (k_compress; reset by the last block)
-  int pad[23];
+  int giant_cnt;   // samples (of 1024) that fell in the giant at its pick
+  int pad[22];
 };
 
 // ---------------------------------------------------------------------------

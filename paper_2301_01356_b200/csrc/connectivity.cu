@@ -489,7 +489,10 @@ __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable)
       int ov = __shfl_down_sync(0xffffffffu, mine, o);
       if (oc > cnt || (oc == cnt && ov < mine)) { cnt = oc; mine = ov; }
     }
-    if (t == 0) sc->giant = enable ? mine : -1;
+    if (t == 0) {
+      sc->giant = enable ? mine : -1;
+      sc->giant_cnt = enable ? cnt : 0;
+    }
   }
 }
 
