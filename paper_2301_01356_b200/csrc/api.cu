@@ -159,6 +159,8 @@ struct Pipeline {
       R.offs[l] = (int*)at(lay.loffs[l]);
     }
     R.rec = (int4*)at(lay.rec);
+    R.firsts = (int*)at(lay.lh1);  // Stage 3's compact first[] (see stage3_tags)
+    R.nlow = (int*)at(lay.nlow);
     R.cub_tmp = at(lay.cub);
     R.cub_bytes = lay.cub_bytes;
     T.AP = (int4*)at(lay.AP);

@@ -69,6 +69,8 @@ struct Rooting {
   int2* own[8];
   int* offs[8];
   int4* rec;       // [n] {first, last, parent, fence}
+  int* firsts = nullptr;  // pipeline: k_positions also writes Stage 3's compact first[] ...
+  int* nlow = nullptr;    // ... and zeroes the lower-degree counters (no k_firsts pass)
   void* cub_tmp;
   size_t cub_bytes;
 };

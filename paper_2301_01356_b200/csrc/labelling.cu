@@ -341,11 +341,29 @@ __global__ void __launch_bounds__(kEBThreads, 1)
   if (run_blk >= 0) atomicMin(bmin + run_blk, run_min);
 }
 
+// block -> minimum edge id of the block, 4 edges per thread (16-byte
+// streaming loads and stores; the bmin gathers of the giant block hit one
+// L1-resident word)
 __global__ void k_edge_final(int* eblk, const int* __restrict__ bmin, const int* __restrict__ uoff, int n) {
   pdl_enter();
   const int E = uoff[n];
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x)
-    eblk[e] = __ldg(bmin + eblk[e]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(eblk) & 15) == 0) {
+    const int64_t nv = E / 4;
+    int4* e4 = reinterpret_cast<int4*>(eblk);
+    for (int64_t i = tid; i < nv; i += stride) {
+      int4 b = __ldcs(e4 + i);
+      b.x = __ldg(bmin + b.x);
+      b.y = __ldg(bmin + b.y);
+      b.z = __ldg(bmin + b.z);
+      b.w = __ldg(bmin + b.w);
+      __stcs(e4 + i, b);
+    }
+    for (int64_t e = 4 * nv + tid; e < E; e += stride) eblk[e] = __ldg(bmin + eblk[e]);
+  } else {
+    for (int64_t e = tid; e < E; e += stride) eblk[e] = __ldg(bmin + eblk[e]);
+  }
 }
 
 __global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) {

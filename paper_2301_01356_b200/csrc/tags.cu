@@ -342,8 +342,10 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
   } else {
     // compact first[] lives in lh1 until k_tile overwrites it
     int* firsts = reinterpret_cast<int*>(T.lh1);
-    launch(k_firsts, grid_for(g.n, B), B, 0, st, R.rec, g.n, firsts, nlow);
-    note(K_FIRSTS);
+    if (R.firsts != firsts || R.nlow != nlow) {  // (else k_positions wrote both)
+      launch(k_firsts, grid_for(g.n, B), B, 0, st, R.rec, g.n, firsts, nlow);
+      note(K_FIRSTS);
+    }
     if (g.m > 0)
       launch(k_w_gather<false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts,
              T.AP, nlow);
