@@ -264,7 +264,10 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
 // chunks, the whole warp for longer (hub) rows.  One pass of n threads
 // replaces a binary search per chunk in each arc-balanced kernel of a run
 // (consumers keep a row_of fallback for a negative entry).
-constexpr int kRowChunks = 64;
+#ifndef FBCC_ROW_CHUNKS
+#define FBCC_ROW_CHUNKS 64
+#endif
+constexpr int kRowChunks = FBCC_ROW_CHUNKS;
 
 // rows of at least kHubDeg slots get kHubWays out-list heads in rooting
 // (see k_root_flags)
