@@ -25,14 +25,14 @@ static int cuda_fail(cudaError_t e, const char* where) {
   return FBCC_ERR_CUDA;
 }
 
-int g_opt[OPT_NUM] = {/*sample rounds*/ 3, /*giant skip*/ 1, /*retired*/ 0, /*S0*/ 16, /*SL*/ 8,
+int g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*giant skip*/ 1, /*retired*/ 0, /*S0*/ 16, /*SL*/ 8,
                       /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last*/ 0,
                       /*retired*/ 0, /*retired*/ 0,
                       /*programmatic dependent launch (dependents launch as the previous grid exits)*/ 1,
                       /*fbcc_run_host edge-copy chunks*/ 8, /*skeleton parent-edge rounds (hook_min + round 1)*/ 3,
                       /*giant pick folded into the last compress*/ 1,
                       /*warp-staged edge-block pass with the giant bitmap*/ 1,
-                      /*adaptive sampling rounds up to*/ 3, 0, 0, 0};
+                      /*... plus adaptive rounds up to (skip_round)*/ 3, 0, 0, 0};
 constexpr int kFinalMaxHost = kFinalMax;
 constexpr int kMaxStreamChunks = 64;
 

@@ -11,7 +11,8 @@
 // B200 design: union-find with the root of every set equal to its minimum
 // id, so final labels are canonical (== reference labels) with no min pass.
 // Parents live in one int32 array (4 MB per 1M vertices).
-//   1. k sampling rounds (default 3) over arc r of every row, each a
+//   1. sampling rounds over arc r of every row (default: rounds 0 and 1, and
+//      round 2 unless round 1 hooked < n/8192 roots), each a
 //      PROPOSE/ACCEPT step: every vertex fires one fire-and-forget 64-bit
 //      atomicMin((lower root << 32) | proposer) at the higher of the two
 //      component roots; k_accept hooks each proposed-to root under its
@@ -277,10 +278,16 @@ constexpr int kPerRoot = 32;
 // 1-4 -- keep merging, which leaves k_link_rows far fewer components; a
 // low-diameter graph's round 2 hooks < 1% of round 1's and the extra rounds
 // exit at once).
+// (round 2 has only the absolute test: on the tori and the chain round 0
+// already hooks all but a handful of vertices, round 1 hooks < n/8192 and
+// round 2 is skipped -- 4a -0.47 ms; config 2's round 1 hooks 65k, RMAT's
+// 466k.  A ratio against round 0's roots would count RMAT's 16.5 M isolated
+// vertices and starve its giant.)
 __device__ __forceinline__ bool skip_round(const int* hooks, int round, int rbase, int n) {
   if (round < rbase || round < 2) return false;
-  const int h1 = hooks[round - 1], h2 = hooks[round - 2];
-  return (int64_t)h1 * 20 < (int64_t)h2 || (int64_t)h1 * 8192 < (int64_t)n;
+  const int h1 = hooks[round - 1];
+  if ((int64_t)h1 * 8192 < (int64_t)n) return true;
+  return round > 2 && (int64_t)h1 * 20 < (int64_t)hooks[round - 2];
 }
 
 template <int kPred>
@@ -330,7 +337,7 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
 
 template <bool kRecord>
 __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
-                         unsigned long long* prop, int2* fe, int* hooks, int rbase) {
+                         unsigned long long* prop, int2* fe, int* hooks, const int* nroots, int rbase) {
   pdl_enter();
   if (skip_round(hooks, round, rbase, n)) return;
   int hooked = 0;
@@ -659,7 +666,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat,
              ((g_opt[OPT_SKEL_PARENT] >> r) & 1) != 0, kBase);
       note(K_PROPOSE);
-      launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase);
+      launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, (const int*)nroots, kBase);
       note(K_ACCEPT);
     }
     if ((cmask >> r) & 1) {
