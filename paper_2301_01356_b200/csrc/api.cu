@@ -26,7 +26,7 @@ static int cuda_fail(cudaError_t e, const char* where) {
 }
 
 int g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*giant skip*/ 1, /*retired*/ 0, /*S0*/ 16, /*SL*/ 8,
-                      /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last*/ 0,
+                      /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last; all rounds: 4b -13%, config 3 -2%*/ 0xFF,
                       /*retired*/ 0, /*retired*/ 0,
                       /*programmatic dependent launch (dependents launch as the previous grid exits)*/ 1,
                       /*fbcc_run_host edge-copy chunks*/ 8, /*skeleton parent-edge rounds (hook_min + round 1)*/ 3,

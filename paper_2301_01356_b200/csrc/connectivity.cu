@@ -379,16 +379,21 @@ __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable)
 
 // giant_sc != nullptr: the last block to finish also picks the sampled giant
 // root (Afforest skip) -- one launch instead of a separate 1-block kernel.
+// (hooks != nullptr: the compress after adaptive sampling round `round`; it
+// does no pointer work when that round was skipped -- comp is still flat
+// from the previous round's compress -- but still picks the giant)
 template <bool kJump>
-__global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable, RootInit ri) {
+__global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable, RootInit ri,
+                           const int* hooks, int round, int rbase) {
   pdl_enter();
   int roots = 0;
+  const int n_work = (hooks && skip_round(hooks, round, rbase, n)) ? 0 : n;
   const int64_t* hoff = (ri.flags && ri.off && ri.sc->has_hubs) ? ri.off : nullptr;
   if (ri.flags && blockIdx.x == 0 && threadIdx.x == 0) ri.flags[n] = 0;
   __shared__ int sp[kJump ? 1024 : 1];
   // block-uniform trip count (kJump): each step the block owns blockDim.x
   // consecutive vertices and may first shorten their chains in shared memory
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_work; base += (int64_t)gridDim.x * blockDim.x) {
     const int v = (int)base + threadIdx.x;
     int c = v < n ? __ldcg(comp + v) : v;
     const bool root = c == v;
@@ -673,7 +678,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       // the last sampling round's compress also picks the giant
       const bool last_round = r == kRounds - 1 && g_opt[OPT_GIANT_FOLD];
       launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
-             last_round ? sc : nullptr, g_opt[OPT_GIANT_SKIP] != 0, RootInit{});
+             last_round ? sc : nullptr, g_opt[OPT_GIANT_SKIP] != 0, RootInit{}, r >= kBase ? (const int*)hooks : nullptr,
+             r, kBase);
       note(K_COMPRESS);
     }
   }
@@ -693,7 +699,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
                                                                                      heavy, nheavy);
     note(K_LINK_HEAVY);
   }
-  launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri);  // final root count (= components)
+  launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0,
+         0);  // final root count (= components)
   note(K_COMPRESS);
 }
 
@@ -754,7 +761,8 @@ void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2
 
 void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st, RootInit ri) {
   const int B = 256;
-  launch(k_compress<true>, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri);
+  launch(k_compress<true>, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
+         (const int*)nullptr, 0, 0);
   note(K_COMPRESS);
 }
 

@@ -47,7 +47,10 @@ __device__ __forceinline__ void root_init(const RootInit& ri, const int64_t* hof
 }
 
 // Device arrays for the rooting / tags stages (see api.cu for the layout).
-constexpr int kFinalMax = 16384;  // list-ranking level finished in one CTA
+#ifndef FBCC_FINAL_MAX
+#define FBCC_FINAL_MAX 16384
+#endif
+constexpr int kFinalMax = FBCC_FINAL_MAX;  // list-ranking level finished in one CTA
 
 struct Rooting {
   int* flags;      // [n+1] comp[v] == v
