@@ -337,7 +337,7 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
 
 template <bool kRecord>
 __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
-                         unsigned long long* prop, int2* fe, int* hooks, const int* nroots, int rbase) {
+                         unsigned long long* prop, int2* fe, int* hooks, int rbase) {
   pdl_enter();
   if (skip_round(hooks, round, rbase, n)) return;
   int hooked = 0;
@@ -671,7 +671,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat,
              ((g_opt[OPT_SKEL_PARENT] >> r) & 1) != 0, kBase);
       note(K_PROPOSE);
-      launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, (const int*)nroots, kBase);
+      launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase);
       note(K_ACCEPT);
     }
     if ((cmask >> r) & 1) {
