@@ -182,7 +182,7 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    const bool round0 = build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, comp, fe, prop);
+    const bool round0 = build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, comp, fe, prop, nlow);
     stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args());
     mk(1);
     enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
@@ -260,7 +260,7 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    build_chunk_rows(g, const_cast<int*>(g.crow), sc, st);
+    build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, nullptr, nullptr, nullptr, nlow);
     stage1_stream_begin(g, comp, st);
     for (int c = 0; c < nchunk; c++) {
       cudaStreamWaitEvent(st, ev_chunk[c], 0);

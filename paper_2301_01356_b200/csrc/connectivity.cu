@@ -181,7 +181,7 @@ __device__ __forceinline__ int round0_target(const uint32_t* __restrict__ adj, i
 // into this pass over the offsets (comp != nullptr).
 __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow, Scalars* sc,
                              const uint32_t* __restrict__ adj, int* __restrict__ comp, int2* __restrict__ fe,
-                             unsigned long long* __restrict__ prop) {
+                             unsigned long long* __restrict__ prop, int* __restrict__ nlow) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -190,6 +190,7 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
     int q0 = 0, q1 = 0;
     if (v < n) {
       const int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+      if (nlow) nlow[v] = 0;  // Stage 3 accumulates rows split across warps into it
       q0 = (int)((rs + kItems - 1) / kItems);
       q1 = (int)((re + kItems - 1) / kItems);
       if (comp) {  // sampling round 0 (see k_hook_min)
@@ -218,10 +219,14 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
 }
 
 bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp, int2* fe,
-                      unsigned long long* prop) {
-  if (g.m == 0) return false;
+                      unsigned long long* prop, int* nlow) {
+  if (g.m == 0) {
+    if (nlow) cudaMemsetAsync(nlow, 0, sizeof(int) * g.n, st);
+    return false;
+  }
   const bool fold = comp != nullptr && g_opt[OPT_SAMPLE_ROUNDS] > 0;
-  launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow, sc, g.adj, fold ? comp : nullptr, fe, prop);
+  launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow, sc, g.adj, fold ? comp : nullptr, fe, prop,
+         nlow);
   note(K_CHUNK_ROWS);
   return fold;
 }

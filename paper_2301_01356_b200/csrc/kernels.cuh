@@ -17,8 +17,9 @@ struct Graph {
 };
 
 // (comp/fe/prop given: also Stage 1's sampling round 0; returns whether it ran)
+// (nlow given: also zeroes Stage 3's lower-degree counters, coalesced)
 bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp = nullptr,
-                      int2* fe = nullptr, unsigned long long* prop = nullptr);
+                      int2* fe = nullptr, unsigned long long* prop = nullptr, int* nlow = nullptr);
 
 // Stage 2 initial state written by Stage 1's final compress (one pass over
 // the vertices instead of a separate k_root_flags): flags[v] = v is a root
@@ -73,7 +74,7 @@ struct Rooting {
   int* offs[8];
   int4* rec;       // [n] {first, last, parent, fence}
   int* firsts = nullptr;  // pipeline: k_positions also writes Stage 3's compact first[] ...
-  int* nlow = nullptr;    // ... and zeroes the lower-degree counters (no k_firsts pass)
+  int* nlow = nullptr;    // ... and k_chunk_rows zeroed these counters (no k_firsts pass)
   void* cub_tmp;
   size_t cub_bytes;
 };

@@ -337,12 +337,9 @@ __global__ void k_expand(int64_t K, const int2* __restrict__ own, const int* __r
 // ---------------------------------------------------------------------------
 // AP[first] = {first, first (w1 = w2 = own entry, gathered into by stage 3), v, last};
 // AP[last] = {filler (tagging.py:33-39), ~v, first}: two 16 B stores per vertex
-__device__ __forceinline__ void place(int v, int f, int l, int par, int4* rec, int4* AP, int* firsts, int* nlow) {
+__device__ __forceinline__ void place(int v, int f, int l, int par, int4* rec, int4* AP, int* firsts) {
   rec[v] = make_int4(f, l, par, 0);
-  if (firsts) {  // the pipeline: Stage 3's compact first[] and zeroed lower-degree counters
-    firsts[v] = f;
-    nlow[v] = 0;
-  }
+  if (firsts) firsts[v] = f;  // the pipeline: Stage 3's compact first[]
   AP[f] = make_int4(f, f, v, l);
   AP[l] = make_int4(kINF, -1, ~v, f);
 }
@@ -360,16 +357,16 @@ __global__ void k_rank0(int64_t N, const int2* __restrict__ own0, const int* __r
 
 __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict__ fe,
                             const int2* __restrict__ rank0, int n, int4* __restrict__ rec,
-                            int4* __restrict__ AP, int* __restrict__ firsts, int* __restrict__ nlow) {
+                            int4* __restrict__ AP, int* __restrict__ firsts) {
   pdl_enter();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     int2 r = __ldg(rank0 + x);  // ranks of elements 2x and 2x+1, one 8-byte load
     if (__ldg(comp + x) == x) {
-      place(x, r.x, r.y, -1, rec, AP, firsts, nlow);  // enter(x), exit(x)
+      place(x, r.x, r.y, -1, rec, AP, firsts);  // enter(x), exit(x)
     } else {
       int2 uv = __ldg(fe + x);
-      if (r.x < r.y) place(uv.y, r.x, r.y, uv.x, rec, AP, firsts, nlow);  // u -> v is the down arc
-      else place(uv.x, r.y, r.x, uv.y, rec, AP, firsts, nlow);
+      if (r.x < r.y) place(uv.y, r.x, r.y, uv.x, rec, AP, firsts);  // u -> v is the down arc
+      else place(uv.x, r.y, r.x, uv.y, rec, AP, firsts);
     }
   }
 }
@@ -440,8 +437,7 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
   }
   launch(k_rank0, grid_for(N0, B), B, 0, st, N0, R.own0, R.offs[1], R.rank0);
   note(K_RANK0);
-  launch(k_positions, gv, B, 0, st, comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP, R.firsts,
-         R.nlow);
+  launch(k_positions, gv, B, 0, st, comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP, R.firsts);
   note(K_POSITIONS);
 }
 
