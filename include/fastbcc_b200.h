@@ -148,9 +148,20 @@ int fbcc_plan_stats(fbcc_plan plan, fbcc_stats *stats);
 int fbcc_plan_destroy(fbcc_plan plan);
 
 /* Process-wide tuning knobs (result-neutral, like the reference's beta /
-   block / seed, bcc.py:147-155).  Keys: 0 Afforest sampling rounds (0..8),
-   1 giant-component skip (0/1), 2 path halving (0/1), 3 level-0 splitter
-   spacing, 4 higher-level splitter spacing (powers of two >= 2). */
+   block / seed, bcc.py:147-155; every setting gives identical outputs,
+   tests/test_gpu_mid.py::test_mid_graph_option_paths).  Keys:
+     0  sampling rounds always run (0..8; default 2)
+     1  giant-component skip in the remaining-arc link pass (0/1; 1)
+     3  level-0 list-ranking splitter spacing (power of two >= 2; 16)
+     4  higher-level splitter spacing (power of two >= 2; 8)
+     8  bitmask of sampling rounds followed by a compress (0 = first + last; 0xFF)
+    11  programmatic dependent launch (0/1; 1)
+    12  fbcc_run_host: arc ranges the edge upload is split into (1..64; 8)
+    13  Stage 5: bitmask of rounds that also hook along plain parent edges (3)
+    14  the last sampling compress also picks the giant (0/1; 1)
+    15  Stage 6 edge pass: staged rows + giant bitmap (0/1; 1)
+    16  adaptive sampling rounds beyond key 0, up to this many (3)
+   Keys 2, 5, 6, 7, 9, 10 are retired experiments: accepted and ignored. */
 int fbcc_set_option(int key, int value);
 int fbcc_get_option(int key);
 
