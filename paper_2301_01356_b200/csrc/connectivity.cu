@@ -239,13 +239,17 @@ bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, i
 // later rounds.
 template <int kPred, bool kRecord>
 __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int* comp,
-                           int2* fe, unsigned long long* __restrict__ prop, PredData pd, bool skel_parent) {
+                           int2* fe, unsigned long long* __restrict__ prop, PredData pd, bool skel_parent,
+                           bool parent_only) {
   pdl_enter();
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t s = __ldg(off + v);
     int c = v;
     const int64_t e = __ldg(off + v + 1);
-    if (s < e) {
+    if (kPred == PRED_SKEL && parent_only) {  // round 0 along plain parent edges only (no arc read)
+      const int4 rv = __ldg(pd.rec + v);
+      if (rv.z >= 0 && rv.w == 0 && rv.z < c) c = rv.z;
+    } else if (s < e) {
       int w = kPred == PRED_NONE ? round0_target(adj, v, s, e) : (int)__ldg(adj + s);
       int4 rv;
       if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
@@ -664,7 +668,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     // (k_chunk_rows)
   } else if (kRounds > 0) {
     const int sp = g_opt[OPT_SKEL_PARENT];
-    launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd, (sp & 1) != 0);  // round 0
+    launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd, (sp & 1) != 0,
+           (sp & 0x80) != 0);  // round 0
     note(K_HOOK_MIN);
   } else {
     launch(k_iota, gv, B, 0, st, comp, g.n, nullptr);
