@@ -341,6 +341,17 @@ def run_ours(args, rank, world, local_rank):
                             "l1tex_model_per_s": 148 * (clocks.get("sm_mhz") or 1965.0) * 1e6}
         sum_alg = 46 * m + 165 * n + 48 * T + 16  # SURVEY §8(d) end-to-end algorithmic bytes
         ms = total_ms / args.steps
+        # per-stage roofline (each stage reads its contract
+        # inputs and writes its outputs once) over the per-stage event times
+        stage_names = ["forest", "rooting", "tags", "fence", "skeleton_cc", "labelling"]
+        stage_bytes = [4 * (n + 1) + 4 * m + 4 * n + 8 * T, 8 * T + 16 * (2 * T) + 12 * n,
+                       4 * (n + 1) + 12 * m + 40 * n, 40 * n, 4 * (n + 1) + 16 * m + 16 * n,
+                       4 * (n + 1) + 14 * m + 37 * n]
+        stage_roof = {}
+        for nm, b_s, t_s in zip(stage_names, stage_bytes, stage_ms / args.steps):
+            gbs = b_s / (float(t_s) / 1e3) / 1e9 if t_s > 0 else None
+            stage_roof[nm] = {"alg_bytes": int(b_s), "ms": float(t_s), "achieved_gbs": gbs,
+                              "frac": gbs / hbm if gbs else None}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -351,6 +362,7 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
                          "frac": ach / hbm, "traffic": traffic, "peak_source": src,
                          "alg_bytes_per_launch": b, "gather_bound": gather_bound},
+            "stage_roofline": stage_roof,
             "pipeline_roofline": {"alg_bytes": sum_alg, "achieved_gbs": sum_alg / (ms / 1e3) / 1e9,
                                   "frac": sum_alg / (ms / 1e3) / 1e9 / hbm},
             "stage_ms": dict(zip(["forest", "rooting", "tags", "fence", "skeleton_cc", "labelling"],
