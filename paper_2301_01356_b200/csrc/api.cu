@@ -121,6 +121,7 @@ struct Pipeline {
   int* nlow;
   int* bmin;
   uint32_t* gbits;  // [ceil(n/32)] Stage 6: bit v = v in the giant skeleton component
+  const Side* side = nullptr;  // second stream for Stage 6's independent pieces (plan capture, host path)
 
   Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
            const fbcc_outputs* o)
@@ -217,7 +218,7 @@ struct Pipeline {
                     cudaEvent_t heads_done) {
     stage2_rooting_fused(g, comp, fe, R, T.AP, sc, st);
     mk(2);
-    stage3_tags(g, R, T, st, nlow);
+    stage3_tags(g, R, T, st, nlow, side, uoff, R.cub_tmp, R.cub_bytes);
     mk(3);
     stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st);
     mk(4);
@@ -225,7 +226,7 @@ struct Pipeline {
     mk(5);
     if (label_done) cudaEventRecord(label_done, st);
     stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, gbits, R.cub_tmp,
-                     R.cub_bytes, sc, st, heads_done);
+                     R.cub_bytes, sc, st, heads_done, side);
     mk(6);
   }
 
@@ -425,6 +426,7 @@ int fbcc_run(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m
 struct HostStreams {
   int dev = -1;
   cudaStream_t cs = nullptr;
+  Side side;  // Stage 6's independent pieces
   cudaEvent_t ev[5 + kMaxStreamChunks] = {};
 };
 static thread_local HostStreams g_hs;
@@ -435,10 +437,15 @@ static cudaError_t host_streams() {
   if (e != cudaSuccess || g_hs.dev == dev) return e;
   if (g_hs.cs) {  // switched device: the old objects belong to the old one
     cudaStreamDestroy(g_hs.cs);
+    cudaStreamDestroy(g_hs.side.s);
     for (auto& x : g_hs.ev) cudaEventDestroy(x);
+    for (auto& x : g_hs.side.ev) cudaEventDestroy(x);
   }
   g_hs = HostStreams{};
   e = cudaStreamCreateWithFlags(&g_hs.cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g_hs.side.s, cudaStreamNonBlocking);
+  for (auto& x : g_hs.side.ev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
   for (auto& x : g_hs.ev)
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
   if (e == cudaSuccess) g_hs.dev = dev;
@@ -468,6 +475,7 @@ int fbcc_run_host(const fbcc_host_io* io, int64_t n, int64_t m, int64_t* d_offse
   int nchunk = g_opt[OPT_STREAM_CHUNKS];
   if (nchunk < 1) nchunk = 1;
   if (nchunk > kMaxStreamChunks) nchunk = kMaxStreamChunks;
+  if (!log->profile) P.side = &g_hs.side;  // (profiled runs stay on one stream)
   P.enqueue_host(st, g_hs.cs, *io, g_hs.ev, nchunk, timing ? ev : nullptr);
   g_log = nullptr;
   e = cudaGetLastError();
@@ -511,6 +519,14 @@ int fbcc_plan_create(const int64_t* offsets, const uint32_t* edges, int64_t n, i
     // kernels also cuts their programmatic (PDL) edge
     p->timing = (flags & (FBCC_FLAG_TIMING | FBCC_FLAG_PROFILE)) != 0;
     for (int i = 0; i < 7 && e == cudaSuccess && p->timing; i++) e = cudaEventCreate(&p->ev[i]);
+    // Stage 6's independent pieces on a forked capture stream (not when
+    // profiling: the launch log times consecutive launches on one stream)
+    Side side;
+    const bool use_side = !p->log->profile;
+    if (use_side && e == cudaSuccess) e = cudaStreamCreateWithFlags(&side.s, cudaStreamNonBlocking);
+    for (int i = 0; i < 4 && use_side && e == cudaSuccess; i++)
+      e = cudaEventCreateWithFlags(&side.ev[i], cudaEventDisableTiming);
+    if (use_side && e == cudaSuccess) p->pipe->side = &side;
     if (e == cudaSuccess) e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
       g_log = p->log;
@@ -519,9 +535,13 @@ int fbcc_plan_create(const int64_t* offsets, const uint32_t* edges, int64_t n, i
       g_log = nullptr;
       e = cudaStreamEndCapture(cap, &graph);
     }
+    p->pipe->side = nullptr;
     if (e == cudaSuccess) e = cudaGraphInstantiate(&p->exec, graph, 0);
     if (graph) cudaGraphDestroy(graph);
     cudaStreamDestroy(cap);
+    if (side.s) cudaStreamDestroy(side.s);
+    for (auto& x : side.ev)
+      if (x) cudaEventDestroy(x);
     if (e == cudaSuccess) e = cudaMallocHost((void**)&p->host, sizeof(Scalars));
     if (e != cudaSuccess) {
       fbcc_plan_destroy(p);

@@ -112,7 +112,17 @@ void stage2_rooting_fused(const Graph& g, const int* comp, const int2* fe, Rooti
 // nlow == nullptr: the reference's exact w2 (both forest directions
 // excluded, stand-alone op); otherwise the pipeline's relaxed gather (same
 // w1/low/high), which also counts each row's lower neighbours into nlow
-void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow);
+// A second stream for the two Stage-6 pieces that do not depend on the
+// stages in between: the upper-degree scan (needs only Stage 3's nlow) runs
+// beside Stages 3-5, the articulation flags beside the edge pass.  Fork/join
+// by events (captured into the plan's graph as edges).
+struct Side {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[4] = {};  // fork scan, join scan, fork ap, join ap
+};
+
+void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow, const Side* side = nullptr,
+                 int* uoff = nullptr, void* cub_tmp = nullptr, size_t cub_bytes = 0);
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
                   int* bmin,
                   cudaStream_t st);
@@ -120,7 +130,8 @@ void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned lo
                         cudaStream_t st);
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, uint32_t* gbits, void* cub_tmp,
-                      size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done = nullptr);
+                      size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done = nullptr,
+                      const Side* side = nullptr);
 void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* AP, int* forest,
                   int* parent, int* first, int* last, int* w1, int* w2, uint8_t* fence,
                   cudaStream_t st);

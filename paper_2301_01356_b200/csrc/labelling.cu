@@ -371,22 +371,34 @@ __global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) {
 
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, uint32_t* gbits, void* cub_tmp,
-                      size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done) {
+                      size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done, const Side* side) {
   const int n = g.n;
   const int B = 256;
   const int gv = grid_for(n + 1, B);
   // head = -1, cnt = 0, bmin = INF were initialised by the stage-4 kernel
   launch(k_heads, gv, B, 0, st, n, rec, label, head, cnt, gbits, sc);
   note(K_HEADS);
-  if (is_ap) {
-    launch(k_ap, gv, B, 0, st, n, label, head, cnt, is_ap);
-    note(K_AP);
+  if (side) {  // articulation flags beside the edge pass; the scan ran beside Stages 3-5
+    cudaEventRecord(side->ev[2], st);
+    cudaStreamWaitEvent(side->s, side->ev[2], 0);
+    if (is_ap) {
+      launch(k_ap, gv, B, 0, side->s, n, label, head, cnt, is_ap);
+      note(K_AP);
+    }
+    if (heads_done) cudaEventRecord(heads_done, side->s);  // head / is_ap final: their D2H may start
+    cudaEventRecord(side->ev[3], side->s);
+    cudaStreamWaitEvent(st, side->ev[1], 0);  // uoff
+  } else {
+    if (is_ap) {
+      launch(k_ap, gv, B, 0, st, n, label, head, cnt, is_ap);
+      note(K_AP);
+    }
+    if (heads_done) cudaEventRecord(heads_done, st);  // head / is_ap final: their D2H may start
+    // edge ids: exclusive scan of the upper degrees deg - nlow (nlow counted
+    // by the Stage-3 gather) -> uoff (uoff[n] = E)
+    scan_upper_degrees(g.off, nlow, n, uoff, cub_tmp, cub_bytes, st);
+    note(K_SCAN);
   }
-  if (heads_done) cudaEventRecord(heads_done, st);  // head / is_ap final: their D2H may start
-  // edge ids: exclusive scan of the upper degrees deg - nlow (nlow counted
-  // by the Stage-3 gather) -> uoff (uoff[n] = E)
-  scan_upper_degrees(g.off, nlow, n, uoff, cub_tmp, cub_bytes, st);
-  note(K_SCAN);
   if (!edge_label || g.m == 0) {
     launch(k_set_edges, 1, 1, 0, st, uoff, n, sc);
     note(K_SET_EDGES);
@@ -405,6 +417,7 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
     launch(k_edge_final, grid_for(g.m / 2, B), B, 0, st, edge_label, bmin, uoff, n);
     note(K_EDGE_FINAL);
   }
+  if (side) cudaStreamWaitEvent(st, side->ev[3], 0);  // join the articulation flags
 }
 
 // ---------------------------------------------------------------------------

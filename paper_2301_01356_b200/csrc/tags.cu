@@ -332,7 +332,8 @@ __global__ void k_table_level(int2* table, int ntile, int k) {
   }
 }
 
-void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow) {
+void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow, const Side* side, int* uoff,
+                 void* cub_tmp, size_t cub_bytes) {
   const int B = 256;
   int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (!nlow) {  // stand-alone compute_tags: the reference's exact w2
@@ -352,6 +353,13 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
   }
   if (g.m > 0) {
     note(K_W_GATHER);
+  }
+  if (side && nlow) {  // nlow is final: Stage 6's upper-degree scan runs beside Stages 3-5
+    cudaEventRecord(side->ev[0], st);
+    cudaStreamWaitEvent(side->s, side->ev[0], 0);
+    scan_upper_degrees(g.off, nlow, g.n, uoff, cub_tmp, cub_bytes, side->s);
+    note(K_SCAN);
+    cudaEventRecord(side->ev[1], side->s);
   }
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
   launch(k_tile, grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile, T.lh1,
