@@ -89,7 +89,10 @@ struct Tags {
   int tlev;
 };
 
-constexpr int kTile = 4096;      // tour positions per tile in the low/high pass
+#ifndef FBCC_TILE
+#define FBCC_TILE 4096
+#endif
+constexpr int kTile = FBCC_TILE;  // tour positions per tile in the low/high pass
 
 void rooting_roots(int n, const int* comp, Rooting& R, Scalars* sc, cudaStream_t st);
 void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc, cudaStream_t st);

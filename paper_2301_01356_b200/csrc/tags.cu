@@ -202,7 +202,7 @@ __global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ 
 constexpr int kTileThreads = 512;
 constexpr int kSub = 32;
 constexpr int kNSub = kTile / kSub;  // 128
-constexpr int kSubLev = 8;           // levels 0..7 over 128 sub-blocks
+constexpr int kSubLev = 32 - __builtin_clz(kNSub);  // levels 0..log2(kNSub) (8 for 128 sub-blocks)
 constexpr size_t kTileSmem = sizeof(int2) * (3 * kTile + kSubLev * kNSub);
 
 struct TileSmem {
