@@ -80,6 +80,7 @@ enum Option : int {
   OPT_GIANT_FOLD = 14,    // the last sampling compress also picks the giant (no k_find_giant)
   OPT_EB_STAGED = 15,     // Stage 6 edge blocks: warp-staged rows + giant bitmap (0: plain arc visitor)
   OPT_MAX_ROUNDS = 16,    // adaptive sampling rounds beyond OPT_SAMPLE_ROUNDS, up to this many (see skip_round)
+  OPT_SKEL_MAX_ROUNDS = 17,  // Stage 5's cap instead (0: OPT_MAX_ROUNDS)
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 20
 };

@@ -650,8 +650,10 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
                    int slot, cudaStream_t st, bool round0_done = false, RootInit ri = RootInit{}) {
   const int B = 256;
   const int kBase = g_opt[OPT_SAMPLE_ROUNDS];
-  // adaptive rounds kBase .. kRounds-1 (skip_round)
-  const int kRounds = g_opt[OPT_MAX_ROUNDS] > kBase ? std::min(g_opt[OPT_MAX_ROUNDS], 8) : kBase;
+  // adaptive rounds kBase .. kRounds-1 (skip_round); Stage 5 may cap them separately
+  int max_rounds = g_opt[OPT_MAX_ROUNDS];
+  if (kPred == PRED_SKEL && g_opt[OPT_SKEL_MAX_ROUNDS] > 0) max_rounds = g_opt[OPT_SKEL_MAX_ROUNDS];
+  const int kRounds = max_rounds > kBase ? std::min(max_rounds, 8) : kBase;
   const int gv = grid_for(g.n, B);
   // k_compress relies on concurrent threads advancing each other's pointers:
   // its grid must be fully resident (2048 threads/SM), or grid-stride
