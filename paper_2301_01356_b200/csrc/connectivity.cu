@@ -279,7 +279,10 @@ __global__ void k_iota(int* __restrict__ comp, int n, unsigned long long* __rest
 // ---------------------------------------------------------------------------
 // sampling rounds
 // ---------------------------------------------------------------------------
-constexpr int kPerRoot = 32;
+#ifndef FBCC_PER_ROOT
+#define FBCC_PER_ROOT 32
+#endif
+constexpr int kPerRoot = FBCC_PER_ROOT;
 
 // Rounds at or past rbase are adaptive: they run only while the previous
 // round still hooked >= 5% as many roots as the one before it and >= n/8192
