@@ -118,3 +118,24 @@ def test_mid_graph_option_paths(name, oracle_mod):
     finally:
         for k, v in defaults.items():
             _lib.set_option(k, v)
+
+
+# Graphs past the edge pass's shared-memory bitmap (n > 1.6M vertices): the
+# global-bitmap path (a giant holding >= 1/4 of Stage 5's samples) and the
+# label-gather path (small giant), plus the largest graph the shared-memory
+# path takes.
+BIG = {
+    "uniform_1p55m_d4": lambda: workloads.uniform(1_550_000, 4, seed=7),   # shared-memory bitmap, near its limit
+    "uniform_1p8m_d4": lambda: workloads.uniform(1_800_000, 4, seed=8),    # global bitmap (giant ~all)
+    "uniform_1p8m_d1": lambda: workloads.uniform(1_800_000, 1, seed=9),    # label gathers (no giant)
+}
+
+
+@pytest.mark.parametrize("name", sorted(BIG))
+def test_big_graph_edge_paths(name, oracle_mod):
+    g = BIG[name]()
+    ref = oracle_mod.fast_bcc(g.offsets, g.edges)
+    r = _run(g, debug=False)
+    for k in ("label", "head", "is_ap", "edge_label"):
+        assert np.array_equal(r[k], ref[k]), (name, k)
+    assert r["num_bccs"] == ref["num_bccs"] and r["num_components"] == ref["num_components"]
