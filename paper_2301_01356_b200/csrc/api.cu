@@ -218,7 +218,7 @@ struct Pipeline {
                     cudaEvent_t heads_done) {
     stage2_rooting_fused(g, comp, fe, R, T.AP, sc, st);
     mk(2);
-    stage3_tags(g, R, T, st, nlow, side, uoff, R.cub_tmp, R.cub_bytes);
+    stage3_tags(g, R, T, st, nlow, side, uoff, R.cub_tmp, R.cub_bytes, sc);
     mk(3);
     stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st);
     mk(4);

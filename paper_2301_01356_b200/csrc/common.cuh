@@ -26,7 +26,8 @@ struct Scalars {
   int has_hubs;    // some row has >= kHubDeg slots (set by k_chunk_rows)
   unsigned ticket; // last-block detection (k_compress; reset by the last block)
   int giant_cnt;   // samples (of 1024) that fell in the giant at its pick
-  int pad[22];
+  unsigned tile_ticket;  // k_tile: last block builds the tile-extreme table (reset by it)
+  int pad[21];
 };
 
 // ---------------------------------------------------------------------------

@@ -125,7 +125,7 @@ struct Side {
 };
 
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow, const Side* side = nullptr,
-                 int* uoff = nullptr, void* cub_tmp = nullptr, size_t cub_bytes = 0);
+                 int* uoff = nullptr, void* cub_tmp = nullptr, size_t cub_bytes = 0, Scalars* sc = nullptr);
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
                   int* bmin,
                   cudaStream_t st);

@@ -239,9 +239,26 @@ struct TileSmem {
   }
 };
 
+constexpr int kTableOneCta = 16384;
+
+__device__ __forceinline__ void table_levels(int2* table, int ntile, int tlev) {
+  for (int k = 1; k < tlev; k++) {
+    const int2* prev = table + (int64_t)(k - 1) * ntile;
+    int2* cur = table + (int64_t)k * ntile;
+    const int half = 1 << (k - 1);
+    for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
+      int2 a = prev[i];
+      cur[i] = (i + half < ntile) ? comb(a, prev[i + half]) : a;
+    }
+    __syncthreads();
+  }
+}
+
+// (sc != nullptr: the last block to finish also builds every level of the
+// tile-extreme sparse table -- k_table_all's work, one launch fewer)
 __global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int4* __restrict__ AP,
                                                           int64_t N, int ntile, int2* __restrict__ lh1,
-                                                          int2* __restrict__ lh2, int2* __restrict__ table0) {
+                                                          int2* __restrict__ lh2, int2* __restrict__ table0, Scalars* sc, int tlev) {
   pdl_enter();
   extern __shared__ int2 smem[];
   TileSmem S;
@@ -300,25 +317,28 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int4* __restrict
     }
     __syncthreads();
   }
+  if (sc) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(&sc->tile_ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      table_levels(table0, ntile, tlev);
+      if (threadIdx.x == 0) sc->tile_ticket = 0;
+    }
+  }
 }
 
 // all levels of the tile-extreme sparse table in one CTA (levels are
 // published to the block by __syncthreads; every level is tiny next to a
 // launch when ntile <= kTableOneCta)
-constexpr int kTableOneCta = 16384;
 
 __global__ void __launch_bounds__(1024) k_table_all(int2* table, int ntile, int tlev) {
   pdl_enter();
-  for (int k = 1; k < tlev; k++) {
-    const int2* prev = table + (int64_t)(k - 1) * ntile;
-    int2* cur = table + (int64_t)k * ntile;
-    const int half = 1 << (k - 1);
-    for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
-      int2 a = prev[i];
-      cur[i] = (i + half < ntile) ? comb(a, prev[i + half]) : a;
-    }
-    __syncthreads();
-  }
+  table_levels(table, ntile, tlev);
 }
 
 __global__ void k_table_level(int2* table, int ntile, int k) {
@@ -333,7 +353,7 @@ __global__ void k_table_level(int2* table, int ntile, int k) {
 }
 
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow, const Side* side, int* uoff,
-                 void* cub_tmp, size_t cub_bytes) {
+                 void* cub_tmp, size_t cub_bytes, Scalars* sc) {
   const int B = 256;
   int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (!nlow) {  // stand-alone compute_tags: the reference's exact w2
@@ -362,10 +382,13 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
     cudaEventRecord(side->ev[1], side->s);
   }
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+  // (the table in k_tile's last block when it fits one CTA and a ticket word exists)
+  Scalars* tsc = (sc && T.ntile <= kTableOneCta && T.tlev > 1) ? sc : nullptr;
   launch(k_tile, grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile, T.lh1,
-                                                                  T.lh2, T.table);
+         T.lh2, T.table, tsc, T.tlev);
   note(K_TILE);
-  if (T.ntile <= kTableOneCta) {
+  if (tsc) {
+  } else if (T.ntile <= kTableOneCta) {
     if (T.tlev > 1) {
       launch(k_table_all, 1, 1024, 0, st, T.table, T.ntile, T.tlev);
       note(K_TABLE);
