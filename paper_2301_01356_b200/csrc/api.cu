@@ -39,7 +39,7 @@ constexpr int kMaxStreamChunks = 64;
 struct Layout {
   size_t total = 0;
   size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, hsub, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
-      nlow, bmin, gbits, cub;
+      nlow, bmin, gbits, w0, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
   int64_t K[8] = {0};
@@ -101,6 +101,7 @@ struct Layout {
     nlow = take(4 * n);
     bmin = take(4 * n);
     gbits = take(4 * ((n + 31) / 32 + 4));
+    w0 = take(4 * n);
     cub = take(cub_bytes);
   }
 };
@@ -122,6 +123,8 @@ struct Pipeline {
   int* bmin;
   uint32_t* gbits;  // [ceil(n/32)] Stage 6: bit v = v in the giant skeleton component
   const Side* side = nullptr;  // second stream for Stage 6's independent pieces (plan capture, host path)
+  int* w0;          // [n] each row's first arc target (Stage 1's round 0 -> Stage 5's round 0)
+  bool w0_valid = false;
 
   Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
            const fbcc_outputs* o)
@@ -175,6 +178,7 @@ struct Pipeline {
     nlow = (int*)at(lay.nlow);
     bmin = (int*)at(lay.bmin);
     gbits = (uint32_t*)at(lay.gbits);
+    w0 = (int*)at(lay.w0);
   }
 
   // Enqueue all six stages.  ev (7 events) brackets the stages when given.
@@ -183,7 +187,8 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    const bool round0 = build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, comp, fe, prop, nlow);
+    const bool round0 = build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, comp, fe, prop, nlow, w0);
+    w0_valid = round0;
     stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args());
     mk(1);
     enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
@@ -222,7 +227,7 @@ struct Pipeline {
     mk(3);
     stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st);
     mk(4);
-    stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st);
+    stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st, w0_valid ? w0 : nullptr);
     mk(5);
     if (label_done) cudaEventRecord(label_done, st);
     stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, gbits, R.cub_tmp,

@@ -45,6 +45,7 @@ enum : int { PRED_NONE = 0, PRED_SKEL = 1, PRED_MASK = 2 };
 
 struct PredData {
   const int4* rec;        // PRED_SKEL: {first, last, parent, fence}
+  const int* w0;          // PRED_SKEL (optional): each row's first arc target, recorded by Stage 3
   const uint8_t* mask;    // PRED_MASK: per-slot keep byte
   const int64_t* off;     // PRED_MASK: to find the canonical (u < w) slot
   const uint32_t* adj;
@@ -155,8 +156,10 @@ __device__ __forceinline__ int link(int u, int w, int* comp, int2* fe) {
 #endif
 constexpr int kNear = FBCC_NEAR;
 
-__device__ __forceinline__ int round0_target(const uint32_t* __restrict__ adj, int v, int64_t rs, int64_t re) {
+__device__ __forceinline__ int round0_target(const uint32_t* __restrict__ adj, int v, int64_t rs, int64_t re,
+                                             int* first_arc = nullptr) {
   const int w0 = (int)__ldg(adj + rs);
+  if (first_arc) *first_arc = w0;
   if (w0 >= v) return v;  // no smaller neighbour
   if (re - rs <= kItems) {
     int best = w0;
@@ -181,7 +184,7 @@ __device__ __forceinline__ int round0_target(const uint32_t* __restrict__ adj, i
 // into this pass over the offsets (comp != nullptr).
 __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __restrict__ crow, Scalars* sc,
                              const uint32_t* __restrict__ adj, int* __restrict__ comp, int2* __restrict__ fe,
-                             unsigned long long* __restrict__ prop, int* __restrict__ nlow) {
+                             unsigned long long* __restrict__ prop, int* __restrict__ nlow, int* __restrict__ w0) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -196,8 +199,10 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
       if (comp) {  // sampling round 0 (see k_hook_min)
         int c = v;
         if (rs < re) {
-          c = round0_target(adj, v, rs, re);
+          int first = v;
+          c = round0_target(adj, v, rs, re, &first);
           if (c < v) fe[v] = make_int2(v, c);
+          w0[v] = first;  // Stage 5's round-0 arc (coalesced; saves it a cold sector per row)
         }
         comp[v] = c;
         prop[v] = ~0ull;
@@ -219,14 +224,14 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
 }
 
 bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp, int2* fe,
-                      unsigned long long* prop, int* nlow) {
+                      unsigned long long* prop, int* nlow, int* w0) {
   if (g.m == 0) {
     if (nlow) cudaMemsetAsync(nlow, 0, sizeof(int) * g.n, st);
     return false;
   }
   const bool fold = comp != nullptr && g_opt[OPT_SAMPLE_ROUNDS] > 0;
   launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow, sc, g.adj, fold ? comp : nullptr, fe, prop,
-         nlow);
+         nlow, w0);
   note(K_CHUNK_ROWS);
   return fold;
 }
@@ -250,7 +255,10 @@ __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __re
       const int4 rv = __ldg(pd.rec + v);
       if (rv.z >= 0 && rv.w == 0 && rv.z < c) c = rv.z;
     } else if (s < e) {
-      int w = kPred == PRED_NONE ? round0_target(adj, v, s, e) : (int)__ldg(adj + s);
+      // (Stage 5: the first arc's target as Stage 3's gather recorded it --
+      // a coalesced 4-byte read instead of one cold adjacency sector per row)
+      int w = kPred == PRED_NONE ? round0_target(adj, v, s, e)
+                                 : (kPred == PRED_SKEL && pd.w0) ? __ldg(pd.w0 + v) : (int)__ldg(adj + s);
       int4 rv;
       if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
       if (w < v && keep<kPred>(pd, v, rv, w, s)) {
@@ -787,9 +795,10 @@ void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop
 }
 
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
-                        cudaStream_t st) {
+                        cudaStream_t st, const int* w0) {
   PredData pd{};
   pd.rec = rec;
+  pd.w0 = w0;
   run_cc<PRED_SKEL, false>(g, label, nullptr, prop, pd, sc, 8, st);
 }
 

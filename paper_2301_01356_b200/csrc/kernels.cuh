@@ -19,7 +19,7 @@ struct Graph {
 // (comp/fe/prop given: also Stage 1's sampling round 0; returns whether it ran)
 // (nlow given: also zeroes Stage 3's lower-degree counters, coalesced)
 bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp = nullptr,
-                      int2* fe = nullptr, unsigned long long* prop = nullptr, int* nlow = nullptr);
+                      int2* fe = nullptr, unsigned long long* prop = nullptr, int* nlow = nullptr, int* w0 = nullptr);
 
 // Stage 2 initial state written by Stage 1's final compress (one pass over
 // the vertices instead of a separate k_root_flags): flags[v] = v is a root
@@ -129,8 +129,9 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
                   int* bmin,
                   cudaStream_t st);
+// (w0: each row's first arc target, recorded by k_chunk_rows' round 0; nullptr: read adj)
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
-                        cudaStream_t st);
+                        cudaStream_t st, const int* w0 = nullptr);
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, uint32_t* gbits, void* cub_tmp,
                       size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done = nullptr,
