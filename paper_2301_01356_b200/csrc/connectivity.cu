@@ -718,9 +718,11 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     launch(k_link_rows<kPred, kRecord>, grid_for(g.n, B, 32), B, 0, st, g.off, g.adj, g.n, comp, fe, pd, sc, heavy,
                                                                     nheavy);
     note(K_LINK_ROWS);
-    launch(k_link_heavy<kPred, kRecord>, grid_for((int64_t)kNumSMs * 2048, B), B, 0, st, g.off, g.adj, comp, fe, pd,
-                                                                                     heavy, nheavy);
-    note(K_LINK_HEAVY);
+    if (!g.no_super_rows) {
+      launch(k_link_heavy<kPred, kRecord>, grid_for((int64_t)kNumSMs * 2048, B), B, 0, st, g.off, g.adj, comp, fe,
+             pd, heavy, nheavy);
+      note(K_LINK_HEAVY);
+    }
   }
   launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0,
          0);  // final root count (= components)
@@ -787,6 +789,21 @@ void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t s
   launch(k_compress<true>, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
          (const int*)nullptr, 0, 0);
   note(K_COMPRESS);
+}
+
+__global__ void k_super_rows(const int64_t* __restrict__ off, int n, int* flag) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (__ldg(off + v + 1) - __ldg(off + v) > kSuperRow) *flag = 1;
+}
+
+bool graph_has_super_rows(const Graph& g, void* scratch4, cudaStream_t st) {
+  int* d = (int*)scratch4;
+  int h = 1;
+  if (cudaMemsetAsync(d, 0, sizeof(int), st) != cudaSuccess) return true;
+  k_super_rows<<<grid_for(g.n, 256), 256, 0, st>>>(g.off, g.n, d);
+  if (cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) return true;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return true;
+  return h != 0;
 }
 
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st,
