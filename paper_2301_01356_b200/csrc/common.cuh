@@ -82,6 +82,7 @@ enum Option : int {
   OPT_EB_STAGED = 15,     // Stage 6 edge blocks: warp-staged rows + giant bitmap (0: plain arc visitor)
   OPT_MAX_ROUNDS = 16,    // adaptive sampling rounds beyond OPT_SAMPLE_ROUNDS, up to this many (see skip_round)
   OPT_SKEL_MAX_ROUNDS = 17,  // Stage 5's cap instead (0: OPT_MAX_ROUNDS)
+  OPT_ACCEPT_FOLD = 18,   // a sampling round's accept runs inside the compress that follows it
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 20
 };

@@ -365,8 +365,9 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
     unsigned long long key = prop[v];
     if (key == ~0ull) continue;
     prop[v] = ~0ull;  // ready for the next round
+    if (__ldcg(comp + v) != v) continue;  // proposed to on a two-level view (see k_compress<kAccept>)
     int lo = (int)(key >> 32);
-    comp[v] = lo;     // v is a round-start root (only roots receive proposals)
+    comp[v] = lo;
     hooked++;
     if (kRecord) {
       int u = (int)(key & 0xffffffffull);
@@ -402,11 +403,21 @@ __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable)
 // (hooks != nullptr: the compress after adaptive sampling round `round`; it
 // does no pointer work when that round was skipped -- comp is still flat
 // from the previous round's compress -- but still picks the giant)
-template <bool kJump>
+// kAccept: the compress after propose round `round` first applies that
+// round's proposals (k_accept folded in: one pass over the vertices fewer per
+// round).  A vertex hooked here may already have been taken for a root by a
+// thread that climbed through it, so the array can come out two levels deep:
+// the next round's proposals then verify their target is still a root
+// (accept below), k_link_rows' giant test looks two levels up and falls back
+// to linking, and the final compress (no kAccept) makes the labels flat.
+template <bool kJump, bool kAccept = false, bool kRecord = false>
 __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable, RootInit ri,
-                           const int* hooks, int round, int rbase) {
+                           const int* hooks, int round, int rbase, unsigned long long* prop = nullptr,
+                           int* hooks_out = nullptr, int2* fe = nullptr, const int64_t* __restrict__ off = nullptr,
+                           const uint32_t* __restrict__ adj = nullptr) {
   pdl_enter();
   int roots = 0;
+  int hooked = 0;
   const int n_work = (hooks && skip_round(hooks, round, rbase, n)) ? 0 : n;
   const int64_t* hoff = (ri.flags && ri.off && ri.sc->has_hubs) ? ri.off : nullptr;
   if (ri.flags && blockIdx.x == 0 && threadIdx.x == 0) ri.flags[n] = 0;
@@ -416,6 +427,21 @@ __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, boo
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_work; base += (int64_t)gridDim.x * blockDim.x) {
     const int v = (int)base + threadIdx.x;
     int c = v < n ? __ldcg(comp + v) : v;
+    if (kAccept && v < n) {
+      const unsigned long long key = prop[v];
+      if (key != ~0ull) {
+        prop[v] = ~0ull;  // ready for the next round
+        if (c == v) {     // still a root (a stale proposal is dropped)
+          c = (int)(key >> 32);
+          comp[v] = c;
+          hooked++;
+          if (kRecord) {
+            const int u = (int)(key & 0xffffffffull);
+            fe[v] = make_int2(u, (int)__ldg(adj + __ldg(off + u) + round));
+          }
+        }
+      }
+    }
     const bool root = c == v;
     if (kJump) {
       // Pointer jumping inside the block's id range (after sampling round 0
@@ -458,6 +484,7 @@ __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, boo
     __stcg(comp + v, c);
   }
   if (nroots) block_count_add(nroots, roots);
+  if (kAccept) block_count_add(hooks_out, hooked);
   if (giant_sc) {
     __shared__ bool last;
     __syncthreads();
@@ -690,19 +717,30 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   }
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
+    // a round followed by a compress folds its accept into it (OPT_ACCEPT_FOLD)
+    const bool fold = r > 0 && ((cmask >> r) & 1) && g_opt[OPT_ACCEPT_FOLD];
     if (r > 0) {
       launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat,
              ((g_opt[OPT_SKEL_PARENT] >> r) & 1) != 0, kBase);
       note(K_PROPOSE);
-      launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase);
-      note(K_ACCEPT);
+      if (!fold) {
+        launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase);
+        note(K_ACCEPT);
+      }
     }
     if ((cmask >> r) & 1) {
       // the last sampling round's compress also picks the giant
       const bool last_round = r == kRounds - 1 && g_opt[OPT_GIANT_FOLD];
-      launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
-             last_round ? sc : nullptr, g_opt[OPT_GIANT_SKIP] != 0, RootInit{}, r >= kBase ? (const int*)hooks : nullptr,
-             r, kBase);
+      const int* skip_hooks = r >= kBase ? (const int*)hooks : nullptr;
+      if (fold) {
+        launch(k_compress<false, true, kRecord>, gres, B, 0, st, comp, g.n, (int*)nullptr, last_round ? sc : nullptr,
+               g_opt[OPT_GIANT_SKIP] != 0, RootInit{}, skip_hooks, r, kBase, prop, hooks + r, fe, g.off, g.adj);
+      } else {
+        launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
+               last_round ? sc : nullptr, g_opt[OPT_GIANT_SKIP] != 0, RootInit{}, skip_hooks, r, kBase,
+               (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
+               (const uint32_t*)nullptr);
+      }
       note(K_COMPRESS);
     }
   }
@@ -724,8 +762,9 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       note(K_LINK_HEAVY);
     }
   }
-  launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0,
-         0);  // final root count (= components)
+  launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0, 0,
+         (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
+         (const uint32_t*)nullptr);  // final root count (= components)
   note(K_COMPRESS);
 }
 
@@ -787,7 +826,8 @@ void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2
 void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st, RootInit ri) {
   const int B = 256;
   launch(k_compress<true>, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
-         (const int*)nullptr, 0, 0);
+         (const int*)nullptr, 0, 0, (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr,
+         (const int64_t*)nullptr, (const uint32_t*)nullptr);
   note(K_COMPRESS);
 }
 

@@ -94,7 +94,9 @@ def test_mid_graph_rungs(name, oracle_mod):
 # outputs (the edge-block pass without the bitmap is what graphs with
 # n > 1.6M run; max_rounds runs the adaptive sampling rounds and their skips)
 OPTION_VARIANTS = [{"eb_staged": 0}, {"max_rounds": 6}, {"max_rounds": 8, "sample_rounds": 2}, {"pdl": 0},
-                   {"sample_rounds": 1}, {"giant_skip": 0}, {"s0": 8, "sl": 4}]
+                   {"sample_rounds": 1}, {"giant_skip": 0}, {"s0": 8, "sl": 4}, {"accept_fold": 1},
+                   {"accept_fold": 1, "max_rounds": 5}, {"skel_parent": 131}, {"skel_max_rounds": 4},
+                   {"compress_mask": 0}]
 
 
 @pytest.mark.parametrize("name", ["rmat_s16", "isolated_mix", "star_mid_20k", "uniform_64k_d3", "chain_300k",
