@@ -355,12 +355,22 @@ __global__ void k_rank0(int64_t N, const int2* __restrict__ own0, const int* __r
   }
 }
 
+// (own0 != nullptr: the level-0 ranks are expanded here -- rank(e) =
+// offs1[own0[e].seg] + own0[e].off, one 16-byte load for both elements of x
+// -- instead of by k_rank0)
 __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict__ fe,
                             const int2* __restrict__ rank0, int n, int4* __restrict__ rec,
-                            int4* __restrict__ AP, int* __restrict__ firsts) {
+                            int4* __restrict__ AP, int* __restrict__ firsts, const int4* __restrict__ own0,
+                            const int* __restrict__ offs1) {
   pdl_enter();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-    int2 r = __ldg(rank0 + x);  // ranks of elements 2x and 2x+1, one 8-byte load
+    int2 r;
+    if (own0) {
+      const int4 o = __ldg(own0 + x);  // (seg, off) of elements 2x and 2x+1
+      r = make_int2(__ldg(offs1 + o.x) + o.y, __ldg(offs1 + o.z) + o.w);
+    } else {
+      r = __ldg(rank0 + x);  // ranks of elements 2x and 2x+1, one 8-byte load
+    }
     if (__ldg(comp + x) == x) {
       place(x, r.x, r.y, -1, rec, AP, firsts);  // enter(x), exit(x)
     } else {
@@ -435,10 +445,20 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
     launch(k_expand, grid_for(R.K[l], B), B, 0, st, R.K[l], R.own[l], R.offs[l + 1], R.offs[l]);
     note(K_EXPAND);
   }
-  launch(k_rank0, grid_for(N0, B), B, 0, st, N0, R.own0, R.offs[1], R.rank0);
-  note(K_RANK0);
-  launch(k_positions, gv, B, 0, st, comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP, R.firsts);
-  note(K_POSITIONS);
+#ifndef FBCC_FUSED_RANK0
+#define FBCC_FUSED_RANK0 1
+#endif
+  if (FBCC_FUSED_RANK0) {
+    launch(k_positions, gv, B, 0, st, comp, fe, (const int2*)nullptr, n, R.rec, AP, R.firsts,
+           reinterpret_cast<const int4*>(R.own0), (const int*)R.offs[1]);
+    note(K_POSITIONS);
+  } else {
+    launch(k_rank0, grid_for(N0, B), B, 0, st, N0, R.own0, R.offs[1], R.rank0);
+    note(K_RANK0);
+    launch(k_positions, gv, B, 0, st, comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP, R.firsts,
+           (const int4*)nullptr, (const int*)nullptr);
+    note(K_POSITIONS);
+  }
 }
 
 }  // namespace fbcc
