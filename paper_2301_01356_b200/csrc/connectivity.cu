@@ -443,6 +443,7 @@ __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, boo
       }
     }
     const bool root = c == v;
+    const int mem = c;  // what comp[v] holds now
     if (kJump) {
       // Pointer jumping inside the block's id range (after sampling round 0
       // only): chains of consecutive ids -- round 0's left-neighbour hooks on
@@ -475,13 +476,15 @@ __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, boo
       if (x == c) { done = true; break; }
       c = x;
     }
+    bool stored = false;
     while (!done) {
       if (__ldca(comp + c) == c) break;  // root (stable during compress)
       int cc = __ldcg(comp + c);           // c's current pointer
       __stcg(comp + v, cc);
+      stored = true;
       c = cc;
     }
-    __stcg(comp + v, c);
+    if (stored || c != mem) __stcg(comp + v, c);  // (already-flat entries are not rewritten)
   }
   if (nroots) block_count_add(nroots, roots);
   if (kAccept) block_count_add(hooks_out, hooked);
