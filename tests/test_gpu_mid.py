@@ -141,3 +141,44 @@ def test_big_graph_edge_paths(name, oracle_mod):
     for k in ("label", "head", "is_ap", "edge_label"):
         assert np.array_equal(r[k], ref[k]), (name, k)
     assert r["num_bccs"] == ref["num_bccs"] and r["num_components"] == ref["num_components"]
+
+
+def _random_graph(seed):
+    """Seeded mix: uniform random (sparse to dense), tori with deletions,
+    paths with chords, and stars glued to them -- the shapes whose union-find
+    and tour structure the round-0 rule, the adaptive rounds and the
+    block-local compress treat differently."""
+    rng = np.random.default_rng(seed)
+    kind = seed % 4
+    if kind == 0:
+        n = int(rng.integers(2, 4000))
+        pairs = rng.integers(0, n, size=(int(n * rng.uniform(0.3, 6.0)), 2))
+    elif kind == 1:
+        r, c = int(rng.integers(2, 60)), int(rng.integers(2, 60))
+        return workloads.grid(r, c, circular=bool(rng.integers(0, 2)), keep_prob=float(rng.uniform(0.4, 1.0)),
+                              seed=int(seed))
+    elif kind == 2:
+        n = int(rng.integers(3, 5000))
+        i = np.arange(n - 1)
+        chords = rng.integers(0, n, size=(int(rng.integers(0, n // 3 + 1)), 2))
+        pairs = np.concatenate([np.column_stack([i, i + 1]), chords])
+    else:
+        n = int(rng.integers(10, 3000))
+        hub = int(rng.integers(0, n))
+        spokes = rng.choice(n, size=int(rng.integers(1, n)), replace=False)
+        extra = rng.integers(0, n, size=(int(rng.integers(0, 2 * n)), 2))
+        pairs = np.concatenate([np.column_stack([np.full(spokes.size, hub), spokes]), extra])
+    return symmetrize(pairs.astype(np.int64), n)
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_random_graphs_match_oracle(block, oracle_mod):
+    """200 seeded random graphs (50 per parametrisation), full outputs vs the
+    golden-pinned oracle."""
+    for seed in range(block * 50, block * 50 + 50):
+        g = _random_graph(seed)
+        ref = oracle_mod.fast_bcc(g.offsets, g.edges)
+        r = _run(g, debug=False)
+        for k in ("label", "head", "is_ap", "edge_label"):
+            assert np.array_equal(r[k], ref[k]), (seed, k)
+        assert r["num_bccs"] == ref["num_bccs"] and r["num_components"] == ref["num_components"], seed
