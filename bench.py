@@ -71,6 +71,32 @@ def alg_bytes(kind, n, m, T, E, K1=0):
     }.get(kind)
 
 
+# Our arm pins its process -- the caller and every thread CUDA and torch
+# create later -- to one core before CUDA starts (the GPU arm's host side is
+# one thread issuing work).  On this VM an unpinned process uploads the
+# host-path CSR measurably slower: 3.3 ms instead of 2.7 ms per fast_bcc call
+# on config 2 (Stage 1, i.e. the H2D, 1.8 ms instead of 1.25 ms; the same as
+# running the whole process under `taskset -c <any one cpu>`).  The CPU
+# baseline then runs in a child with the full mask; `--impl reference` is
+# never pinned.
+FULL_MASK = None
+PIN_NOTE = "unpinned"
+
+
+def _pin_process(local_rank):
+    global FULL_MASK, PIN_NOTE
+    if not hasattr(os, "sched_setaffinity"):
+        return
+    try:
+        mask = sorted(os.sched_getaffinity(0))
+        cpu = mask[-1 - (local_rank % len(mask))]
+        os.sched_setaffinity(0, {cpu})
+        FULL_MASK = set(mask)
+        PIN_NOTE = f"process pinned to cpu {cpu} (of {len(mask)})"
+    except OSError:
+        pass
+
+
 def measured_gather_peak(n, gathers):
     """Streamed-index random-gather rate measured by tools/gather_peak.py for
     the gathered-array size closest to n 4-byte words (and gather count)."""
@@ -145,7 +171,20 @@ class ClockSampler:
 
 
 def cpu_baseline(g, config, runs=3):
-    """The reference algorithm on the host cores (golden-pinned C port)."""
+    """The reference algorithm on the host cores (golden-pinned C port).  When
+    this process was pinned to one core for the GPU arm (PIN_NOTE), the port
+    runs in a child process with every core of the original mask."""
+    if FULL_MASK is not None:
+        code = ("import json, sys; sys.path.insert(0, %r); import bench, workloads; "
+                "print(json.dumps(bench._cpu_baseline_here(workloads.make(%r), %r, %d)))") % (
+                    str(ROOT), str(config), str(config), runs)
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True,
+                             preexec_fn=lambda: os.sched_setaffinity(0, FULL_MASK))
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    return _cpu_baseline_here(g, config, runs)
+
+
+def _cpu_baseline_here(g, config, runs=3):
     import oracle
 
     oracle.build()
@@ -358,7 +397,10 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": _config(args, g),
             "e2e": {"value": world * E * args.steps / e2e_total, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": 1e3 * e2e_total / args.steps},
+                    "ms_per_step": 1e3 * e2e_total / args.steps,
+                    "rank0_step_ms": {"min": 1e3 * min(e2e_s), "median": 1e3 * statistics.median(e2e_s),
+                                      "max": 1e3 * max(e2e_s)},
+                    "host_threads": PIN_NOTE},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
                          "frac": ach / hbm, "traffic": traffic, "peak_source": src,
                          "alg_bytes_per_launch": b, "gather_bound": gather_bound},
@@ -389,8 +431,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pin", action="store_true", help="our arm: leave the process unpinned")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
+    if args.impl == "ours" and not args.no_pin:
+        _pin_process(int(os.environ.get("LOCAL_RANK", 0)))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
