@@ -345,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
         lab = fast_bcc(gp, device=dev)
         e2e_s.append(time.perf_counter() - t0)
     e2e_total = replica_value(sum(e2e_s), world, E, args.steps, dist, dev)[1]
-    h2d = 8 * (n + 1) + 4 * m
+    h2d = (4 if getattr(gp, "_pinned_off32", None) is not None else 8) * (n + 1) + 4 * m  # as uploaded
     d2h = 4 * n + 4 * n + 4 * E + n + 64
 
     if rank == 0:

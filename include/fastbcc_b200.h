@@ -54,6 +54,8 @@ extern "C" {
 /* run flags */
 #define FBCC_FLAG_TIMING 1u   /* record per-stage CUDA-event times in stats   */
 #define FBCC_FLAG_PROFILE 2u  /* also bracket every launch with CUDA events   */
+#define FBCC_FLAG_HOST_OFFSETS32 4u  /* fbcc_run_host: io->offsets holds int32 offsets
+                                        (m < 2^31; half the upload, widened on the device) */
 #define FBCC_MAX_PROFILE 512
 
 /* Outputs of one run; all DEVICE pointers.  label/head are required. */
@@ -69,7 +71,8 @@ typedef struct {
 /* HOST buffers of fbcc_run_host.  Pinned (page-locked) memory lets the
    copies overlap the kernels; pageable memory works but serialises them. */
 typedef struct {
-  const int64_t *offsets; /* [n+1] symmetric CSR, as fbcc_run                 */
+  const int64_t *offsets; /* [n+1] symmetric CSR, as fbcc_run (int32 values
+                             with FBCC_FLAG_HOST_OFFSETS32)                    */
   const uint32_t *edges;  /* [m]                                              */
   int32_t *label;         /* [n] or NULL                                      */
   int32_t *head;          /* [n] or NULL                                      */

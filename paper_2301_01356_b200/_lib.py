@@ -22,6 +22,7 @@ FBCC_ERR_CYCLE = 5
 FBCC_ERR_COVER = 6
 FBCC_FLAG_TIMING = 1
 FBCC_FLAG_PROFILE = 2
+FBCC_FLAG_HOST_OFFSETS32 = 4
 FBCC_MAX_PROFILE = 512
 
 # every symbol the header declares (checked by tests/test_abi.py)

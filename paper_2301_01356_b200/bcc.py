@@ -280,9 +280,13 @@ class _HostRunner:
         import torch
 
         n, m = self.n, self.m
+        flags = _lib.FBCC_FLAG_TIMING
         if g._pinned is not None:
             off_h, adj_h = g._pinned
             off_p, adj_p = off_h.data_ptr(), adj_h.data_ptr()
+            if getattr(g, "_pinned_off32", None) is not None:  # int32 offsets: half the upload
+                off_p = g._pinned_off32.data_ptr()
+                flags |= _lib.FBCC_FLAG_HOST_OFFSETS32
         else:  # pageable: correct, but the copies cannot overlap the kernels
             off_p, adj_p = g.offsets.ctypes.data, g.edges.ctypes.data
         h = {"label": torch.empty(n, dtype=torch.int32, pin_memory=True),
@@ -295,7 +299,7 @@ class _HostRunner:
         s = torch.cuda.current_stream(self.dev)
         _lib.check(self.L.fbcc_run_host(ctypes.byref(io), n, m, self.off.data_ptr(), self.adj.data_ptr(),
                                         self.ws.data_ptr(), self.ws.numel(), ctypes.byref(self.outs),
-                                        ctypes.byref(st), ctypes.c_void_p(s.cuda_stream), _lib.FBCC_FLAG_TIMING))
+                                        ctypes.byref(st), ctypes.c_void_p(s.cuda_stream), flags))
         E = int(st.num_edges)
         return st, {k: v.numpy() for k, v in h.items()}, E
 

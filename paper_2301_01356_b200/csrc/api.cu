@@ -242,7 +242,8 @@ struct Pipeline {
   // the union-find hides under the H2D transfer.  label is copied back while
   // Stage 6 runs, head / is_ap while the per-edge labels are computed; only
   // the per-edge labels' own D2H trails the last kernel.
-  void enqueue_host(cudaStream_t st, cudaStream_t cs, const fbcc_host_io& io, cudaEvent_t* hev, int nchunk,
+  void enqueue_host(cudaStream_t st, cudaStream_t cs, const fbcc_host_io& io, bool host_off32, cudaEvent_t* hev,
+                    int nchunk,
                     cudaEvent_t* ev) {
     Marks mk{st, ev, false};
     cudaEvent_t ev_start = hev[0], ev_off = hev[1], ev_label = hev[2], ev_heads = hev[3], ev_copies = hev[4];
@@ -251,7 +252,15 @@ struct Pipeline {
     // the copies must not overwrite inputs a previous run on st still reads
     cudaEventRecord(ev_start, st);
     cudaStreamWaitEvent(cs, ev_start, 0);
-    cudaMemcpyAsync(const_cast<int64_t*>(g.off), io.offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, cs);
+    // int32 host offsets (FBCC_FLAG_HOST_OFFSETS32): half the bytes over
+    // PCIe, widened on the device from a workspace scratch area (the tour
+    // list's nexto, untouched until Stage 2)
+    int* off32 = host_off32 ? R.nexto : nullptr;
+    if (off32)
+      cudaMemcpyAsync(off32, io.offsets, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, cs);
+    else
+      cudaMemcpyAsync(const_cast<int64_t*>(g.off), io.offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice,
+                      cs);
     cudaEventRecord(ev_off, cs);
     const int64_t nq = (m + kItems - 1) / kItems;
     int64_t qb[kMaxStreamChunks + 1];
@@ -267,6 +276,7 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
+    if (off32) widen_offsets(off32, const_cast<int64_t*>(g.off), n, st);
     build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, nullptr, nullptr, nullptr, nlow);
     stage1_stream_begin(g, comp, st);
     for (int c = 0; c < nchunk; c++) {
@@ -482,7 +492,7 @@ int fbcc_run_host(const fbcc_host_io* io, int64_t n, int64_t m, int64_t* d_offse
   if (nchunk < 1) nchunk = 1;
   if (nchunk > kMaxStreamChunks) nchunk = kMaxStreamChunks;
   if (!log->profile) P.side = &g_hs.side;  // (profiled runs stay on one stream)
-  P.enqueue_host(st, g_hs.cs, *io, g_hs.ev, nchunk, timing ? ev : nullptr);
+  P.enqueue_host(st, g_hs.cs, *io, (flags & FBCC_FLAG_HOST_OFFSETS32) != 0, g_hs.ev, nchunk, timing ? ev : nullptr);
   g_log = nullptr;
   e = cudaGetLastError();
   Scalars host;

@@ -839,6 +839,17 @@ __global__ void k_super_rows(const int64_t* __restrict__ off, int n, int* flag) 
     if (__ldg(off + v + 1) - __ldg(off + v) > kSuperRow) *flag = 1;
 }
 
+__global__ void k_widen(const int* __restrict__ src, int64_t* __restrict__ dst, int64_t count) {
+  pdl_enter();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (int64_t)(uint32_t)__ldg(src + i);
+}
+
+void widen_offsets(const int* src, int64_t* dst, int64_t n, cudaStream_t st) {
+  launch(k_widen, grid_for(n + 1, 256), 256, 0, st, src, dst, n + 1);
+  note(K_IOTA);
+}
+
 bool graph_has_super_rows(const Graph& g, void* scratch4, cudaStream_t st) {
   int* d = (int*)scratch4;
   int h = 1;

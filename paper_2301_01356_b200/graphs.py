@@ -21,13 +21,14 @@ class Graph:
     :param edges: uint32[m] neighbour ids
     """
 
-    __slots__ = ("offsets", "edges", "_dev", "_pinned")
+    __slots__ = ("offsets", "edges", "_dev", "_pinned", "_pinned_off32")
 
     def __init__(self, offsets, edges, validate: bool = False):
         self.offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         self.edges = np.ascontiguousarray(edges, dtype=np.uint32)
         self._dev = None
         self._pinned = None
+        self._pinned_off32 = None
         if self.offsets.ndim != 1 or self.offsets.size == 0:
             raise ValueError("offsets must be a 1-d array of length n+1")
         if validate:
@@ -41,6 +42,10 @@ class Graph:
         if self._pinned is None and self._dev is None:
             self._pinned = (torch.from_numpy(self.offsets).pin_memory(),
                             torch.from_numpy(self.edges.view(np.int32)).pin_memory())
+            # the host path uploads int32 offsets (half the bytes; widened on
+            # the device) whenever the slot count fits 32 bits
+            if self.m < (1 << 31):
+                self._pinned_off32 = torch.from_numpy(self.offsets.astype(np.int32)).pin_memory()
         return self
 
     @classmethod
@@ -58,6 +63,7 @@ class Graph:
         g.edges = None
         g._dev = (offsets_t.contiguous(), edges_t.contiguous())
         g._pinned = None
+        g._pinned_off32 = None
         return g
 
     @property
