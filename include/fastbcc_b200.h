@@ -159,7 +159,8 @@ int fbcc_plan_destroy(fbcc_plan plan);
      4  higher-level splitter spacing (power of two >= 2; 8)
      8  bitmask of sampling rounds followed by a compress (0 = first + last; 0xFF)
     11  programmatic dependent launch (0/1; 1)
-    12  fbcc_run_host: arc ranges the edge upload is split into (1..64; 8)
+    12  fbcc_run_host: arc ranges the edge upload is split into, at most one per
+        2^21 arcs (1..64; 4)
     13  Stage 5: bitmask of rounds that also hook along plain parent edges (3);
         bit 7: round 0 along parent edges only (config 2 -0.6 %, 4a/4b +2 %: off)
     14  the last sampling compress also picks the giant (0/1; 1)
