@@ -225,3 +225,22 @@ def test_public_api_paths_match_reference(name, config_meta):
     gd = Graph.from_device(torch.from_numpy(g.offsets).cuda(), torch.from_numpy(g.edges.view(np.int32)).cuda())
     check(fast_bcc(gd))
     check(fast_bcc(gd, device_outputs=True))
+
+
+def test_host_offsets_widths_agree():
+    """fbcc_run_host with the int32 offsets Graph.pin() keeps
+    (FBCC_FLAG_HOST_OFFSETS32, widened on the device) and with the int64
+    reference offsets give identical outputs."""
+    import workloads
+    from paper_2301_01356_b200 import Graph, fast_bcc
+
+    for name in ("1", "3"):
+        g = workloads.make(name)
+        gp = Graph(g.offsets, g.edges).pin()
+        assert gp._pinned_off32 is not None
+        a = fast_bcc(gp)
+        gp._pinned_off32 = None  # int64 upload
+        b = fast_bcc(gp)
+        for k in ("label", "head", "edge_label", "is_ap"):
+            assert np.array_equal(getattr(a, k), getattr(b, k)), (name, k)
+        assert a.num_bccs == b.num_bccs and a.num_components == b.num_components
