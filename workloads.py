@@ -226,6 +226,83 @@ def make_device(name, device="cuda"):
     return symmetrize_device(u, v, n, device)
 
 
+# ---------------------------------------------------------------------------
+# Host CSR in seconds (tools/hostgen.c, OpenMP): the same PCG64 draws and the
+# same symmetrize() result as rmat() above, which takes minutes in numpy at
+# scale 25.  Bit-identity: tests/test_hostgen.py (small scales, vs rmat()) and
+# the committed config-5 CSR digest (tests/golden/configs.json).
+# ---------------------------------------------------------------------------
+def _hostgen_lib():
+    import ctypes
+    import subprocess
+    from pathlib import Path
+
+    tools = Path(__file__).resolve().parent / "tools"
+    so = tools / "libhostgen.so"
+    src = tools / "hostgen.c"
+    if not so.exists() or so.stat().st_mtime < src.stat().st_mtime:
+        tmp = so.with_suffix(".so.tmp")
+        subprocess.run(["gcc", "-O3", "-march=x86-64-v2", "-fopenmp", "-shared", "-fPIC", "-o", str(tmp), str(src)],
+                       check=True)
+        tmp.replace(so)
+    lib = ctypes.CDLL(str(so))
+    u64, i64, vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p
+    lib.hg_rmat_pairs.restype = ctypes.c_int
+    lib.hg_rmat_pairs.argtypes = [u64, u64, u64, u64, ctypes.c_int, i64, i64, vp, vp]
+    lib.hg_symmetrize.restype = i64
+    lib.hg_symmetrize.argtypes = [vp, vp, i64, i64, ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    lib.hg_free.restype = None
+    lib.hg_free.argtypes = [vp]
+    lib.hg_num_threads.restype = ctypes.c_int
+    return lib
+
+
+def _owned(lib, ptr, count, ctype, dtype):
+    """numpy view of a malloc'd buffer, freed with the array."""
+    import ctypes
+    import weakref
+
+    if count == 0:
+        lib.hg_free(ptr)
+        return np.empty(0, dtype)
+    arr = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctype)), shape=(count,)).view(dtype)
+    weakref.finalize(arr, lib.hg_free, ptr)
+    return arr
+
+
+def symmetrize_host(u, v, n: int) -> Graph:
+    """symmetrize() for uint32 pair arrays, on all host cores."""
+    import ctypes
+
+    lib = _hostgen_lib()
+    u = np.ascontiguousarray(u, np.uint32)
+    v = np.ascontiguousarray(v, np.uint32)
+    po, pe = ctypes.c_void_p(), ctypes.c_void_p()
+    m = lib.hg_symmetrize(u.ctypes.data, v.ctypes.data, u.size, n, ctypes.byref(po), ctypes.byref(pe))
+    if m < 0:
+        raise ValueError("edge endpoint out of range (or out of memory)")
+    off = _owned(lib, po.value, n + 1, ctypes.c_int64, np.int64)
+    edges = _owned(lib, pe.value, m, ctypes.c_uint32, np.uint32)
+    return Graph(off, edges)
+
+
+def rmat_fast(scale: int = 25, edge_factor: int = 16, seed: int = 0, chunk: int = 1 << 24) -> Graph:
+    """rmat() on all host cores (tools/hostgen.c): same pairs, same CSR."""
+    lib = _hostgen_lib()
+    st = np.random.PCG64(seed).state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    total = edge_factor * (1 << scale)
+    u = np.empty(total, np.uint32)
+    v = np.empty(total, np.uint32)
+    rc = lib.hg_rmat_pairs(s >> 64, s & m64, inc >> 64, inc & m64, scale, total, chunk, u.ctypes.data, v.ctypes.data)
+    if rc:
+        raise RuntimeError("hg_rmat_pairs failed")
+    g = symmetrize_host(u, v, 1 << scale)
+    del u, v
+    return g
+
+
 CONFIGS = {
     "1": ("torus 300x300 p=0.6", lambda: grid(300, 300, circular=True, keep_prob=0.6, seed=0)),
     "2": ("uniform n=2^20 m=8n", lambda: uniform()),
@@ -233,7 +310,7 @@ CONFIGS = {
     "4a": ("torus 10^4x10^4", lambda: grid(10**4, 10**4, circular=True)),
     "4b": ("torus 10^3x10^5 p=0.6", lambda: grid(10**3, 10**5, circular=True, keep_prob=0.6, seed=0)),
     "4c": ("chain 10^8", lambda: chain(10**8)),
-    "5": ("RMAT scale 25 ef 16", lambda: rmat()),
+    "5": ("RMAT scale 25 ef 16", lambda: rmat_fast()),
 }
 
 
