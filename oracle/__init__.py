@@ -68,6 +68,8 @@ def lib():
         L.orc_edge_labels.argtypes = [_I64, _P, _P, _P, _P, _P]
         L.orc_fast_bcc.restype = ctypes.c_int
         L.orc_fast_bcc.argtypes = [_I64, _P, _P, _P, _P, _P, _P, _P, _P]
+        L.orc_fast_bcc_mode.restype = ctypes.c_int
+        L.orc_fast_bcc_mode.argtypes = [_I64, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int]
         L.orc_num_threads.restype = ctypes.c_int
         L.orc_set_threads.argtypes = [ctypes.c_int]
         _LIB = L
@@ -199,9 +201,11 @@ def edge_labels(offsets, edges, label, head):
     return out[:E]
 
 
-def fast_bcc(offsets, edges):
+def fast_bcc(offsets, edges, parallel=False):
     """Whole pipeline: dict with label, head, is_ap, edge_label, num_bccs,
-    num_components, num_edges, seconds[5]."""
+    num_components, num_edges, seconds[5].  ``parallel``: the concurrent
+    union-find / splitter list-ranking variants (same outputs; the CPU
+    baseline's mode)."""
     off, adj, n = _csr(offsets, edges)
     label = np.empty(n, np.int32)
     head = np.empty(n, np.int32)
@@ -209,8 +213,8 @@ def fast_bcc(offsets, edges):
     el = np.empty(max(adj.size // 2, 1), np.int32)
     counts = np.zeros(3, np.int64)
     secs = np.zeros(5, np.float64)
-    rc = lib().orc_fast_bcc(n, _ptr(off), _ptr(adj), _ptr(label), _ptr(head),
-                            _ptr(is_ap), _ptr(el), _ptr(counts), _ptr(secs))
+    rc = lib().orc_fast_bcc_mode(n, _ptr(off), _ptr(adj), _ptr(label), _ptr(head),
+                                 _ptr(is_ap), _ptr(el), _ptr(counts), _ptr(secs), int(bool(parallel)))
     if rc:
         raise RuntimeError(f"oracle error {rc}")
     return dict(label=label, head=head, is_ap=is_ap,

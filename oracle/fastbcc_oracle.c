@@ -23,6 +23,13 @@
  * i.e. _union_batch over all arcs u<w.  Everything downstream consumes the
  * forest exactly as _rooted_from_claims does.
  *
+ * Two modes.  Sequential (orc_fast_bcc): the checker -- union-find and list
+ * ranking sequential as in the reference's _union_batch / _accumulate_chains.
+ * Parallel (orc_fast_bcc_mode(..., 1)): the CPU baseline -- every loop on all
+ * host cores, the union-find concurrent (CAS hooking) and the list ranking
+ * in the reference's splitter / walk / chain / scatter shape.  Both produce
+ * the same outputs (forest-independent, SURVEY §0 finding 2).
+ *
  * Parity is pinned by tests/test_oracle_golden.py against golden vectors
  * produced by running the reference itself (tests/golden/make_golden.py).
  */
@@ -161,15 +168,156 @@ int orc_list_ranking(int64_t L, const int32_t *nxt, int64_t nheads,
   return rc;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Parallel mode (orc_fast_bcc_mode(..., parallel=1)): the same outputs from */
+/* the reference's parallel structure.  The reference grows LDD clusters in   */
+/* parallel (connectivity.py:195-246) and unions the crossing arcs; here all  */
+/* arcs are unioned concurrently (CAS hooking larger root under smaller, the  */
+/* reference's link rule connectivity.py:302-305, so roots stay component     */
+/* minima).  The forest differs from the sequential one -- it is a spanning   */
+/* forest all the same, and every output downstream is forest-independent    */
+/* (SURVEY §0 finding 2; pinned by the golden tests in both modes).          */
+/* ------------------------------------------------------------------------ */
+static inline int32_t par_find(int32_t *p, int32_t x) {
+  for (;;) {
+    int32_t px = __atomic_load_n(&p[x], __ATOMIC_RELAXED);
+    if (px == x) return x;
+    int32_t gp = __atomic_load_n(&p[px], __ATOMIC_RELAXED);
+    if (gp != px) __atomic_store_n(&p[x], gp, __ATOMIC_RELAXED); /* path halving: an ancestor */
+    x = gp;
+  }
+}
+
+int64_t orc_cc_par(int64_t n, const int64_t *off, const uint32_t *adj,
+                   const int64_t *skel, int32_t *label, int32_t *forest_u,
+                   int32_t *forest_v, int64_t *fcount_out) {
+  int32_t *p = (int32_t *)malloc(sizeof(int32_t) * (n ? n : 1));
+  int32_t *hu = forest_u ? (int32_t *)malloc(sizeof(int32_t) * (n ? n : 1)) : NULL;
+  int32_t *hv = forest_u ? (int32_t *)malloc(sizeof(int32_t) * (n ? n : 1)) : NULL;
+  if (!p || (forest_u && (!hu || !hv))) { free(p); free(hu); free(hv); return -1; }
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; v++) { p[v] = (int32_t)v; if (hu) hu[v] = -1; }
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t u = 0; u < n; u++) {
+    for (int64_t s = off[u]; s < off[u + 1]; s++) {
+      int64_t w = adj[s];
+      if (u >= w) continue;
+      if (skel && !skel_kept(skel, u, w)) continue;
+      for (;;) {
+        int32_t ru = par_find(p, (int32_t)u), rw = par_find(p, (int32_t)w);
+        if (ru == rw) break;
+        int32_t hi = ru > rw ? ru : rw, lo = ru ^ rw ^ hi, exp = hi;
+        if (__atomic_compare_exchange_n(&p[hi], &exp, lo, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+          if (hu) { hu[hi] = (int32_t)u; hv[hi] = (int32_t)w; } /* one winner per hooked root */
+          break;
+        }
+      }
+    }
+  }
+  int64_t ncomp = 0;
+#pragma omp parallel for schedule(static) reduction(+ : ncomp)
+  for (int64_t v = 0; v < n; v++) {
+    label[v] = par_find(p, (int32_t)v);
+    ncomp += label[v] == v;
+  }
+  int64_t fcount = 0;
+  if (hu) {
+    for (int64_t v = 0; v < n; v++)
+      if (hu[v] >= 0) { forest_u[fcount] = hu[v]; forest_v[fcount] = hv[v]; fcount++; }
+  }
+  free(p); free(hu); free(hv);
+  if (fcount_out) *fcount_out = fcount;
+  return ncomp;
+}
+
+/*
+ * Parallel list ranking in the reference's shape (euler_tour.py:322-358):
+ * splitters = every head plus every cell i with i % S == 0 (the reference
+ * samples ~sqrt(L) at random, :337-343; ranks are exact either way), each
+ * splitter walks to the next one in parallel (_walk_segments :179-195), a
+ * sequential pass chains the splitters of each list (_accumulate_chains
+ * :198-218), and a parallel re-walk writes the ranks (_scatter_ranks
+ * :221-233).  For pipeline tours (valid by construction); the sequential
+ * orc_list_ranking keeps the reference's error classification.
+ */
+int orc_list_ranking_par(int64_t L, const int32_t *nxt, int64_t nheads,
+                         const int32_t *heads, int32_t *ranks) {
+  if (L == 0) return ORC_OK;
+  const int64_t S = 256;
+  int32_t *sid = (int32_t *)malloc(sizeof(int32_t) * L);
+  if (!sid) return ORC_ERR_NOMEM;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < L; i++) sid[i] = -1;
+  /* splitter ids: regular cells first, then heads not already splitters */
+  int64_t nreg = (L + S - 1) / S, ns = nreg;
+  for (int64_t i = 0; i < nreg; i++) sid[i * S] = (int32_t)i;
+  for (int64_t h = 0; h < nheads; h++)
+    if (heads[h] >= 0 && sid[heads[h]] < 0) sid[heads[h]] = (int32_t)ns++;
+  int32_t *scell = (int32_t *)malloc(sizeof(int32_t) * ns);
+  int32_t *snext = (int32_t *)malloc(sizeof(int32_t) * ns); /* next splitter id, -1 = end */
+  int64_t *slen = (int64_t *)malloc(sizeof(int64_t) * ns);
+  int64_t *sbase = (int64_t *)malloc(sizeof(int64_t) * ns);
+  if (!scell || !snext || !slen || !sbase) { free(sid); free(scell); free(snext); free(slen); free(sbase); return ORC_ERR_NOMEM; }
+  for (int64_t i = 0; i < nreg; i++) scell[i] = (int32_t)(i * S);
+  for (int64_t h = 0; h < nheads; h++)
+    if (heads[h] >= 0 && sid[heads[h]] >= nreg) scell[sid[heads[h]]] = heads[h];
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(| : bad)
+  for (int64_t j = 0; j < ns; j++) {
+    int64_t c = scell[j], len = 1;
+    int64_t x = nxt[c];
+    while (x >= 0 && sid[x] < 0) {
+      if (++len > L) { bad = 1; break; }
+      x = nxt[x];
+    }
+    slen[j] = len;
+    snext[j] = x >= 0 ? sid[x] : -1;
+    sbase[j] = -1;
+  }
+  if (bad) { free(sid); free(scell); free(snext); free(slen); free(sbase); return ORC_ERR_CYCLE; }
+  int64_t covered = 0;
+  for (int64_t h = 0; h < nheads && !bad; h++) {
+    if (heads[h] < 0) continue;
+    int64_t j = sid[heads[h]], r = 0;
+    while (j >= 0) {
+      if (sbase[j] >= 0) { bad = 1; break; }
+      sbase[j] = r;
+      r += slen[j];
+      covered += slen[j];
+      j = snext[j];
+    }
+  }
+  if (bad || covered != L) { free(sid); free(scell); free(snext); free(slen); free(sbase); return ORC_ERR_COVER; }
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t j = 0; j < ns; j++) {
+    int64_t c = scell[j], r = sbase[j];
+    ranks[c] = (int32_t)r;
+    int64_t x = nxt[c];
+    while (x >= 0 && sid[x] < 0) { ranks[x] = (int32_t)++r; x = nxt[x]; }
+  }
+  free(sid); free(scell); free(snext); free(slen); free(sbase);
+  return ORC_OK;
+}
+
 /*
  * Root a spanning forest at each component's minimum vertex
  * (_rooted_from_claims euler_tour.py:397-411 -> _rooted_from_csr 414-437).
  * Forest = k undirected pairs (forest_u[i], forest_v[i]); label = min-id
  * component labels.  Outputs parent (-1 at roots), first, last in [0, 2n).
  */
+static int root_forest(int64_t n, const int32_t *label, int64_t k,
+                       const int32_t *fu, const int32_t *fv, int32_t *parent,
+                       int32_t *first, int32_t *last, int parallel);
+
 int orc_root_forest(int64_t n, const int32_t *label, int64_t k,
                     const int32_t *fu, const int32_t *fv, int32_t *parent,
                     int32_t *first, int32_t *last) {
+  return root_forest(n, label, k, fu, fv, parent, first, last, 0);
+}
+
+static int root_forest(int64_t n, const int32_t *label, int64_t k,
+                       const int32_t *fu, const int32_t *fv, int32_t *parent,
+                       int32_t *first, int32_t *last, int parallel) {
   if (n == 0) return ORC_OK;
   int64_t L = 2 * k;
   int64_t *toff = (int64_t *)calloc(n + 1, sizeof(int64_t));
@@ -187,12 +335,30 @@ int orc_root_forest(int64_t n, const int32_t *label, int64_t k,
     goto done;
   }
   /* tree CSR by counting sort of directed slots (_tree_csr euler_tour.py:68-89) */
-  for (int64_t i = 0; i < k; i++) { toff[fu[i] + 1]++; toff[fv[i] + 1]++; }
-  for (int64_t v = 0; v < n; v++) { toff[v + 1] += toff[v]; cur[v] = toff[v]; }
-  for (int64_t i = 0; i < k; i++) {
-    int64_t su = cur[fu[i]]++, sv = cur[fv[i]]++;
-    tedges[su] = fv[i]; tedges[sv] = fu[i];
-    twin[su] = (int32_t)sv; twin[sv] = (int32_t)su;
+  if (parallel) {
+    /* concurrent counting sort: slot order within a row differs, which only
+       re-orders the Euler circuit -- positions stay a valid tour */
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < k; i++) {
+      __atomic_fetch_add(&toff[fu[i] + 1], 1, __ATOMIC_RELAXED);
+      __atomic_fetch_add(&toff[fv[i] + 1], 1, __ATOMIC_RELAXED);
+    }
+    for (int64_t v = 0; v < n; v++) { toff[v + 1] += toff[v]; cur[v] = toff[v]; }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < k; i++) {
+      int64_t su = __atomic_fetch_add(&cur[fu[i]], 1, __ATOMIC_RELAXED);
+      int64_t sv = __atomic_fetch_add(&cur[fv[i]], 1, __ATOMIC_RELAXED);
+      tedges[su] = fv[i]; tedges[sv] = fu[i];
+      twin[su] = (int32_t)sv; twin[sv] = (int32_t)su;
+    }
+  } else {
+    for (int64_t i = 0; i < k; i++) { toff[fu[i] + 1]++; toff[fv[i] + 1]++; }
+    for (int64_t v = 0; v < n; v++) { toff[v + 1] += toff[v]; cur[v] = toff[v]; }
+    for (int64_t i = 0; i < k; i++) {
+      int64_t su = cur[fu[i]]++, sv = cur[fv[i]]++;
+      tedges[su] = fv[i]; tedges[sv] = fu[i];
+      twin[su] = (int32_t)sv; twin[sv] = (int32_t)su;
+    }
   }
   /* Euler circuit: incoming slot i of v -> outgoing slot i+1 (_link_circuit :134-145) */
 #pragma omp parallel for schedule(static)
@@ -208,10 +374,16 @@ int orc_root_forest(int64_t n, const int32_t *label, int64_t k,
     if (d == 0) heads[nroots++] = -1;
     else { nxt[twin[b + d - 1]] = -1; heads[nroots++] = (int32_t)b; }
   }
-  rc = orc_list_ranking(L, nxt, nroots, heads, ranks);
+  rc = parallel ? orc_list_ranking_par(L, nxt, nroots, heads, ranks)
+                : orc_list_ranking(L, nxt, nroots, heads, ranks);
   if (rc != ORC_OK) goto done;
   /* per-tree base = sum of 2*size over trees with smaller root (_tree_bases :250-259) */
-  for (int64_t v = 0; v < n; v++) sizes[label[v]]++;
+  if (parallel) {
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < n; v++) __atomic_fetch_add(&sizes[label[v]], 1, __ATOMIC_RELAXED);
+  } else {
+    for (int64_t v = 0; v < n; v++) sizes[label[v]]++;
+  }
   {
     int64_t acc = 0;
     for (int64_t v = 0; v < n; v++)
@@ -429,15 +601,99 @@ int64_t orc_edge_labels(int64_t n, const int64_t *off, const uint32_t *adj,
   return e;
 }
 
+/* parallel mode: _component_heads by an atomic min of (first << 32 | v) per label */
+static void component_heads_par(int64_t n, const int32_t *label, const int32_t *parent,
+                                const int32_t *first, int32_t *head) {
+  int64_t *best = (int64_t *)malloc(sizeof(int64_t) * (n ? n : 1));
+  const int64_t BIG = (int64_t)1 << 62;
+#pragma omp parallel for schedule(static)
+  for (int64_t l = 0; l < n; l++) { best[l] = BIG; head[l] = -1; }
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; v++) {
+    int64_t pk = ((int64_t)first[v] << 32) | v, cur = __atomic_load_n(&best[label[v]], __ATOMIC_RELAXED);
+    while (pk < cur && !__atomic_compare_exchange_n(&best[label[v]], &cur, pk, 1, __ATOMIC_RELAXED,
+                                                     __ATOMIC_RELAXED)) {
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t l = 0; l < n; l++)
+    if (best[l] != BIG) head[l] = parent[best[l] & 0xFFFFFFFFLL];
+  free(best);
+}
+
+static void articulation_par(int64_t n, const int32_t *label, const int32_t *head, uint8_t *is_ap) {
+  int32_t *headed = (int32_t *)calloc(n ? n : 1, sizeof(int32_t));
+#pragma omp parallel for schedule(static)
+  for (int64_t l = 0; l < n; l++)
+    if (head[l] != -1) __atomic_fetch_add(&headed[head[l]], 1, __ATOMIC_RELAXED);
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < n; v++) {
+    int root = (label[v] == v) && (head[v] == -1);
+    is_ap[v] = (uint8_t)(root ? headed[v] >= 2 : headed[v] >= 1);
+  }
+  free(headed);
+}
+
+/* orc_edge_labels with edge ids from a prefix of per-row upper-arc counts */
+static int64_t edge_labels_par(int64_t n, const int64_t *off, const uint32_t *adj, const int32_t *label,
+                               const int32_t *head, int32_t *edge_label) {
+  int32_t *bmin = (int32_t *)malloc(sizeof(int32_t) * (n ? n : 1));
+  int64_t *ebase = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+#pragma omp parallel for schedule(static)
+  for (int64_t u = 0; u < n; u++) {
+    bmin[u] = 0x7FFFFFFF;
+    /* rows are sorted: the upper arcs are the tail after the last target <= u */
+    int64_t lo = off[u], hi = off[u + 1];
+    while (lo < hi) {
+      int64_t mid = (lo + hi) / 2;
+      if (adj[mid] <= u) lo = mid + 1; else hi = mid;
+    }
+    ebase[u + 1] = off[u + 1] - lo;
+  }
+  ebase[0] = 0;
+  for (int64_t u = 0; u < n; u++) ebase[u + 1] += ebase[u];
+  const int64_t E = ebase[n];
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t u = 0; u < n; u++) {
+    int64_t e = ebase[u], s0 = off[u + 1] - (ebase[u + 1] - ebase[u]);
+    for (int64_t s = s0; s < off[u + 1]; s++, e++) {
+      int64_t w = adj[s];
+      int32_t lu = label[u], lw = label[w];
+      int32_t blk = (lu == lw) ? lu : (head[lw] == u ? lw : lu);
+      edge_label[e] = blk;
+      int32_t cur = __atomic_load_n(&bmin[blk], __ATOMIC_RELAXED);
+      while (e < cur && !__atomic_compare_exchange_n(&bmin[blk], &cur, (int32_t)e, 1, __ATOMIC_RELAXED,
+                                                      __ATOMIC_RELAXED)) {
+      }
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < E; i++) edge_label[i] = bmin[edge_label[i]];
+  free(bmin);
+  free(ebase);
+  return E;
+}
+
 /*
  * The whole pipeline (fast_bcc bcc.py:147-196) plus the derived outputs.
  * label/head/is_ap sized n; edge_label sized E (may be NULL).
  * out_counts[0] = num_bccs, [1] = num_components, [2] = E.
  * seconds[0..4] = first_cc, rooting, tagging, last_cc, labelling (may be NULL).
  */
+int orc_fast_bcc_mode(int64_t n, const int64_t *off, const uint32_t *adj,
+                      int32_t *label, int32_t *head, uint8_t *is_ap,
+                      int32_t *edge_label, int64_t *out_counts, double *seconds, int parallel);
+
 int orc_fast_bcc(int64_t n, const int64_t *off, const uint32_t *adj,
                  int32_t *label, int32_t *head, uint8_t *is_ap,
                  int32_t *edge_label, int64_t *out_counts, double *seconds) {
+  return orc_fast_bcc_mode(n, off, adj, label, head, is_ap, edge_label, out_counts, seconds, 0);
+}
+
+/* parallel != 0: the parallel variants above (same outputs, all host cores) */
+int orc_fast_bcc_mode(int64_t n, const int64_t *off, const uint32_t *adj,
+                      int32_t *label, int32_t *head, uint8_t *is_ap,
+                      int32_t *edge_label, int64_t *out_counts, double *seconds, int parallel) {
   out_counts[0] = out_counts[1] = out_counts[2] = 0;
   if (n == 0) return ORC_OK;
   int rc = ORC_OK;
@@ -463,9 +719,11 @@ int orc_fast_bcc(int64_t n, const int64_t *off, const uint32_t *adj,
 #endif
     t0 = NOW();
     int64_t k = 0;
-    int64_t ncomp = orc_cc(n, off, adj, NULL, NULL, lab1, fu, fv, &k);
+    int64_t ncomp = parallel ? orc_cc_par(n, off, adj, NULL, lab1, fu, fv, &k)
+                             : orc_cc(n, off, adj, NULL, NULL, lab1, fu, fv, &k);
+    if (ncomp < 0) { rc = ORC_ERR_NOMEM; goto done; }
     t1 = NOW(); if (seconds) seconds[0] = t1 - t0; t0 = t1;
-    rc = orc_root_forest(n, lab1, k, fu, fv, parent, first, last);
+    rc = root_forest(n, lab1, k, fu, fv, parent, first, last, parallel);
     if (rc != ORC_OK) goto done;
     t1 = NOW(); if (seconds) seconds[1] = t1 - t0; t0 = t1;
     orc_compute_w(n, off, adj, parent, first, w1, w2);
@@ -473,14 +731,24 @@ int orc_fast_bcc(int64_t n, const int64_t *off, const uint32_t *adj,
     if (rc != ORC_OK) goto done;
     t1 = NOW(); if (seconds) seconds[2] = t1 - t0; t0 = t1;
     orc_pack_skeleton(n, parent, first, last, low, high, skel);
-    orc_cc(n, off, adj, NULL, skel, label, NULL, NULL, NULL);
-    orc_component_heads(n, label, parent, first, head);
+    if (parallel) {
+      if (orc_cc_par(n, off, adj, skel, label, NULL, NULL, NULL) < 0) { rc = ORC_ERR_NOMEM; goto done; }
+      component_heads_par(n, label, parent, first, head);
+    } else {
+      orc_cc(n, off, adj, NULL, skel, label, NULL, NULL, NULL);
+      orc_component_heads(n, label, parent, first, head);
+    }
     int64_t nb = 0;
+#pragma omp parallel for schedule(static) reduction(+ : nb)
     for (int64_t l = 0; l < n; l++) nb += head[l] != -1;
     t1 = NOW(); if (seconds) seconds[3] = t1 - t0; t0 = t1;
-    if (is_ap) orc_articulation(n, label, head, is_ap);
+    if (is_ap) {
+      if (parallel) articulation_par(n, label, head, is_ap);
+      else orc_articulation(n, label, head, is_ap);
+    }
     int64_t E = 0;
-    if (edge_label) E = orc_edge_labels(n, off, adj, label, head, edge_label);
+    if (edge_label) E = parallel ? edge_labels_par(n, off, adj, label, head, edge_label)
+                                 : orc_edge_labels(n, off, adj, label, head, edge_label);
     else E = off[n] / 2;
     t1 = NOW(); if (seconds) seconds[4] = t1 - t0;
     out_counts[0] = nb;

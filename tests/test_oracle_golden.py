@@ -51,9 +51,12 @@ def test_tags_and_fence_on_reference_forest(corpus, oracle_mod):
         assert np.array_equal((skel[:, 1] & 1).astype(np.uint8), corpus.get(i, "fence")), name
 
 
-def test_fast_bcc_matches_reference(corpus, oracle_mod):
+@pytest.mark.parametrize("parallel", [False, True])
+def test_fast_bcc_matches_reference(corpus, oracle_mod, parallel):
+    """Both oracle modes: sequential (the checker) and parallel (the CPU
+    baseline: concurrent union-find, splitter list ranking)."""
     for i, name, g in corpus.items():
-        r = oracle_mod.fast_bcc(g.offsets, g.edges)
+        r = oracle_mod.fast_bcc(g.offsets, g.edges, parallel=parallel)
         assert np.array_equal(r["label"], corpus.get(i, "label")), name
         assert np.array_equal(r["head"], corpus.get(i, "head")), name
         assert r["num_bccs"] == corpus.get(i, "num_bccs") == corpus.get(i, "ht_num_bccs"), name
@@ -133,16 +136,17 @@ def _sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("name", ["2", "3"])
-def test_config_digests(oracle_mod, config_meta, name):
-    """Configs 2-3 at full size: the oracle reproduces the reference's
-    outputs bit for bit (sha256 of label/head/is_ap/edge_label)."""
+@pytest.mark.parametrize("name,parallel", [("2", False), ("3", False), ("1", True), ("2", True), ("3", True)])
+def test_config_digests(oracle_mod, config_meta, name, parallel):
+    """Configs 1-3 at full size: the oracle reproduces the reference's
+    outputs bit for bit (sha256 of label/head/is_ap/edge_label), in both
+    modes."""
     import workloads
 
     g = workloads.make(name)
     meta = config_meta[name]
     assert workloads.csr_digest(g) == meta["csr_sha256"]
-    r = oracle_mod.fast_bcc(g.offsets, g.edges)
+    r = oracle_mod.fast_bcc(g.offsets, g.edges, parallel=parallel)
     assert r["num_bccs"] == meta["num_bccs"]
     assert r["num_components"] == meta["num_components"]
     assert _sha(r["label"]) == meta["label_sha256"]
