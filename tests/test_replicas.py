@@ -66,3 +66,13 @@ def test_reference_arm_json_line():
         assert k in line, k
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
     assert line["value"] > 0
+
+
+def test_bench_spawns_n_ranks():
+    """``bench.py --gpus 2`` outside torchrun re-launches itself as 2 ranks
+    (gloo here, NCCL on a GPU box) -- the replica bench's process plumbing."""
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--check-ranks"],
+                         capture_output=True, text=True, timeout=300, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["ranks"] == 2 and line["allreduce_sum"] == 2.0

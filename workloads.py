@@ -307,9 +307,10 @@ CONFIGS = {
     "1": ("torus 300x300 p=0.6", lambda: grid(300, 300, circular=True, keep_prob=0.6, seed=0)),
     "2": ("uniform n=2^20 m=8n", lambda: uniform()),
     "3": ("2-D kNN 10^6 k=5", lambda: knn2d()),
-    "4a": ("torus 10^4x10^4", lambda: grid(10**4, 10**4, circular=True)),
-    "4b": ("torus 10^3x10^5 p=0.6", lambda: grid(10**3, 10**5, circular=True, keep_prob=0.6, seed=0)),
-    "4c": ("chain 10^8", lambda: chain(10**8)),
+    # the same pairs as grid() / chain() (workloads._pairs), symmetrised on the host cores
+    "4a": ("torus 10^4x10^4", lambda: symmetrize_host(*_pairs("4a"))),
+    "4b": ("torus 10^3x10^5 p=0.6", lambda: symmetrize_host(*_pairs("4b"))),
+    "4c": ("chain 10^8", lambda: symmetrize_host(*_pairs("4c"))),
     "5": ("RMAT scale 25 ef 16", lambda: rmat_fast()),
 }
 
