@@ -135,7 +135,10 @@ int fbcc_run(const int64_t *offsets, const uint32_t *edges, int64_t n,
    results as fbcc_run).  The graph records the six stage boundaries as event
    nodes (stats.stage_ms after each run); with FBCC_FLAG_PROFILE it also
    records one event node after every kernel (stats.prof_*).  The bound
-   buffers must stay valid until fbcc_plan_destroy. */
+   buffers must stay valid until fbcc_plan_destroy.  A plan depends on the
+   buffers, not on their contents: the caller may refill them with another
+   graph of the same n and m between replays.  It freezes the options in
+   force when it was created. */
 typedef struct fbcc_plan_s *fbcc_plan;
 int fbcc_plan_create(const int64_t *offsets, const uint32_t *edges, int64_t n,
                      int64_t m, void *workspace, size_t workspace_bytes,
@@ -150,9 +153,12 @@ int fbcc_plan_launch(fbcc_plan plan, void *stream);
 int fbcc_plan_stats(fbcc_plan plan, fbcc_stats *stats);
 int fbcc_plan_destroy(fbcc_plan plan);
 
-/* Process-wide tuning knobs (result-neutral, like the reference's beta /
+/* Process-wide tuning defaults (result-neutral, like the reference's beta /
    block / seed, bcc.py:147-155; every setting gives identical outputs,
-   tests/test_gpu_mid.py::test_mid_graph_option_paths).  Keys:
+   tests/test_gpu_mid.py::test_mid_graph_option_paths).  Thread-safe: each
+   call (fbcc_run, fbcc_run_host, an op) and each plan snapshots the defaults
+   once and runs with its own copy, so a concurrent fbcc_set_option never
+   changes a run in flight.  Keys 3/4 change fbcc_workspace_bytes.  Keys:
      0  sampling rounds always run (0..8; default 2)
      1  giant-component skip in the remaining-arc link pass (0/1; 1)
      3  level-0 list-ranking splitter spacing (power of two >= 2; 16)

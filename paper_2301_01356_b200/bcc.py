@@ -29,18 +29,20 @@ from .graphs import Graph
 class StepTimings:
     """Seconds per pipeline step (bcc.py:78-95), from CUDA events.
 
-    ``first_cc`` = Stage 1, ``rooting`` = Stage 2, ``tagging`` = Stage 3,
-    ``last_cc`` = Stages 4+5 (fence + skeleton connectivity), ``labelling`` =
-    Stage 6 (heads, articulation flags, edge labels -- outside the reference's
-    timed region), ``total`` = all six.  ``stage_ms`` has the six raw values.
+    The first five fields are the reference's, in its order (positional
+    construction works the same): ``first_cc`` = Stage 1, ``rooting`` =
+    Stage 2, ``tagging`` = Stage 3, ``last_cc`` = Stages 4+5 (fence +
+    skeleton connectivity), ``total`` = all six stages.  Appended:
+    ``labelling`` = Stage 6 (heads, articulation flags, edge labels -- outside
+    the reference's timed region) and ``stage_ms``, the six raw values.
     """
 
     first_cc: float = 0.0
     rooting: float = 0.0
     tagging: float = 0.0
     last_cc: float = 0.0
-    labelling: float = 0.0
     total: float = 0.0
+    labelling: float = 0.0
     stage_ms: tuple = field(default_factory=tuple)
 
     def as_dict(self) -> dict:
@@ -113,6 +115,17 @@ def _workspace(nbytes: int, device):
     return buf
 
 
+def _as_graph(g) -> Graph:
+    """Accept the reference's ``Graph`` (``__slots__ = ("offsets", "edges")``,
+    graphs.py:43-58) or any object with those two arrays: wrapped without a
+    copy when they already are contiguous int64 / uint32."""
+    if isinstance(g, Graph):
+        return g
+    if hasattr(g, "offsets") and hasattr(g, "edges"):
+        return Graph(g.offsets, g.edges)
+    raise TypeError("expected a Graph (offsets int64[n+1], edges uint32[m])")
+
+
 def _device_csr(g: Graph, device):
     import torch
 
@@ -181,7 +194,12 @@ def run_device(off, adj, *, edge_labels=True, articulation=True, timing=True, de
 class Plan:
     """A CUDA-graph replay of the six stages bound to device tensors
     (``fbcc_plan_*`` in the C ABI).  ``run()`` launches the graph, waits and
-    returns the counts; outputs land in ``self.label`` etc."""
+    returns the counts; outputs land in ``self.label`` etc.
+
+    A plan is bound to the input *buffers* (pointers, n, m) and freezes the
+    options in force at its creation; it does not depend on the buffers'
+    contents, so refilling them with another graph of the same size and
+    replaying is correct."""
 
     def __init__(self, off, adj, *, edge_labels=True, articulation=True, profile=False, timing=False):
         import torch
@@ -246,7 +264,8 @@ _SESSIONS = {}
 
 def _session(g: Graph, dev) -> Plan:
     """A graph-replay plan bound to a device-resident input (keyed by its
-    buffers), reused across calls."""
+    buffers), reused across calls -- safe when the caller rewrites the
+    buffers in between (plans are content-independent, see Plan)."""
     off, adj, _ = _device_csr(g, dev)
     key = ("dev", off.data_ptr(), adj.data_ptr(), g.n, g.m)
     plan = _SESSIONS.get(key)
@@ -344,6 +363,7 @@ def fast_bcc(g: Graph, *, beta: float | None = None, seed: int = 0, block: int =
 
     t_start = time.perf_counter()
     _check_knobs(beta, block)
+    g = _as_graph(g)
     n = g.n
     if n and 2 * n > (1 << 31) - 1:
         raise ValueError("tour positions need n <= 2**30")
@@ -384,8 +404,8 @@ def fast_bcc(g: Graph, *, beta: float | None = None, seed: int = 0, block: int =
 def _timings(stats) -> StepTimings:
     ms = [float(x) for x in stats.stage_ms]
     return StepTimings(first_cc=ms[0] / 1e3, rooting=ms[1] / 1e3, tagging=ms[2] / 1e3,
-                       last_cc=(ms[3] + ms[4]) / 1e3, labelling=ms[5] / 1e3,
-                       total=float(stats.total_ms) / 1e3, stage_ms=tuple(ms))
+                       last_cc=(ms[3] + ms[4]) / 1e3, total=float(stats.total_ms) / 1e3,
+                       labelling=ms[5] / 1e3, stage_ms=tuple(ms))
 
 
 def _pinned_or_numpy(g: Graph):

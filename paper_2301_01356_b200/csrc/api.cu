@@ -1,6 +1,7 @@
 // api.cu -- the C ABI (include/fastbcc_b200.h): workspace layout, the
 // six-stage orchestration of fast_bcc (bcc.py:147-196) on one stream, and
 // CUDA-graph plans that replay the whole launch sequence.
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 
@@ -18,14 +19,16 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "chunk_rows", "hook_min", "iota", "propose", "accept", "compress", "find_giant", "link_rows", "link_heavy",
     "root_flags", "scan", "root_list", "out_lists", "link_tour", "walk0", "walk_level", "final_rank", "expand", "rank0",
     "positions", "firsts", "w_gather", "tile", "table", "fence", "heads", "count_blocks", "ap", "set_edges",
-    "edge_blocks", "edge_final", "memset", "export"};
+    "edge_blocks", "edge_final", "memset", "export", "widen"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
   return FBCC_ERR_CUDA;
 }
 
-int g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*giant skip*/ 1, /*retired*/ 0, /*S0*/ 16, /*SL*/ 8,
+// process-wide defaults (fbcc_set_option; atomic: the setter may race an
+// enqueue on another thread -- every enqueue works from its own snapshot)
+static std::atomic<int> g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*giant skip*/ 1, /*retired*/ 0, /*S0*/ 16, /*SL*/ 8,
                       /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last; all rounds: 4b -13%, config 3 -2%*/ 0xFF,
                       /*retired*/ 0, /*retired*/ 0,
                       /*programmatic dependent launch (dependents launch as the previous grid exits)*/ 1,
@@ -34,6 +37,16 @@ int g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*giant skip*/ 1, /*reti
                       /*warp-staged edge-block pass with the giant bitmap*/ 1,
                       /*... plus adaptive rounds up to (skip_round)*/ 3, /*Stage 5 cap (0: same)*/ 0,
                       /*accept folded into the following compress (config 2 +3.8 %, 4b -3.6 %: off)*/ 0, 0};
+thread_local const Options* t_opt = nullptr;
+
+int option_default(int key) { return g_opt[key].load(std::memory_order_relaxed); }
+
+Options options_snapshot() {
+  Options o;
+  for (int k = 0; k < OPT_NUM; k++) o.v[k] = g_opt[k].load(std::memory_order_relaxed);
+  return o;
+}
+
 constexpr int kFinalMaxHost = kFinalMax;
 constexpr int kMaxStreamChunks = 64;
 
@@ -54,9 +67,9 @@ struct Layout {
     return at;
   }
 
-  explicit Layout(int64_t n, int64_t m) {
+  explicit Layout(int64_t n, int64_t m, const Options& o) {
     const int64_t N0 = 2 * n;
-    const int kS0 = g_opt[OPT_S0], kSl = g_opt[OPT_SL];
+    const int kS0 = o.v[OPT_S0], kSl = o.v[OPT_SL];
     S[0] = kS0;
     K[1] = (N0 + kS0 - 1) / kS0;
     nlev = 1;
@@ -109,6 +122,7 @@ struct Layout {
 
 // One bound instance of the pipeline: graph, workspace carve-up, outputs.
 struct Pipeline {
+  Options opts;  // snapshot taken at creation; every enqueue runs under it
   Graph g;
   Layout lay;
   Scalars* sc;
@@ -128,8 +142,8 @@ struct Pipeline {
   bool w0_valid = false;
 
   Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
-           const fbcc_outputs* o)
-      : lay(n, m) {
+           const fbcc_outputs* o, const Options& op)
+      : opts(op), lay(n, m, op) {
     out = *o;
     char* ws = (char*)workspace;
     auto at = [&](size_t off) { return (void*)(ws + off); };
@@ -184,6 +198,7 @@ struct Pipeline {
 
   // Enqueue all six stages.  ev (7 events) brackets the stages when given.
   void enqueue(cudaStream_t st, cudaEvent_t* ev, int* low_out, int* high_out, bool capturing = false) {
+    OptScope scope(&opts);
     Marks mk{st, ev, capturing};
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
@@ -245,6 +260,7 @@ struct Pipeline {
   void enqueue_host(cudaStream_t st, cudaStream_t cs, const fbcc_host_io& io, bool host_off32, cudaEvent_t* hev,
                     int nchunk,
                     cudaEvent_t* ev) {
+    OptScope scope(&opts);
     Marks mk{st, ev, false};
     cudaEvent_t ev_start = hev[0], ev_off = hev[1], ev_label = hev[2], ev_heads = hev[3], ev_copies = hev[4];
     cudaEvent_t* ev_chunk = hev + 5;
@@ -323,11 +339,11 @@ int fbcc_set_option(int key, int value) {
   if ((key == OPT_S0 || key == OPT_SL) && (value < 2 || (value & (value - 1)))) return FBCC_ERR_ARG;
   if (key == OPT_SAMPLE_ROUNDS && (value < 0 || value > 8)) return FBCC_ERR_ARG;
   if (key == OPT_STREAM_CHUNKS && (value < 1 || value > kMaxStreamChunks)) return FBCC_ERR_ARG;
-  g_opt[key] = value;
+  g_opt[key].store(value, std::memory_order_relaxed);
   return FBCC_OK;
 }
 
-int fbcc_get_option(int key) { return (key >= 0 && key < OPT_NUM) ? g_opt[key] : -1; }
+int fbcc_get_option(int key) { return (key >= 0 && key < OPT_NUM) ? g_opt[key].load(std::memory_order_relaxed) : -1; }
 
 const char* fbcc_last_cuda_error(void) { return g_cuda_err; }
 
@@ -358,13 +374,13 @@ static int check_sizes(int64_t n, int64_t m) {
 }
 
 static int check_args(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
-                      size_t workspace_bytes, const fbcc_outputs* out) {
+                      size_t workspace_bytes, const fbcc_outputs* out, const Options& o) {
   int rc = check_sizes(n, m);
   if (rc) return rc;
   if (!out || !offsets || (m > 0 && !edges)) return FBCC_ERR_ARG;
   if (n == 0) return FBCC_OK;
   if (!out->label || !out->head || !workspace) return FBCC_ERR_ARG;
-  Layout lay(n, m);
+  Layout lay(n, m, o);
   if (workspace_bytes < lay.total) return FBCC_ERR_WORKSPACE;
   return FBCC_OK;
 }
@@ -373,7 +389,7 @@ int fbcc_workspace_bytes(int64_t n, int64_t m, size_t* bytes_out) {
   if (!bytes_out) return FBCC_ERR_ARG;
   int rc = check_sizes(n, m);
   if (rc) return rc;
-  Layout lay(n, m);
+  Layout lay(n, m, options_snapshot());
   *bytes_out = lay.total;
   return FBCC_OK;
 }
@@ -396,12 +412,13 @@ static void fill_profile(fbcc_stats* stats, const LaunchLog& log) {
 int fbcc_run(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
              size_t workspace_bytes, fbcc_outputs* out, fbcc_debug* dbg, fbcc_stats* stats, void* stream,
              uint32_t flags) {
-  int rc = check_args(offsets, edges, n, m, workspace, workspace_bytes, out);
+  const Options opts = options_snapshot();
+  int rc = check_args(offsets, edges, n, m, workspace, workspace_bytes, out, opts);
   if (rc) return rc;
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n == 0) return FBCC_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  Pipeline P(offsets, edges, n, m, workspace, out);
+  Pipeline P(offsets, edges, n, m, workspace, out, opts);
 
   const bool timing = (flags & FBCC_FLAG_TIMING) && stats;
   cudaEvent_t ev[7];
@@ -472,14 +489,15 @@ int fbcc_run_host(const fbcc_host_io* io, int64_t n, int64_t m, int64_t* d_offse
                   void* workspace, size_t workspace_bytes, fbcc_outputs* out, fbcc_stats* stats, void* stream,
                   uint32_t flags) {
   if (!io || !io->offsets || (m > 0 && !io->edges)) return FBCC_ERR_ARG;
-  int rc = check_args(d_offsets, d_edges, n, m, workspace, workspace_bytes, out);
+  const Options opts = options_snapshot();
+  int rc = check_args(d_offsets, d_edges, n, m, workspace, workspace_bytes, out, opts);
   if (rc) return rc;
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n == 0) return FBCC_OK;
   cudaError_t e = host_streams();
   if (e != cudaSuccess) return cuda_fail(e, "run_host streams");
   cudaStream_t st = (cudaStream_t)stream;
-  Pipeline P(d_offsets, d_edges, n, m, workspace, out);
+  Pipeline P(d_offsets, d_edges, n, m, workspace, out, opts);
   const bool timing = (flags & FBCC_FLAG_TIMING) && stats;
   cudaEvent_t ev[7];
   if (timing)
@@ -491,7 +509,7 @@ int fbcc_run_host(const fbcc_host_io* io, int64_t n, int64_t m, int64_t* d_offse
   // upload ranges: at most the option (default 4), and one per 2^21 arcs --
   // each range costs a fixed link launch and event hop (configs 1/2/3: 1/4/2
   // ranges measured best; 8 was 25 %, 1 %, 5 % slower)
-  int nchunk = g_opt[OPT_STREAM_CHUNKS];
+  int nchunk = opts.v[OPT_STREAM_CHUNKS];
   if (nchunk > (int)(m >> 21)) nchunk = (int)(m >> 21);
   if (nchunk < 1) nchunk = 1;
   if (nchunk > kMaxStreamChunks) nchunk = kMaxStreamChunks;
@@ -523,11 +541,14 @@ int fbcc_plan_create(const int64_t* offsets, const uint32_t* edges, int64_t n, i
                      size_t workspace_bytes, const fbcc_outputs* out, uint32_t flags, fbcc_plan* plan_out) {
   if (!plan_out) return FBCC_ERR_ARG;
   *plan_out = nullptr;
-  int rc = check_args(offsets, edges, n, m, workspace, workspace_bytes, out);
+  // a plan freezes the options in force at its creation (and is bound to
+  // the buffers it was created on -- not to their contents)
+  const Options opts = options_snapshot();
+  int rc = check_args(offsets, edges, n, m, workspace, workspace_bytes, out, opts);
   if (rc) return rc;
   fbcc_plan p = new fbcc_plan_s();
   if (n > 0) {
-    p->pipe = new Pipeline(offsets, edges, n, m, workspace, out);
+    p->pipe = new Pipeline(offsets, edges, n, m, workspace, out, opts);
     cudaStream_t cap;
     cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
     cudaGraph_t graph = nullptr;
@@ -547,9 +568,6 @@ int fbcc_plan_create(const int64_t* offsets, const uint32_t* edges, int64_t n, i
     for (int i = 0; i < 4 && use_side && e == cudaSuccess; i++)
       e = cudaEventCreateWithFlags(&side.ev[i], cudaEventDisableTiming);
     if (use_side && e == cudaSuccess) p->pipe->side = &side;
-    // the plan is replayed many times: one query decides whether the
-    // super-heavy link pass is needed at all (two launches fewer on most graphs)
-    if (e == cudaSuccess && m > 0) p->pipe->g.no_super_rows = !graph_has_super_rows(p->pipe->g, p->pipe->sc, cap);
     e = e == cudaSuccess ? cudaGetLastError() : e;
     if (e == cudaSuccess) e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
@@ -661,6 +679,8 @@ static size_t op_bytes(int op, int64_t a, int64_t b) {
 }
 
 int fbcc_op_workspace_bytes(int op, int64_t a, int64_t b, size_t* bytes_out) {
+  const Options opts = options_snapshot();  // one snapshot for sizing and enqueue
+  OptScope scope(&opts);
   if (!bytes_out || a < 0 || b < 0) return FBCC_ERR_ARG;
   size_t s = op_bytes(op, a, b);
   if (!s) return FBCC_ERR_ARG;
@@ -691,6 +711,8 @@ static Scalars* op_start(void* ws, cudaStream_t st) {
 int fbcc_connected_components(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m,
                               const uint8_t* keep_mask, void* ws, size_t ws_bytes, int32_t* label, int32_t* forest,
                               int64_t* ncomp_out, void* stream) {
+  const Options opts = options_snapshot();  // one snapshot for sizing and enqueue
+  OptScope scope(&opts);
   int rc = check_sizes(n, m);
   if (rc) return rc;
   if (!offsets || (m && !edges) || !label || !ws) return FBCC_ERR_ARG;
@@ -712,6 +734,8 @@ int fbcc_connected_components(const int64_t* offsets, const uint32_t* edges, int
 
 int fbcc_list_ranking(const int32_t* nxt, int64_t L, const int32_t* heads, int64_t H, int32_t* ranks, void* ws,
                       size_t ws_bytes, void* stream) {
+  const Options opts = options_snapshot();  // one snapshot for sizing and enqueue
+  OptScope scope(&opts);
   if (L < 0 || H < 0 || (L && (!nxt || !ranks)) || (H && !heads) || !ws) return FBCC_ERR_ARG;
   if (L > 2147483647LL) return FBCC_ERR_TOO_LARGE;
   if (ws_bytes < op_bytes(FBCC_OP_LIST_RANKING, L, H)) return FBCC_ERR_WORKSPACE;
@@ -725,6 +749,8 @@ int fbcc_list_ranking(const int32_t* nxt, int64_t L, const int32_t* heads, int64
 
 int fbcc_build_euler_tour(int64_t n, const int32_t* pairs, int64_t k, const int32_t* labels, int32_t* parent,
                           int32_t* first, int32_t* last, void* ws, size_t ws_bytes, void* stream) {
+  const Options opts = options_snapshot();  // one snapshot for sizing and enqueue
+  OptScope scope(&opts);
   if (n < 0 || k < 0 || !ws) return FBCC_ERR_ARG;
   if (n && 2 * n > 2147483647LL) return FBCC_ERR_TOO_LARGE;
   if (k >= n && n > 0) return FBCC_ERR_NOT_FOREST;  // euler_tour.py:381-382
@@ -743,6 +769,8 @@ int fbcc_build_euler_tour(int64_t n, const int32_t* pairs, int64_t k, const int3
 int fbcc_compute_tags(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, const int32_t* parent,
                       const int32_t* first, const int32_t* last, int32_t* w1, int32_t* w2, int32_t* low,
                       int32_t* high, void* ws, size_t ws_bytes, void* stream) {
+  const Options opts = options_snapshot();  // one snapshot for sizing and enqueue
+  OptScope scope(&opts);
   int rc = check_sizes(n, m);
   if (rc) return rc;
   if (n == 0) return FBCC_OK;
@@ -760,6 +788,8 @@ int fbcc_compute_tags(const int64_t* offsets, const uint32_t* edges, int64_t n, 
 
 int fbcc_extract_bccs(const int32_t* label, const int32_t* head, int64_t n, int32_t* block_off, int32_t* block_vtx,
                       int64_t* nblocks, void* ws, size_t ws_bytes, void* stream) {
+  const Options opts = options_snapshot();  // one snapshot for sizing and enqueue
+  OptScope scope(&opts);
   if (n < 0 || !nblocks || !ws) return FBCC_ERR_ARG;
   *nblocks = 0;
   if (n == 0) return FBCC_OK;
@@ -776,6 +806,8 @@ int fbcc_extract_bccs(const int32_t* label, const int32_t* head, int64_t n, int3
 
 int fbcc_symmetrize(const int64_t* u, const int64_t* v, int64_t k, int64_t n, int64_t* offsets, uint32_t* edges,
                     int64_t* m_out, void* ws, size_t ws_bytes, void* stream) {
+  const Options opts = options_snapshot();  // one snapshot for sizing and enqueue
+  OptScope scope(&opts);
   if (k < 0 || n < 0 || !m_out || !offsets || !ws || (k && (!u || !v || !edges))) return FBCC_ERR_ARG;
   if (n >= (1LL << 31) || 2 * k > 2147483647LL) return FBCC_ERR_TOO_LARGE;
   if (ws_bytes < op_bytes(FBCC_OP_SYMMETRIZE, k, n)) return FBCC_ERR_WORKSPACE;

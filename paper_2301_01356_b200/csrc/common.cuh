@@ -38,7 +38,7 @@ enum KernelKind : int {  // one kind per kernel function (names: api.cu kKernelN
   K_CHUNK_ROWS = 0, K_HOOK_MIN, K_IOTA, K_PROPOSE, K_ACCEPT, K_COMPRESS, K_FIND_GIANT, K_LINK_ROWS, K_LINK_HEAVY,
   K_ROOT_FLAGS, K_SCAN, K_ROOT_LIST, K_OUT_LISTS, K_LINK_TOUR, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_RANK0,
   K_POSITIONS, K_FIRSTS, K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_COUNT_BLOCKS, K_AP, K_SET_EDGES,
-  K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_NUM_KINDS
+  K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_WIDEN, K_NUM_KINDS
 };
 
 struct LaunchLog {
@@ -68,7 +68,9 @@ struct LaunchLog {
 
 extern thread_local LaunchLog* g_log;
 
-// process-wide tunables (fbcc_set_option); defaults are the tuned values
+// tunables (fbcc_set_option sets the process-wide defaults; each pipeline,
+// plan and op snapshots them once when it is created and enqueues with its
+// own copy, see OptScope)
 enum Option : int {
   OPT_SAMPLE_ROUNDS = 0,  // Afforest neighbour-sampling rounds
   OPT_GIANT_SKIP = 1,     // skip rows already in the sampled giant component
@@ -86,7 +88,19 @@ enum Option : int {
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 20
 };
-extern int g_opt[OPT_NUM];
+struct Options {
+  int v[OPT_NUM];
+};
+// the snapshot the current thread is enqueueing with (nullptr: the defaults)
+extern thread_local const Options* t_opt;
+Options options_snapshot();    // the current process-wide defaults (atomic reads)
+int option_default(int key);
+inline int opt(int key) { return t_opt ? t_opt->v[key] : option_default(key); }
+struct OptScope {  // RAII: enqueue with the given snapshot on this thread
+  const Options* prev;
+  explicit OptScope(const Options* o) : prev(t_opt) { t_opt = o; }
+  ~OptScope() { t_opt = prev; }
+};
 
 // ---------------------------------------------------------------------------
 // launches: programmatic dependent launch (PDL).  Every kernel of ours starts
@@ -117,7 +131,7 @@ inline void launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, c
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = g_opt[OPT_PDL] ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);

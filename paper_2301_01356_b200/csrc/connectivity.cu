@@ -45,7 +45,7 @@ enum : int { PRED_NONE = 0, PRED_SKEL = 1, PRED_MASK = 2 };
 
 struct PredData {
   const int4* rec;        // PRED_SKEL: {first, last, parent, fence}
-  const int* w0;          // PRED_SKEL (optional): each row's first arc target, recorded by Stage 3
+  const int* w0;          // PRED_SKEL (optional): each row's first arc target, recorded by Stage 1's k_chunk_rows
   const uint8_t* mask;    // PRED_MASK: per-slot keep byte
   const int64_t* off;     // PRED_MASK: to find the canonical (u < w) slot
   const uint32_t* adj;
@@ -229,7 +229,7 @@ bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, i
     if (nlow) cudaMemsetAsync(nlow, 0, sizeof(int) * g.n, st);
     return false;
   }
-  const bool fold = comp != nullptr && g_opt[OPT_SAMPLE_ROUNDS] > 0;
+  const bool fold = comp != nullptr && opt(OPT_SAMPLE_ROUNDS) > 0;
   launch(k_chunk_rows, grid_for(g.n, 256), 256, 0, st, g.off, g.n, crow, sc, g.adj, fold ? comp : nullptr, fe, prop,
          nlow, w0);
   note(K_CHUNK_ROWS);
@@ -255,7 +255,7 @@ __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __re
       const int4 rv = __ldg(pd.rec + v);
       if (rv.z >= 0 && rv.w == 0 && rv.z < c) c = rv.z;
     } else if (s < e) {
-      // (Stage 5: the first arc's target as Stage 3's gather recorded it --
+      // (Stage 5: the first arc's target as Stage 1's k_chunk_rows recorded it --
       // a coalesced 4-byte read instead of one cold adjacency sector per row)
       int w = kPred == PRED_NONE ? round0_target(adj, v, s, e)
                                  : (kPred == PRED_SKEL && pd.w0) ? __ldg(pd.w0 + v) : (int)__ldg(adj + s);
@@ -690,10 +690,10 @@ template <int kPred, bool kRecord>
 static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop, PredData pd, Scalars* sc,
                    int slot, cudaStream_t st, bool round0_done = false, RootInit ri = RootInit{}) {
   const int B = 256;
-  const int kBase = g_opt[OPT_SAMPLE_ROUNDS];
+  const int kBase = opt(OPT_SAMPLE_ROUNDS);
   // adaptive rounds kBase .. kRounds-1 (skip_round); Stage 5 may cap them separately
-  int max_rounds = g_opt[OPT_MAX_ROUNDS];
-  if (kPred == PRED_SKEL && g_opt[OPT_SKEL_MAX_ROUNDS] > 0) max_rounds = g_opt[OPT_SKEL_MAX_ROUNDS];
+  int max_rounds = opt(OPT_MAX_ROUNDS);
+  if (kPred == PRED_SKEL && opt(OPT_SKEL_MAX_ROUNDS) > 0) max_rounds = opt(OPT_SKEL_MAX_ROUNDS);
   const int kRounds = max_rounds > kBase ? std::min(max_rounds, 8) : kBase;
   const int gv = grid_for(g.n, B);
   // k_compress relies on concurrent threads advancing each other's pointers:
@@ -705,12 +705,12 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   // compress after round 0 (flattens the deep min-neighbour forest) and after
   // the last round (k_link_rows' giant test wants a flat array); rounds in
   // between only hook roots under roots and their proposers find() instead
-  int cmask = g_opt[OPT_COMPRESS_MASK];
+  int cmask = opt(OPT_COMPRESS_MASK);
   if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
   if (kRounds > 0 && round0_done) {
     // (k_chunk_rows)
   } else if (kRounds > 0) {
-    const int sp = g_opt[OPT_SKEL_PARENT];
+    const int sp = opt(OPT_SKEL_PARENT);
     launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd, (sp & 1) != 0,
            (sp & 0x80) != 0);  // round 0
     note(K_HOOK_MIN);
@@ -721,10 +721,10 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
     // a round followed by a compress folds its accept into it (OPT_ACCEPT_FOLD)
-    const bool fold = r > 0 && ((cmask >> r) & 1) && g_opt[OPT_ACCEPT_FOLD];
+    const bool fold = r > 0 && ((cmask >> r) & 1) && opt(OPT_ACCEPT_FOLD);
     if (r > 0) {
       launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat,
-             ((g_opt[OPT_SKEL_PARENT] >> r) & 1) != 0, kBase);
+             ((opt(OPT_SKEL_PARENT) >> r) & 1) != 0, kBase);
       note(K_PROPOSE);
       if (!fold) {
         launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase);
@@ -733,22 +733,22 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     }
     if ((cmask >> r) & 1) {
       // the last sampling round's compress also picks the giant
-      const bool last_round = r == kRounds - 1 && g_opt[OPT_GIANT_FOLD];
+      const bool last_round = r == kRounds - 1 && opt(OPT_GIANT_FOLD);
       const int* skip_hooks = r >= kBase ? (const int*)hooks : nullptr;
       if (fold) {
         launch(k_compress<false, true, kRecord>, gres, B, 0, st, comp, g.n, (int*)nullptr, last_round ? sc : nullptr,
-               g_opt[OPT_GIANT_SKIP] != 0, RootInit{}, skip_hooks, r, kBase, prop, hooks + r, fe, g.off, g.adj);
+               opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase, prop, hooks + r, fe, g.off, g.adj);
       } else {
         launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
-               last_round ? sc : nullptr, g_opt[OPT_GIANT_SKIP] != 0, RootInit{}, skip_hooks, r, kBase,
+               last_round ? sc : nullptr, opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase,
                (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
                (const uint32_t*)nullptr);
       }
       note(K_COMPRESS);
     }
   }
-  if (!g_opt[OPT_GIANT_FOLD] || kRounds == 0 || !((cmask >> (kRounds - 1)) & 1)) {  // not folded
-    launch(k_find_giant, 1, 1024, 0, st, comp, g.n, sc, g_opt[OPT_GIANT_SKIP] != 0 && kRounds > 0);
+  if (!opt(OPT_GIANT_FOLD) || kRounds == 0 || !((cmask >> (kRounds - 1)) & 1)) {  // not folded
+    launch(k_find_giant, 1, 1024, 0, st, comp, g.n, sc, opt(OPT_GIANT_SKIP) != 0 && kRounds > 0);
     note(K_FIND_GIANT);
   }
   if (g.m > 0) {
@@ -759,11 +759,12 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     launch(k_link_rows<kPred, kRecord>, grid_for(g.n, B, 32), B, 0, st, g.off, g.adj, g.n, comp, fe, pd, sc, heavy,
                                                                     nheavy);
     note(K_LINK_ROWS);
-    if (!g.no_super_rows) {
-      launch(k_link_heavy<kPred, kRecord>, grid_for((int64_t)kNumSMs * 2048, B), B, 0, st, g.off, g.adj, comp, fe,
-             pd, heavy, nheavy);
-      note(K_LINK_HEAVY);
-    }
+    // always launched: whether a super-heavy row exists is a property of the
+    // buffer contents, which a replayed plan must not bake in (an empty list
+    // costs one ~2 us launch that exits at once)
+    launch(k_link_heavy<kPred, kRecord>, grid_for((int64_t)kNumSMs * 2048, B), B, 0, st, g.off, g.adj, comp, fe,
+           pd, heavy, nheavy);
+    note(K_LINK_HEAVY);
   }
   launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0, 0,
          (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
@@ -834,11 +835,6 @@ void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t s
   note(K_COMPRESS);
 }
 
-__global__ void k_super_rows(const int64_t* __restrict__ off, int n, int* flag) {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    if (__ldg(off + v + 1) - __ldg(off + v) > kSuperRow) *flag = 1;
-}
-
 __global__ void k_widen(const int* __restrict__ src, int64_t* __restrict__ dst, int64_t count) {
   pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
@@ -847,17 +843,7 @@ __global__ void k_widen(const int* __restrict__ src, int64_t* __restrict__ dst, 
 
 void widen_offsets(const int* src, int64_t* dst, int64_t n, cudaStream_t st) {
   launch(k_widen, grid_for(n + 1, 256), 256, 0, st, src, dst, n + 1);
-  note(K_IOTA);
-}
-
-bool graph_has_super_rows(const Graph& g, void* scratch4, cudaStream_t st) {
-  int* d = (int*)scratch4;
-  int h = 1;
-  if (cudaMemsetAsync(d, 0, sizeof(int), st) != cudaSuccess) return true;
-  k_super_rows<<<grid_for(g.n, 256), 256, 0, st>>>(g.off, g.n, d);
-  if (cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) return true;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return true;
-  return h != 0;
+  note(K_WIDEN);
 }
 
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st,

@@ -14,14 +14,10 @@ struct Graph {
   int n;
   int64_t m;
   const int* crow;       // [ceil(m/kItems)] chunk -> row table (build_chunk_rows)
-  bool no_super_rows = false;  // known: no row exceeds kSuperRow (the super-heavy link pass is not launched)
 };
 
 // int32 offsets [n+1] (uploaded from the host) -> the int64 device CSR offsets
 void widen_offsets(const int* src, int64_t* dst, int64_t n, cudaStream_t st);
-
-// One synchronising query (plan creation): does any row exceed kSuperRow arcs?
-bool graph_has_super_rows(const Graph& g, void* scratch4, cudaStream_t st);
 
 // (comp/fe/prop given: also Stage 1's sampling round 0; returns whether it ran)
 // (nlow given: also zeroes Stage 3's lower-degree counters, coalesced)

@@ -405,12 +405,12 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
   } else {
     int64_t nchunks = (g.m + kItems - 1) / kItems;
     const size_t smem = eb_rows_bytes(kEBThreads) + 16 * (size_t)(((n + 31) / 32 + 3) / 4);
-    if (g_opt[OPT_EB_STAGED] && smem <= (size_t)kEBMaxSmemBytes) {
+    if (opt(OPT_EB_STAGED) && smem <= (size_t)kEBMaxSmemBytes) {
       cudaFuncSetAttribute(k_edge_blocks_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       launch(k_edge_blocks_ws, grid_for(nchunks, kEBThreads, 1), kEBThreads, smem, st, g.off, g.adj, g.crow, n, g.m,
              label, head, uoff, nlow, (const uint32_t*)gbits, sc, edge_label, bmin);
     } else {
-      launch(g_opt[OPT_EB_STAGED] ? k_edge_blocks<true> : k_edge_blocks<false>, grid_for(nchunks, B, 32), B, 0, st,
+      launch(opt(OPT_EB_STAGED) ? k_edge_blocks<true> : k_edge_blocks<false>, grid_for(nchunks, B, 32), B, 0, st,
              g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow, (const uint32_t*)gbits, edge_label, bmin, sc);
     }
     note(K_EDGE_BLOCKS);

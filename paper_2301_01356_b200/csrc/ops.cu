@@ -395,10 +395,10 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   int64_t K[8] = {0};
   int S[8] = {0};
   int nlev = 1;
-  S[0] = g_opt[OPT_S0];
+  S[0] = opt(OPT_S0);
   K[1] = (N0 + S[0] - 1) / S[0];
   while (K[nlev] > kFinalMax) {
-    S[nlev] = g_opt[OPT_SL];
+    S[nlev] = opt(OPT_SL);
     K[nlev + 1] = (K[nlev] + S[nlev] - 1) / S[nlev];
     nlev++;
   }

@@ -109,7 +109,7 @@ def _dev(a, dtype):
 
 def _csr(g: Graph):
     torch = _torch()
-    if g._dev is not None:
+    if getattr(g, "_dev", None) is not None:
         off, adj = g._dev
         return off.to("cuda"), adj.view(torch.int32).to("cuda") if adj.dtype == torch.uint32 else adj.to("cuda")
     return (torch.from_numpy(g.offsets).to("cuda"),
