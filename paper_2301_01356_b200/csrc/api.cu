@@ -19,7 +19,7 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "chunk_rows", "hook_min", "iota", "propose", "accept", "compress", "find_giant", "link_rows", "link_heavy",
     "root_flags", "scan", "root_list", "out_lists", "link_tour", "walk0", "walk_level", "final_rank", "expand", "rank0",
     "positions", "firsts", "w_gather", "tile", "table", "fence", "heads", "count_blocks", "ap", "set_edges",
-    "edge_blocks", "edge_final", "memset", "export", "widen"};
+    "edge_blocks", "edge_final", "memset", "export", "widen", "giant_min", "edge_fill", "edge_search"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -53,7 +53,7 @@ constexpr int kMaxStreamChunks = 64;
 struct Layout {
   size_t total = 0;
   size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, hsub, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
-      nlow, bmin, gbits, w0, cub;
+      nlow, bmin, w0, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
   int64_t K[8] = {0};
@@ -114,7 +114,6 @@ struct Layout {
     uoff = take(4 * (n + 1));
     nlow = take(4 * n);
     bmin = take(4 * n);
-    gbits = take(4 * ((n + 31) / 32 + 4));
     w0 = take(4 * n);
     cub = take(cub_bytes);
   }
@@ -136,7 +135,6 @@ struct Pipeline {
   int* uoff;
   int* nlow;
   int* bmin;
-  uint32_t* gbits;  // [ceil(n/32)] Stage 6: bit v = v in the giant skeleton component
   const Side* side = nullptr;  // second stream for Stage 6's independent pieces (plan capture, host path)
   int* w0;          // [n] each row's first arc target (Stage 1's round 0 -> Stage 5's round 0)
   bool w0_valid = false;
@@ -192,7 +190,6 @@ struct Pipeline {
     uoff = (int*)at(lay.uoff);
     nlow = (int*)at(lay.nlow);
     bmin = (int*)at(lay.bmin);
-    gbits = (uint32_t*)at(lay.gbits);
     w0 = (int*)at(lay.w0);
   }
 
@@ -246,8 +243,11 @@ struct Pipeline {
     stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st, w0_valid ? w0 : nullptr);
     mk(5);
     if (label_done) cudaEventRecord(label_done, st);
-    stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, gbits, R.cub_tmp,
-                     R.cub_bytes, sc, st, heads_done, side);
+    // Stage 2's root list / root ranks / out-list links are dead by Stage 6:
+    // its deferred rows, search flags and searched positions
+    stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, R.rlist,
+                     R.rootidx, R.nexto,
+                     R.cub_tmp, R.cub_bytes, sc, st, heads_done, side);
     mk(6);
   }
 

@@ -27,7 +27,8 @@ struct Scalars {
   unsigned ticket; // last-block detection (k_compress; reset by the last block)
   int giant_cnt;   // samples (of 1024) that fell in the giant at its pick
   unsigned tile_ticket;  // k_tile: last block builds the tile-extreme table (reset by it)
-  int pad[21];
+  int eheavy;      // Stage 6: super-heavy non-giant rows deferred by k_edge_fix
+  int pad[20];
 };
 
 // ---------------------------------------------------------------------------
@@ -38,7 +39,7 @@ enum KernelKind : int {  // one kind per kernel function (names: api.cu kKernelN
   K_CHUNK_ROWS = 0, K_HOOK_MIN, K_IOTA, K_PROPOSE, K_ACCEPT, K_COMPRESS, K_FIND_GIANT, K_LINK_ROWS, K_LINK_HEAVY,
   K_ROOT_FLAGS, K_SCAN, K_ROOT_LIST, K_OUT_LISTS, K_LINK_TOUR, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_RANK0,
   K_POSITIONS, K_FIRSTS, K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_COUNT_BLOCKS, K_AP, K_SET_EDGES,
-  K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_WIDEN, K_NUM_KINDS
+  K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_WIDEN, K_GIANT_MIN, K_EDGE_FILL, K_EDGE_SEARCH, K_NUM_KINDS
 };
 
 struct LaunchLog {
@@ -81,7 +82,7 @@ enum Option : int {
   OPT_STREAM_CHUNKS = 12, // fbcc_run_host: arc ranges the edge copy is split into
   OPT_SKEL_PARENT = 13,   // Stage 5 sampling: bit r = round r samples the plain parent edge
   OPT_GIANT_FOLD = 14,    // the last sampling compress also picks the giant (no k_find_giant)
-  OPT_EB_STAGED = 15,     // Stage 6 edge blocks: warp-staged rows + giant bitmap (0: plain arc visitor)
+  OPT_EB_STAGED = 15,     // (retired: the warp-staged bitmap edge pass)
   OPT_MAX_ROUNDS = 16,    // adaptive sampling rounds beyond OPT_SAMPLE_ROUNDS, up to this many (see skip_round)
   OPT_SKEL_MAX_ROUNDS = 17,  // Stage 5's cap instead (0: OPT_MAX_ROUNDS)
   OPT_ACCEPT_FOLD = 18,   // a sampling round's accept runs inside the compress that follows it

@@ -136,9 +136,9 @@ void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out,
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
                         cudaStream_t st, const int* w0 = nullptr);
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
-                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, uint32_t* gbits, void* cub_tmp,
-                      size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done = nullptr,
-                      const Side* side = nullptr);
+                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, int* heavy, int* sreq, int* spos,
+                      void* cub_tmp, size_t cub_bytes, Scalars* sc, cudaStream_t st,
+                      cudaEvent_t heads_done = nullptr, const Side* side = nullptr);
 void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* AP, int* forest,
                   int* parent, int* first, int* last, int* w1, int* w2, uint8_t* fence,
                   cudaStream_t st);

@@ -42,28 +42,18 @@ __device__ __forceinline__ int giant_label(const int* label, const Scalars* sc) 
 }
 
 __global__ void k_heads(int n, const int4* __restrict__ rec, const int* __restrict__ label, int* head, int* cnt,
-                        uint32_t* __restrict__ gbits, Scalars* sc) {
+                        Scalars* sc) {
   pdl_enter();
-  const int G = giant_label(label, sc);
-  const int lane = threadIdx.x & 31;
   int blocks = 0;
-  // warp-uniform trip count: the warp also writes one word of the giant bitmap
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int v = (int)base + lane;
-    int l = -1;
-    if (v < n) {
-      l = __ldg(label + v);
-      int p = __ldg(&rec[v].z);
-      // (read first: the children of one head inside one component -- RMAT
-      // hubs -- would otherwise serialise their CAS on one word)
-      if (p >= 0 && l != __ldg(label + p) && ld_relaxed(head + l) == -1 && atomicCAS(head + l, -1, p) == -1) {
-        blocks++;
-        if (ld_relaxed(cnt + p) < 2) atomicAdd(cnt + p, 1);
-      }
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int l = __ldg(label + v);
+    const int p = __ldg(&rec[v].z);
+    // (read first: the children of one head inside one component -- RMAT
+    // hubs -- would otherwise serialise their CAS on one word)
+    if (p >= 0 && l != __ldg(label + p) && ld_relaxed(head + l) == -1 && atomicCAS(head + l, -1, p) == -1) {
+      blocks++;
+      if (ld_relaxed(cnt + p) < 2) atomicAdd(cnt + p, 1);
     }
-    const unsigned bits = __ballot_sync(0xffffffffu, l == G && G >= 0);
-    if (lane == 0) gbits[base >> 5] = bits;
   }
   block_count_add(&sc->nbccs, blocks);
 }
@@ -78,280 +68,335 @@ __global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict
   }
 }
 
-// Per-block minimum edge id without a per-run atomic: edge ids grow with the
-// row (u < w, CSR order), so a block's minimum edge is the FIRST upper arc in
-// the row of the block's minimum vertex u0 = min(l, head[l]) (every block
-// vertex has a block edge; u0's all go upward).  Only arcs of u0 rows feed
-// bmin: for an arc in its own component's block (blk == label[v]) that means
-// v == label[v] < head[label[v]]; for an arc into a child block headed by v
-// (blk == label[w]) it means v < label[w].  Those atomics hit distinct
-// addresses (one row per block) -- the old run-length scheme issued a
-// read + atomicMin per block change, i.e. per arc of an RMAT hub.
-// kBits: when the giant holds at least a quarter of Stage 5's 1024 vertex
-// samples (RMAT: ~half -- its other half is isolated vertices), the
-// giant-component bitmap (k_heads) is read first, from global memory (n/8
-// bytes: 4 MB on RMAT, 32x denser than label[] and mostly cache-resident;
-// RMAT 4.57 -> 4.12 ms) and label[w] is gathered only for arcs leaving the
-// giant; a small giant (config 4b: 24 M blocks) keeps the label gather.
-template <bool kBits>
-struct EdgeBlockVisitor {
+// ---------------------------------------------------------------------------
+// Per-edge labels.  edge_label[e] = minimum edge id of e's block, e = rank of
+// the upper arc (u -> w, u < w) in CSR order.
+//
+// Almost every edge of a large graph lies in the block of the giant skeleton
+// component G (RMAT: 99.1 %, config 2: ~100 %), and a G-G edge's label is the
+// block minimum bmin[G] -- known before the edge pass:
+//  1. k_giant_min: bmin[G] = the first upper arc of u0 = min(G, head[G]) (the
+//     block's minimum vertex; edge ids grow with the smaller endpoint) whose
+//     block is G -- one warp, usually the first arc.
+//  2. k_edge_fill: edge_label[0..E) = bmin[G], a streaming store -- no
+//     adjacency read, no label gather.
+//  3. k_edge_fix: over the rows, dropping G's rows by their label before any
+//     adjacency load.  Every upper arc of a non-G row gets its block by the
+//     rule of bcc.py:24-27 (label[w] gathered): G -> the final bmin[G],
+//     otherwise blk | MARK.  An edge (x, v), x < v, between a G row x and a
+//     non-G row v is G's unless v's component hangs off x (x =
+//     head[label[v]]); the row flags that case (sreq[v]) for
+//  4. k_edge_search: binary search of v in x's upper arcs (spos[v] = e), one
+//     request per thread -- inline, the ~10 dependent loads serialised whole
+//     warps of the row pass.  Also the rows over 8192 arcs that k_edge_fix
+//     deferred (a non-giant RMAT hub: 638k arcs), over the whole grid.
+//     Per-block minima: atomicMin from the block's minimum-vertex row only
+//     (one uncontended address per block; one atomic per run of a block).
+//  5. k_edge_final: MARKed entries -> bmin[blk], over the non-G rows again
+//     (and the searched positions, and the deferred rows).
+// No global counters besides the rare deferred-row list: a list append per
+// rewritten edge serialised on one L2 address (RMAT: 4.2 M, ~2 ms).
+// With no large giant (Stage 5's sample put < 1/4 of its points in one
+// component: tori with many blocks, the chain) G = -1: no fill, every row is
+// processed, blocks are written unmarked and k_edge_final maps all E.
+// ---------------------------------------------------------------------------
+constexpr int kEdgeMark = (int)0x80000000;
+constexpr int kEdgeSuperRow = 8192;
+
+__device__ __forceinline__ int big_giant(const int* label, const Scalars* sc) {
+  return sc->giant_cnt >= 256 ? giant_label(label, sc) : -1;
+}
+
+// first upper arc of row u: off[u] + nlow[u] (rows sorted, no self-loops);
+// edge id of upper arc a of row u: uoff[u] + (a - first upper arc)
+__global__ void k_giant_min(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                            const int* __restrict__ label, const int* __restrict__ head,
+                            const int* __restrict__ uoff, const int* __restrict__ nlow, int* bmin, const Scalars* sc) {
+  pdl_enter();
+  const int G = big_giant(label, sc);
+  if (G < 0) return;
+  const int lane = threadIdx.x;
+  const int h = __ldg(head + G);
+  const int u0 = (h >= 0 && h < G) ? h : G;
+  const int lu = __ldg(label + u0);
+  const int64_t a0 = __ldg(off + u0) + __ldg(nlow + u0), re = __ldg(off + u0 + 1);
+  for (int64_t a = a0 + lane; a - lane < re; a += 32) {
+    bool hit = false;
+    if (a < re) {
+      const int w = (int)__ldg(adj + a);
+      const int lw = __ldg(label + w);
+      const int blk = lu == lw ? lu : (__ldg(head + lw) == u0 ? lw : lu);
+      hit = blk == G;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, hit);
+    if (b) {
+      if (lane == __ffs(b) - 1) bmin[G] = __ldg(uoff + u0) + (int)(a - a0);
+      return;
+    }
+  }
+}
+
+__global__ void k_edge_fill(int n, const int* __restrict__ label, const int* __restrict__ uoff,
+                            const int* __restrict__ bmin, int* __restrict__ edge_label, Scalars* sc) {
+  pdl_enter();
+  const int E = __ldg(uoff + n);
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->num_edges = E;
+  const int G = big_giant(label, sc);
+  if (G < 0) return;
+  const int val = __ldg(bmin + G);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(edge_label) & 15) == 0) {
+    const int64_t nv = E / 4;
+    const int4 v4 = make_int4(val, val, val, val);
+    for (int64_t i = tid; i < nv; i += stride) __stcs(reinterpret_cast<int4*>(edge_label) + i, v4);
+    for (int64_t e = 4 * nv + tid; e < E; e += stride) edge_label[e] = val;
+  } else {
+    for (int64_t e = tid; e < E; e += stride) edge_label[e] = val;
+  }
+}
+
+// Per-thread state of the non-giant row passes.  The arcs one thread visits
+// come in increasing order, so per-block minima go out as one atomicMin per
+// run of a block.
+struct EdgeFix {
   const int64_t* off;
+  const uint32_t* adj;
   const int* label;
   const int* head;
   const int* uoff;
   const int* nlow;
-  const uint32_t* gbits;
-  int G;
-  int* eblk;
+  int* edge_label;
   int* bmin;
-  int lu, ebase;
-  bool row_u0;
+  int G, valG;
   int run_blk, run_min;
-  int pl[kBits ? 1 : kItems];
-  unsigned ing;  // kBits: bit i = arc i's target is in the giant
-  // label[w] (or its giant bit) for every arc that can be an upper arc (w > first row of the chunk)
-  __device__ __forceinline__ void prefetch(int v0, const uint32_t* w, int cnt) {
-    if (kBits) {
-      ing = 0;
-#pragma unroll
-      for (int i = 0; i < kItems; i++)
-        if (i < cnt && (int)w[i] > v0) ing |= ((__ldg(gbits + (w[i] >> 5)) >> (w[i] & 31)) & 1u) << i;
-    } else {
-#pragma unroll
-      for (int i = 0; i < kItems; i++) pl[kBits ? 0 : i] = (i < cnt && (int)w[i] > v0) ? __ldg(label + w[i]) : -1;
-    }
+
+  __device__ __forceinline__ void init(const int64_t* o, const uint32_t* a, const int* lb, const int* hd,
+                                       const int* uo, const int* nl, int* el, int* bm, const Scalars* sc) {
+    off = o;
+    adj = a;
+    label = lb;
+    head = hd;
+    uoff = uo;
+    nlow = nl;
+    edge_label = el;
+    bmin = bm;
+    G = big_giant(lb, sc);
+    valG = G >= 0 ? __ldg(bm + G) : 0;  // final (k_giant_min)
+    run_blk = -1;
+    run_min = 0;
   }
   __device__ __forceinline__ void flush() {
     if (run_blk >= 0) atomicMin(bmin + run_blk, run_min);
     run_blk = -1;
   }
-  __device__ __forceinline__ void begin(int v, int64_t rs, int64_t) {
-    lu = __ldg(label + v);
-    ebase = __ldg(uoff + v) - (int)(rs + __ldg(nlow + v));  // e = ebase + a for upper arcs
-    // head[v] >= 0 only for label vertices (v == label[v]): no dependent load
-    const int hv = __ldg(head + v);
+  __device__ __forceinline__ void mark(int e, int blk) {
+    if (G < 0) edge_label[e] = blk;           // no giant: k_edge_final maps every edge
+    else if (blk == G) edge_label[e] = valG;  // final already
+    else edge_label[e] = blk | kEdgeMark;
+  }
+  // row words: hl = head of v's block, row_u0 = v is its block's minimum
+  // vertex (v a label below its head), ebase: edge id of upper arc a = ebase + a
+  __device__ __forceinline__ void row_words(int v, int lu, int64_t rs, int& hl, bool& row_u0, int& ebase) const {
+    hl = __ldg(head + lu);
+    const int hv = v == lu ? hl : -1;  // head[v] >= 0 only at label vertices
     row_u0 = hv >= 0 && v < hv;
+    ebase = __ldg(uoff + v) - (int)(rs + __ldg(nlow + v));
   }
-  __device__ __forceinline__ void arc(int v, int64_t a, int w, int i) {
-    if (w <= v) return;
-    int e = ebase + (int)a;
-    bool mine;
-    int blk;
-    int lw;
-    if (kBits) {
-      if (lu == G && ((ing >> i) & 1u)) {
-        eblk[e] = G;
-        if (row_u0 && G != run_blk) {
-          flush();
-          run_blk = G;
-          run_min = e;
-        }
-        return;
+  // one arc of non-giant row v; returns true for the lower arc to the head of
+  // v's block when that head is in G (the edge sits in the head's G row)
+  __device__ __forceinline__ bool arc(int v, int lu, int hl, bool row_u0, int ebase, int64_t a, int x) {
+    if (x > v) {  // upper arc: this row holds the edge
+      const int lw = __ldg(label + x);
+      int blk;
+      bool mine;
+      if (lu == lw) {
+        blk = lu;
+        mine = row_u0;
+      } else if (__ldg(head + lw) == v) {  // x's component hangs off v: its block
+        blk = lw;
+        mine = v < lw;
+      } else {
+        blk = lu;
+        mine = row_u0;
       }
-      lw = __ldg(label + w);
-    } else {
-      lw = pl[kBits ? 0 : i];
+      const int e = ebase + (int)a;
+      mark(e, blk);
+      if (mine && blk != run_blk && blk != G) {
+        flush();
+        run_blk = blk;
+        run_min = e;
+      }
+      return false;
     }
-    if (lu == lw) {
-      blk = lu;
-      mine = row_u0;
-    } else if (__ldg(head + lw) == v) {  // w's component hangs off v: its block
-      blk = lw;
-      mine = v < lw;
-    } else {
-      blk = lu;
-      mine = row_u0;
-    }
-    eblk[e] = blk;
-    if (mine && blk != run_blk) {
-      flush();
-      run_blk = blk;
-      run_min = e;
-    }
+    return G >= 0 && x == hl && __ldg(label + x) == G;
   }
-  __device__ __forceinline__ void end(int, bool) {}
+  // that edge: binary search of v in x's sorted upper arcs; it belongs to
+  // v's block
+  __device__ __forceinline__ int fix_lower(int v, int lu, int x) {
+    int64_t lo = __ldg(off + x) + __ldg(nlow + x), hi = __ldg(off + x + 1);
+    const int64_t ub = lo;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int)__ldg(adj + mid) < v) lo = mid + 1; else hi = mid;
+    }
+    const int e = __ldg(uoff + x) + (int)(lo - ub);
+    mark(e, lu);
+    if (x < lu) atomicMin(bmin + lu, e);
+    return e;
+  }
 };
 
-template <bool kBits>
-__global__ void __launch_bounds__(256) k_edge_blocks(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
-                                                     int n, int64_t m, const int* __restrict__ label,
-                                                     const int* __restrict__ head, const int* __restrict__ uoff,
-                                                     const int* __restrict__ nlow, const uint32_t* __restrict__ gbits,
-                                                     int* eblk, int* bmin, Scalars* sc) {
+// Row-filtered: each warp reads the labels and offsets of 32 consecutive
+// rows (coalesced) and drops the giant's rows and empty rows before touching
+// any adjacency -- on RMAT that is all but ~4 M of the 33.5 M rows.  Rows of
+// <= 32 arcs are handled by their own lane, longer ones by the whole warp,
+// rows over kEdgeSuperRow arcs are deferred to k_edge_search (whole grid).
+// sreq[v] (every v written): v's lower-arc fix is k_edge_search's.
+__global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                  int n, const int* __restrict__ label, const int* __restrict__ head,
+                                                  const int* __restrict__ uoff, const int* __restrict__ nlow,
+                                                  int* edge_label, int* bmin, int* __restrict__ heavy,
+                                                  int* __restrict__ sreq, Scalars* sc) {
   pdl_enter();
-  if (blockIdx.x == 0 && threadIdx.x == 0) sc->num_edges = uoff[n];  // (k_set_edges' job)
-  EdgeBlockVisitor<kBits> vis;
-  vis.gbits = gbits;
-  vis.G = giant_label(label, sc);
-  if (kBits && sc->giant_cnt < 256) {  // (uniform) small giant: run the label-gather instance
-    EdgeBlockVisitor<false> lv;
-    lv.off = off;
-    lv.label = label;
-    lv.head = head;
-    lv.uoff = uoff;
-    lv.nlow = nlow;
-    lv.eblk = eblk;
-    lv.bmin = bmin;
-    lv.run_blk = -1;
-    visit_arc_chunks(off, adj, crow, n, m, lv);
-    lv.flush();
-    return;
-  }
-  vis.off = off;
-  vis.label = label;
-  vis.head = head;
-  vis.uoff = uoff;
-  vis.nlow = nlow;
-  vis.eblk = eblk;
-  vis.bmin = bmin;
-  vis.run_blk = -1;
-  visit_arc_chunks(off, adj, crow, n, m, vis);
-  vis.flush();
-}
-
-// Warp-staged variant.  Each warp owns 256 consecutive arcs (8 per lane, as
-// visit_arc_chunks); the per-row words every arc needs -- row end, label,
-// edge-id base, "block minimum row" flag -- are loaded ONCE per row, coalesced,
-// by the lane whose index is the row's offset from the warp's first row, into
-// a per-warp shared-memory window of kEBRows rows (rows beyond it fall back to
-// global loads).  label[w] is replaced, for the common case, by one bit of the
-// giant-component bitmap (bit w = label[w] == G; k_heads), held in shared
-// memory (configs 2/3: 128 KB per CTA, one 1024-thread CTA per SM).  Only
-// arcs leaving the giant gather label[w] / head[label[w]].  Used when the
-// bitmap fits (n <= 1.6M); larger graphs run k_edge_blocks (a global bitmap
-// measured 13% slower than the label gather on RMAT, whose hubs keep label
-// lines L1-resident).
-constexpr int kEBRows = 64;
-constexpr int kEBThreads = 1024;
-constexpr int kEBMaxSmemBytes = 227 * 1024;
-
-__host__ __device__ constexpr size_t eb_rows_bytes(int threads) { return sizeof(int4) * kEBRows * (threads / 32); }
-
-__device__ __forceinline__ int4 eb_row(const int64_t* __restrict__ off, const int* __restrict__ label,
-                                       const int* __restrict__ head, const int* __restrict__ uoff,
-                                       const int* __restrict__ nlow, int r) {
-  const int64_t rs = __ldg(off + r);
-  const int re = (int)__ldg(off + r + 1);
-  const int h = __ldg(head + r);
-  return make_int4(re, __ldg(label + r), __ldg(uoff + r) - (int)(rs + __ldg(nlow + r)), (h >= 0 && r < h) ? 1 : 0);
-}
-
-__global__ void __launch_bounds__(kEBThreads, 1)
-    k_edge_blocks_ws(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, const int* __restrict__ crow,
-                     int n, int64_t m, const int* __restrict__ label, const int* __restrict__ head,
-                     const int* __restrict__ uoff, const int* __restrict__ nlow, const uint32_t* __restrict__ gbits,
-                     Scalars* sc, int* __restrict__ eblk, int* bmin) {
-  pdl_enter();
-  if (blockIdx.x == 0 && threadIdx.x == 0) sc->num_edges = uoff[n];  // (k_set_edges' job)
-  extern __shared__ int4 ebsm[];
-  constexpr int kThreads = kEBThreads;
-  int4* rows = ebsm + (threadIdx.x >> 5) * kEBRows;
-  uint32_t* bits = reinterpret_cast<uint32_t*>(ebsm + kEBRows * (kThreads / 32));
-  const int nw4 = ((n + 31) / 32 + 3) / 4;
-  for (int i = threadIdx.x; i < nw4; i += kThreads)
-    reinterpret_cast<uint4*>(bits)[i] = __ldg(reinterpret_cast<const uint4*>(gbits) + i);
-  __syncthreads();
-  const int G = giant_label(label, sc);
+  EdgeFix f;
+  f.init(off, adj, label, head, uoff, nlow, edge_label, bmin, sc);
   const int lane = threadIdx.x & 31;
-  const int64_t nchunks = (m + kItems - 1) / kItems;
-  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
-  const int64_t stride = (int64_t)gridDim.x * kThreads;
-  int run_blk = -1, run_min = 0;
-  for (int64_t qb = (int64_t)blockIdx.x * kThreads + (threadIdx.x & ~31); qb < nchunks; qb += stride) {
-    const int64_t q = qb + lane;
-    const bool live = q < nchunks;
-    int v = 0;
-    uint32_t w[kItems];
-    int64_t a0 = q * kItems, a1 = a0;
-    if (live) {
-      a1 = a0 + kItems < m ? a0 + kItems : m;
-      if (vec_ok && a1 - a0 == kItems) {
-        int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
-        int4 y = ld_stream4(reinterpret_cast<const int4*>(adj + a0 + 4));
-        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-        w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
-      } else {
-#pragma unroll
-        for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;
-      }
-      v = __ldg(crow + q);
-      if (v < 0) v = row_of(off, 0, n - 1, a0);
-    }
-    const int vf = __shfl_sync(0xffffffffu, v, 0);  // lane 0 is live whenever the warp is
-    // rows the warp can touch: up to the last live lane's row plus the rows
-    // its 8 arcs may still enter
-    const int vl = __reduce_max_sync(0xffffffffu, live ? v : vf);
-    const int rend = min(min(vf + kEBRows, vl + kItems + 1), n);
-    __syncwarp();  // the previous iteration's readers of the window are done
-#pragma unroll
-    for (int k = 0; k < kEBRows; k += 32) {
-      const int r = vf + k + lane;
-      if (r < rend) rows[k + lane] = eb_row(off, label, head, uoff, nlow, r);
-    }
-    __syncwarp();
-    if (live) {
-      int vi = v - vf;
-      int4 R = v < rend ? rows[vi] : eb_row(off, label, head, uoff, nlow, v);
-#pragma unroll
-      for (int i = 0; i < kItems; i++) {
-        const int a = (int)(a0 + i);
-        if (a < (int)a1) {
-          while (a >= R.x) {  // next non-empty row (empty rows share the end)
-            if (v + 1 < rend) {
-              vi++;
-              v++;
-              R = rows[vi];
-            } else {
-              v = next_row(off, v, n, a);
-              R = eb_row(off, label, head, uoff, nlow, v);
-            }
-          }
-          const int x = (int)w[i];
-          if (x > v) {
-            int blk;
-            bool mine;
-            if (R.y == G && ((bits[x >> 5] >> (x & 31)) & 1u)) {
-              blk = G;
-              mine = R.w != 0;
-            } else {
-              const int lw = __ldg(label + x);
-              if (R.y == lw) {
-                blk = lw;
-                mine = R.w != 0;
-              } else if (__ldg(head + lw) == v) {  // x's component hangs off v: its block
-                blk = lw;
-                mine = v < lw;
-              } else {
-                blk = R.y;
-                mine = R.w != 0;
-              }
-            }
-            const int e = R.z + a;
-            eblk[e] = blk;
-            if (mine && blk != run_blk) {
-              if (run_blk >= 0) atomicMin(bmin + run_blk, run_min);
-              run_blk = blk;
-              run_min = e;
-            }
-          }
-        }
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n; base += warps * 32) {
+    const int v = (int)base + lane;
+    int64_t rs = 0, re = 0;
+    int lu = f.G;
+    if (v < n) {
+      lu = __ldg(label + v);
+      if (lu != f.G) {
+        rs = __ldg(off + v);
+        re = __ldg(off + v + 1);
       }
     }
+    if (re - rs > kEdgeSuperRow) {
+      heavy[atomicAdd(&sc->eheavy, 1)] = v;
+      rs = re = 0;
+    }
+    bool req = false;
+    const bool coop = re - rs > 32;
+    if (!coop && re > rs) {
+      int hl, ebase;
+      bool row_u0;
+      f.row_words(v, lu, rs, hl, row_u0, ebase);
+      for (int64_t a = rs; a < re; a++) req |= f.arc(v, lu, hl, row_u0, ebase, a, (int)__ldg(adj + a));
+    }
+    unsigned hb = __ballot_sync(0xffffffffu, coop);
+    while (hb) {
+      const int src = __ffs(hb) - 1;
+      hb &= hb - 1;
+      const int hv = __shfl_sync(0xffffffffu, v, src), hlu = __shfl_sync(0xffffffffu, lu, src);
+      const int64_t hs = __shfl_sync(0xffffffffu, rs, src), he = __shfl_sync(0xffffffffu, re, src);
+      int hl, ebase;
+      bool row_u0;
+      f.row_words(hv, hlu, hs, hl, row_u0, ebase);
+      bool r = false;
+      for (int64_t a = hs + lane; a < he; a += 32) r |= f.arc(hv, hlu, hl, row_u0, ebase, a, (int)__ldg(adj + a));
+      f.flush();  // (the lanes' runs interleave across the row)
+      r = __any_sync(0xffffffffu, r);
+      if (lane == src) req = r;
+    }
+    if (v < n) sreq[v] = req;
   }
-  if (run_blk >= 0) atomicMin(bmin + run_blk, run_min);
+  f.flush();
 }
 
-// block -> minimum edge id of the block, 4 edges per thread (16-byte
-// streaming loads and stores; the bmin gathers of the giant block hit one
-// L1-resident word)
-__global__ void k_edge_final(int* eblk, const int* __restrict__ bmin, const int* __restrict__ uoff, int n) {
+// The deferred work: (a) rows over kEdgeSuperRow arcs, every thread of the
+// grid striding over each (their one lower-arc fix inline); (b) the lower-arc
+// fixes k_edge_fix flagged, one per thread.  Disjoint rows: no ordering
+// between the two.
+__global__ void __launch_bounds__(256) k_edge_search(const int64_t* __restrict__ off,
+                                                     const uint32_t* __restrict__ adj, int n,
+                                                     const int* __restrict__ label, const int* __restrict__ head,
+                                                     const int* __restrict__ uoff, const int* __restrict__ nlow,
+                                                     int* edge_label, int* bmin, const int* __restrict__ heavy,
+                                                     int* sreq, int* spos, Scalars* sc) {
   pdl_enter();
-  const int E = uoff[n];
+  EdgeFix f;
+  f.init(off, adj, label, head, uoff, nlow, edge_label, bmin, sc);
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  const int H = sc->eheavy;
+  for (int h = 0; h < H; h++) {
+    const int v = __ldg(heavy + h);
+    const int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+    const int lu = __ldg(label + v);
+    int hl, ebase;
+    bool row_u0;
+    f.row_words(v, lu, rs, hl, row_u0, ebase);
+    for (int64_t a = rs + tid; a < re; a += stride)
+      if (f.arc(v, lu, hl, row_u0, ebase, a, (int)__ldg(adj + a))) {
+        spos[v] = f.fix_lower(v, lu, hl);  // (k_edge_final maps it; a repeat below is idempotent)
+        sreq[v] = 1;
+      }
+    f.flush();
+  }
+  if (f.G < 0) return;  // (no lower-arc fixes without a giant)
+  for (int64_t v = tid; v < n; v += stride)
+    if (sreq[v]) {
+      const int lu = __ldg(label + v);
+      spos[v] = f.fix_lower((int)v, lu, __ldg(head + lu));
+    }
+}
+
+__device__ __forceinline__ void edge_map(int* edge_label, const int* bmin, int e) {
+  const int b = edge_label[e];
+  if (b < 0) edge_label[e] = __ldg(bmin + (b & ~kEdgeMark));
+}
+
+// MARKed entries -> bmin[blk].  Giant mode: the non-G rows' upper arcs, the
+// searched positions and the deferred rows; otherwise every edge (16-byte
+// streaming loads and stores).
+__global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ off, int n,
+                                                    const int* __restrict__ label, const int* __restrict__ uoff,
+                                                    const int* __restrict__ nlow, int* edge_label,
+                                                    const int* __restrict__ bmin, const int* __restrict__ heavy,
+                                                    const int* __restrict__ sreq, const int* __restrict__ spos,
+                                                    const Scalars* sc) {
+  pdl_enter();
+  const int E = __ldg(uoff + n);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if ((reinterpret_cast<uintptr_t>(eblk) & 15) == 0) {
+  const int G = big_giant(label, sc);
+  if (G >= 0) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = stride >> 5;
+    for (int64_t base = (tid >> 5) * 32; base < n; base += warps * 32) {
+      const int v = (int)base + lane;
+      int e0 = 0, e1 = 0;
+      if (v < n) {
+        if (__ldg(label + v) != G) {
+          e0 = __ldg(uoff + v);
+          e1 = __ldg(uoff + v + 1);
+          if (__ldg(off + v + 1) - __ldg(off + v) > kEdgeSuperRow) e1 = e0;  // deferred row: below
+        }
+        if (__ldg(sreq + v)) edge_map(edge_label, bmin, __ldg(spos + v));
+      }
+      const bool coop = e1 - e0 > 32;
+      if (!coop)
+        for (int e = e0; e < e1; e++) edge_map(edge_label, bmin, e);
+      unsigned hb = __ballot_sync(0xffffffffu, coop);
+      while (hb) {
+        const int src = __ffs(hb) - 1;
+        hb &= hb - 1;
+        const int h0 = __shfl_sync(0xffffffffu, e0, src), h1 = __shfl_sync(0xffffffffu, e1, src);
+        for (int e = h0 + lane; e < h1; e += 32) edge_map(edge_label, bmin, e);
+      }
+    }
+    const int H = sc->eheavy;
+    for (int h = 0; h < H; h++) {
+      const int v = __ldg(heavy + h);
+      const int e0 = __ldg(uoff + v), e1 = __ldg(uoff + v + 1);
+      for (int64_t e = e0 + tid; e < e1; e += stride) edge_map(edge_label, bmin, (int)e);
+    }
+    return;
+  }
+  if ((reinterpret_cast<uintptr_t>(edge_label) & 15) == 0) {
     const int64_t nv = E / 4;
-    int4* e4 = reinterpret_cast<int4*>(eblk);
+    int4* e4 = reinterpret_cast<int4*>(edge_label);
     for (int64_t i = tid; i < nv; i += stride) {
       int4 b = __ldcs(e4 + i);
       b.x = __ldg(bmin + b.x);
@@ -360,9 +405,9 @@ __global__ void k_edge_final(int* eblk, const int* __restrict__ bmin, const int*
       b.w = __ldg(bmin + b.w);
       __stcs(e4 + i, b);
     }
-    for (int64_t e = 4 * nv + tid; e < E; e += stride) eblk[e] = __ldg(bmin + eblk[e]);
+    for (int64_t e = 4 * nv + tid; e < E; e += stride) edge_label[e] = __ldg(bmin + edge_label[e]);
   } else {
-    for (int64_t e = tid; e < E; e += stride) eblk[e] = __ldg(bmin + eblk[e]);
+    for (int64_t e = tid; e < E; e += stride) edge_label[e] = __ldg(bmin + edge_label[e]);
   }
 }
 
@@ -370,13 +415,14 @@ __global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) {
   pdl_enter(); sc->num_edges = uoff[n]; }
 
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
-                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, uint32_t* gbits, void* cub_tmp,
-                      size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done, const Side* side) {
+                      int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, int* heavy, int* sreq, int* spos,
+                      void* cub_tmp, size_t cub_bytes, Scalars* sc, cudaStream_t st, cudaEvent_t heads_done,
+                      const Side* side) {
   const int n = g.n;
   const int B = 256;
   const int gv = grid_for(n + 1, B);
   // head = -1, cnt = 0, bmin = INF were initialised by the stage-4 kernel
-  launch(k_heads, gv, B, 0, st, n, rec, label, head, cnt, gbits, sc);
+  launch(k_heads, gv, B, 0, st, n, rec, label, head, cnt, sc);
   note(K_HEADS);
   if (side) {  // articulation flags beside the edge pass; the scan ran beside Stages 3-5
     cudaEventRecord(side->ev[2], st);
@@ -403,18 +449,18 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
     launch(k_set_edges, 1, 1, 0, st, uoff, n, sc);
     note(K_SET_EDGES);
   } else {
-    int64_t nchunks = (g.m + kItems - 1) / kItems;
-    const size_t smem = eb_rows_bytes(kEBThreads) + 16 * (size_t)(((n + 31) / 32 + 3) / 4);
-    if (opt(OPT_EB_STAGED) && smem <= (size_t)kEBMaxSmemBytes) {
-      cudaFuncSetAttribute(k_edge_blocks_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      launch(k_edge_blocks_ws, grid_for(nchunks, kEBThreads, 1), kEBThreads, smem, st, g.off, g.adj, g.crow, n, g.m,
-             label, head, uoff, nlow, (const uint32_t*)gbits, sc, edge_label, bmin);
-    } else {
-      launch(opt(OPT_EB_STAGED) ? k_edge_blocks<true> : k_edge_blocks<false>, grid_for(nchunks, B, 32), B, 0, st,
-             g.off, g.adj, g.crow, n, g.m, label, head, uoff, nlow, (const uint32_t*)gbits, edge_label, bmin, sc);
-    }
+    launch(k_giant_min, 1, 32, 0, st, g.off, g.adj, label, head, uoff, nlow, bmin, (const Scalars*)sc);
+    note(K_GIANT_MIN);
+    launch(k_edge_fill, grid_for(g.m / 8 + 1, B), B, 0, st, n, label, uoff, bmin, edge_label, sc);
+    note(K_EDGE_FILL);
+    launch(k_edge_fix, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin,
+           heavy, sreq, sc);
     note(K_EDGE_BLOCKS);
-    launch(k_edge_final, grid_for(g.m / 2, B), B, 0, st, edge_label, bmin, uoff, n);
+    launch(k_edge_search, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin,
+           (const int*)heavy, sreq, spos, sc);
+    note(K_EDGE_SEARCH);
+    launch(k_edge_final, grid_for(n, B, 32), B, 0, st, g.off, n, label, uoff, nlow, edge_label, bmin,
+           (const int*)heavy, (const int*)sreq, (const int*)spos, (const Scalars*)sc);
     note(K_EDGE_FINAL);
   }
   if (side) cudaStreamWaitEvent(st, side->ev[3], 0);  // join the articulation flags

@@ -9,7 +9,9 @@ WANT = [("gpu__time_duration.sum", "us"), ("dram__bytes_read.sum", "MB_rd"), ("d
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ%"),
         ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts%"),
         ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%"),
-        ("smsp__inst_executed.sum", "inst"), ("launch__registers_per_thread", "regs")]
+        ("smsp__inst_executed.sum", "inst"), ("launch__registers_per_thread", "regs"),
+        ("lts__t_sectors_op_atom.sum", "atom_sect"), ("lts__t_sectors_op_red.sum", "red_sect"),
+        ("lts__t_sectors_srcunit_tex_op_read.sum", "l2_rd_sect")]
 
 
 def rows(path):
@@ -28,6 +30,8 @@ def rows(path):
                         x *= 1e3
                     if short.startswith("MB") and u == "Kbyte":
                         x /= 1e3
+                    if short.startswith("MB") and u == "byte":
+                        x /= 1e6
                     if short == "us" and u == "ms":
                         x *= 1e3
                     if short == "us" and u == "ns":

@@ -36,7 +36,7 @@ __device__ __forceinline__ uint64_t out(u128 s) {
 }
 
 // one chunk of k edges; `base` = draws consumed before the chunk
-__global__ void k_rmat(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t base, int64_t k,
+__global__ void gen_rmat(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t base, int64_t k,
                        int scale, int per, int64_t* u, int64_t* v) {
   const u128 s0 = ((u128)s_hi << 64) | s_lo, inc = ((u128)i_hi << 64) | i_lo;
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * per;
@@ -60,6 +60,6 @@ extern "C" int rmat_pairs_chunk(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uin
   const int per = 256, B = 128;
   const int64_t threads = (k + per - 1) / per;
   const int grid = (int)((threads + B - 1) / B);
-  k_rmat<<<grid, B, 0, (cudaStream_t)stream>>>(s_hi, s_lo, i_hi, i_lo, base, k, scale, per, u, v);
+  gen_rmat<<<grid, B, 0, (cudaStream_t)stream>>>(s_hi, s_lo, i_hi, i_lo, base, k, scale, per, u, v);
   return (int)cudaGetLastError();
 }
