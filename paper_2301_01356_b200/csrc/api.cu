@@ -114,7 +114,7 @@ struct Layout {
     uoff = take(4 * (n + 1));
     nlow = take(4 * n);
     bmin = take(4 * n);
-    w0 = take(4 * n);
+    w0 = take(12 * n);
     cub = take(cub_bytes);
   }
 };
@@ -136,7 +136,7 @@ struct Pipeline {
   int* nlow;
   int* bmin;
   const Side* side = nullptr;  // second stream for Stage 6's independent pieces (plan capture, host path)
-  int* w0;          // [n] each row's first arc target (Stage 1's round 0 -> Stage 5's round 0)
+  int* w0;          // [3][n] each row's arc 0-2 targets (Stage 1's round 0 -> the sampling rounds of Stages 1, 5)
   bool w0_valid = false;
 
   Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
@@ -202,7 +202,7 @@ struct Pipeline {
     mk(0);
     const bool round0 = build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, comp, fe, prop, nlow, w0);
     w0_valid = round0;
-    stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args());
+    stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args(), round0 ? w0 : nullptr);
     mk(1);
     enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
   }

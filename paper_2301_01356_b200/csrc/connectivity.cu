@@ -46,6 +46,8 @@ enum : int { PRED_NONE = 0, PRED_SKEL = 1, PRED_MASK = 2 };
 struct PredData {
   const int4* rec;        // PRED_SKEL: {first, last, parent, fence}
   const int* w0;          // PRED_SKEL (optional): each row's first arc target, recorded by Stage 1's k_chunk_rows
+  const int* warc;        // (optional) [3][n]: targets of arcs 0, 1, 2 of each row (-1: none) for the sampling
+                          // rounds, recorded by k_chunk_rows; nullptr: read the adjacency
   const uint8_t* mask;    // PRED_MASK: per-slot keep byte
   const int64_t* off;     // PRED_MASK: to find the canonical (u < w) slot
   const uint32_t* adj;
@@ -204,6 +206,11 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
           if (c < v) fe[v] = make_int2(v, c);
           w0[v] = first;  // Stage 5's round-0 arc (coalesced; saves it a cold sector per row)
         }
+        // arcs 1 and 2 for the sampling rounds of Stages 1 and 5 (same
+        // sector as arc 0: the proposers then read 4 coalesced bytes instead
+        // of an offsets pair and a cold 32-byte adjacency sector per row)
+        w0[(int64_t)n + v] = re - rs > 1 ? (int)__ldg(adj + rs + 1) : -1;
+        w0[2 * (int64_t)n + v] = re - rs > 2 ? (int)__ldg(adj + rs + 2) : -1;
         comp[v] = c;
         prop[v] = ~0ull;
       }
@@ -325,19 +332,25 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
     uint64_t t = ((uint64_t)kPerRoot * (uint64_t)(R > 0 ? R : 0) << 24) / (uint64_t)n;
     if (t < thr) thr = (uint32_t)t;
   }
+  const int* wr = (kPred != PRED_MASK && pd.warc && round <= 2) ? pd.warc + (int64_t)round * n : nullptr;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     if (thr < (1u << 24) && (hash32((uint32_t)v * 0x9E3779B1u + (uint32_t)round) >> 8) >= thr) continue;
     int w;
-    int64_t s = __ldg(off + v) + round;
+    int64_t s = -1;
     int4 rv;
     if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
     if (kPred == PRED_SKEL && skel_parent) {  // this round samples the plain parent edge
       if (rv.z < 0 || rv.w != 0) continue;
       w = rv.z;
-      s = -1;
     } else {
-      if (s >= __ldg(off + v + 1)) continue;
-      w = (int)__ldg(adj + s);
+      if (wr) {
+        w = __ldg(wr + v);
+        if (w < 0) continue;
+      } else {
+        s = __ldg(off + v) + round;
+        if (s >= __ldg(off + v + 1)) continue;
+        w = (int)__ldg(adj + s);
+      }
       if (!keep<kPred>(pd, v, rv, w, s)) continue;
     }
     // flat after a compress; otherwise (rounds >= 1 hook root -> root only,
@@ -355,9 +368,15 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
   }
 }
 
+// (the proposer u's sampled arc: warc[round][u] when recorded, else adj[off[u] + round])
+__device__ __forceinline__ int sampled_arc(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                           const int* __restrict__ warc, int n, int round, int u) {
+  return (warc && round <= 2) ? __ldg(warc + (int64_t)round * n + u) : (int)__ldg(adj + __ldg(off + u) + round);
+}
+
 template <bool kRecord>
 __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
-                         unsigned long long* prop, int2* fe, int* hooks, int rbase) {
+                         unsigned long long* prop, int2* fe, int* hooks, int rbase, const int* __restrict__ warc) {
   pdl_enter();
   if (skip_round(hooks, round, rbase, n)) return;
   int hooked = 0;
@@ -371,7 +390,7 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
     hooked++;
     if (kRecord) {
       int u = (int)(key & 0xffffffffull);
-      fe[v] = make_int2(u, (int)__ldg(adj + __ldg(off + u) + round));
+      fe[v] = make_int2(u, sampled_arc(off, adj, warc, n, round, u));
     }
   }
   block_count_add(hooks + round, hooked);
@@ -414,7 +433,7 @@ template <bool kJump, bool kAccept = false, bool kRecord = false>
 __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable, RootInit ri,
                            const int* hooks, int round, int rbase, unsigned long long* prop = nullptr,
                            int* hooks_out = nullptr, int2* fe = nullptr, const int64_t* __restrict__ off = nullptr,
-                           const uint32_t* __restrict__ adj = nullptr) {
+                           const uint32_t* __restrict__ adj = nullptr, const int* __restrict__ warc = nullptr) {
   pdl_enter();
   int roots = 0;
   int hooked = 0;
@@ -437,7 +456,7 @@ __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, boo
           hooked++;
           if (kRecord) {
             const int u = (int)(key & 0xffffffffull);
-            fe[v] = make_int2(u, (int)__ldg(adj + __ldg(off + u) + round));
+            fe[v] = make_int2(u, sampled_arc(off, adj, warc, n, round, u));
           }
         }
       }
@@ -727,7 +746,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
              ((opt(OPT_SKEL_PARENT) >> r) & 1) != 0, kBase);
       note(K_PROPOSE);
       if (!fold) {
-        launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase);
+        launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase, pd.warc);
         note(K_ACCEPT);
       }
     }
@@ -737,12 +756,13 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       const int* skip_hooks = r >= kBase ? (const int*)hooks : nullptr;
       if (fold) {
         launch(k_compress<false, true, kRecord>, gres, B, 0, st, comp, g.n, (int*)nullptr, last_round ? sc : nullptr,
-               opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase, prop, hooks + r, fe, g.off, g.adj);
+               opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase, prop, hooks + r, fe, g.off, g.adj,
+               pd.warc);
       } else {
         launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
                last_round ? sc : nullptr, opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase,
                (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
-               (const uint32_t*)nullptr);
+               (const uint32_t*)nullptr, (const int*)nullptr);
       }
       note(K_COMPRESS);
     }
@@ -768,7 +788,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   }
   launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0, 0,
          (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
-         (const uint32_t*)nullptr);  // final root count (= components)
+         (const uint32_t*)nullptr, (const int*)nullptr);  // final root count (= components)
   note(K_COMPRESS);
 }
 
@@ -831,7 +851,7 @@ void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t s
   const int B = 256;
   launch(k_compress<true>, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
          (const int*)nullptr, 0, 0, (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr,
-         (const int64_t*)nullptr, (const uint32_t*)nullptr);
+         (const int64_t*)nullptr, (const uint32_t*)nullptr, (const int*)nullptr);
   note(K_COMPRESS);
 }
 
@@ -847,8 +867,10 @@ void widen_offsets(const int* src, int64_t* dst, int64_t n, cudaStream_t st) {
 }
 
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st,
-                   bool round0_done, RootInit ri) {
-  run_cc<PRED_NONE, true>(g, comp, fe, prop, PredData{}, sc, 0, st, round0_done, ri);
+                   bool round0_done, RootInit ri, const int* warc) {
+  PredData pd{};
+  pd.warc = warc;
+  run_cc<PRED_NONE, true>(g, comp, fe, prop, pd, sc, 0, st, round0_done, ri);
 }
 
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
@@ -856,6 +878,7 @@ void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned lo
   PredData pd{};
   pd.rec = rec;
   pd.w0 = w0;
+  pd.warc = w0;  // (rows [n, 3n): arcs 1 and 2; k_chunk_rows recorded all three)
   run_cc<PRED_SKEL, false>(g, label, nullptr, prop, pd, sc, 8, st);
 }
 

@@ -101,8 +101,9 @@ void rooting_roots(int n, const int* comp, Rooting& R, Scalars* sc, cudaStream_t
 void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc, cudaStream_t st);
 void masked_cc(const Graph& g, const uint8_t* mask, int* comp, int2* fe, unsigned long long* prop, Scalars* sc,
                cudaStream_t st);
+// (warc: [3][n] targets of each row's arcs 0-2 recorded by k_chunk_rows, or nullptr)
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st,
-                   bool round0_done = false, RootInit ri = RootInit{});
+                   bool round0_done = false, RootInit ri = RootInit{}, const int* warc = nullptr);
 // Stage 1 over a streamed edge array (fbcc_run_host): identity init, one link
 // pass per arrived chunk range [q0, q1) of kItems-arc chunks, final compress
 void stage1_stream_begin(const Graph& g, int* comp, cudaStream_t st);
@@ -132,7 +133,7 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
 void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
                   int* bmin,
                   cudaStream_t st);
-// (w0: each row's first arc target, recorded by k_chunk_rows' round 0; nullptr: read adj)
+// (w0: [3][n] each row's first three arc targets, recorded by k_chunk_rows' round 0; nullptr: read adj)
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
                         cudaStream_t st, const int* w0 = nullptr);
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
