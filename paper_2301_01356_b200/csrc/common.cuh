@@ -169,6 +169,17 @@ __device__ __forceinline__ int4 ld_stream4(const int4* p) {
   return r;
 }
 
+// One 8-arc chunk of the adjacency stream: a single 256-bit load (sm_100
+// LDG.256, 32-byte aligned), not allocated in L1 and marked evict-first in
+// L2 -- the 4m-byte stream then does not push out the arrays the arc passes
+// gather from (first[], comp[], label[]), which would otherwise compete with
+// it for the 126 MB L2.
+__device__ __forceinline__ void ld_chunk8(const uint32_t* p, uint32_t* w) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "l"(p));
+}
+
 // ---------------------------------------------------------------------------
 // hashing (splitter choice, sampling)
 // ---------------------------------------------------------------------------
@@ -236,17 +247,14 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
                                                  const int* __restrict__ crow,
                                                  int n, int64_t m, Visitor& vis) {
   const int64_t nchunks = (m + kItems - 1) / kItems;
-  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 31) == 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nchunks; q += stride) {
     int64_t a0 = q * kItems;
     int64_t a1 = a0 + kItems < m ? a0 + kItems : m;
     uint32_t w[kItems];
     if (vec_ok && a1 - a0 == kItems) {
-      int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
-      int4 y = ld_stream4(reinterpret_cast<const int4*>(adj + a0 + 4));
-      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-      w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+      ld_chunk8(adj + a0, w);
     } else {
 #pragma unroll
       for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;

@@ -805,16 +805,13 @@ __global__ void __launch_bounds__(256) k_link_range(const int64_t* __restrict__ 
                                                     const int* __restrict__ crow, int n, int64_t m, int64_t q0,
                                                     int64_t q1, int* comp, int2* fe) {
   pdl_enter();
-  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 31) == 0);
   for (int64_t q = q0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < q1; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a0 = q * kItems;
     const int64_t a1 = a0 + kItems < m ? a0 + kItems : m;
     uint32_t w[kItems];
     if (vec_ok && a1 - a0 == kItems) {
-      int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
-      int4 y = ld_stream4(reinterpret_cast<const int4*>(adj + a0 + 4));
-      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-      w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+      ld_chunk8(adj + a0, w);
     } else {
 #pragma unroll
       for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;

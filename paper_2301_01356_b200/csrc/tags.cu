@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256, kWGatherMinBlocks) k_w_gather(const int64
   // this pass over the same arcs)
   constexpr bool kCount = !kExact;
   const int64_t nchunks = (m + kItems - 1) / kItems;
-  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 15) == 0);
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 31) == 0);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // warp-uniform trip count (the shuffles below need the whole warp)
@@ -111,10 +111,7 @@ __global__ void __launch_bounds__(256, kWGatherMinBlocks) k_w_gather(const int64
       const int a1 = a0 + kItems < (int)m ? a0 + kItems : (int)m;
       uint32_t w[kItems];
       if (vec_ok && a1 - a0 == kItems) {
-        int4 x = ld_stream4(reinterpret_cast<const int4*>(adj + a0));
-        int4 y = ld_stream4(reinterpret_cast<const int4*>(adj + a0 + 4));
-        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-        w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+        ld_chunk8(adj + a0, w);
       } else {
 #pragma unroll
         for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;
@@ -199,17 +196,31 @@ __global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ 
 // ---------------------------------------------------------------------------
 // tile pass
 // ---------------------------------------------------------------------------
-constexpr int kTileThreads = 512;
+// One persistent CTA per SM walks its tiles (blockIdx.x, + gridDim.x, ...).
+// Each 4096-position tile of AP (64 KB of 16-byte records) is staged into
+// shared memory by ONE bulk async copy (cp.async.bulk, completion on an
+// mbarrier), double-buffered: the copy of the CTA's next tile but one is
+// issued as soon as a buffer is free, so the DRAM stream runs under the
+// scans and queries of the current tile instead of every thread stalling on
+// its own loads.  The staged record carries both the tile values (w1, w2)
+// and the query (v or ~v, partner position): nothing is read from global
+// memory twice.
+constexpr int kTileThreads = 1024;
 constexpr int kSub = 32;
 constexpr int kNSub = kTile / kSub;  // 128
 constexpr int kSubLev = 32 - __builtin_clz(kNSub);  // levels 0..log2(kNSub) (8 for 128 sub-blocks)
-constexpr size_t kTileSmem = sizeof(int2) * (3 * kTile + kSubLev * kNSub);
+constexpr int kTileBytes = kTile * (int)sizeof(int4);  // 64 KB
+constexpr size_t kTileSmem = 2 * (size_t)kTileBytes + sizeof(int2) * (2 * kTile + kSubLev * kNSub) + 16;
 
 struct TileSmem {
-  int2* raw;
+  const int4* raw;  // the staged tile: {w1, w2, v or ~v, partner}
   int2* pre;
   int2* suf;
   int2* st;  // [kSubLev][kNSub]
+  __device__ __forceinline__ int2 val(int i) const {
+    const int4 r = raw[i];
+    return make_int2(r.x, r.y);
+  }
   __device__ __forceinline__ int2 st_query(int i, int j) const {  // sub-blocks i..j, i <= j
     int k = 31 - __clz(j - i + 1);
     return comb(st[k * kNSub + i], st[k * kNSub + j - (1 << k) + 1]);
@@ -217,8 +228,8 @@ struct TileSmem {
   __device__ __forceinline__ int2 range(int a, int b) const {  // positions a..b in tile
     int sa = a >> 5, sb = b >> 5;
     if (sa == sb) {
-      int2 r = raw[a];
-      for (int i = a + 1; i <= b; i++) r = comb(r, raw[i]);
+      int2 r = val(a);
+      for (int i = a + 1; i <= b; i++) r = comb(r, val(i));
       return r;
     }
     int2 r = comb(suf[a], pre[b]);
@@ -239,6 +250,27 @@ struct TileSmem {
   }
 };
 
+// bulk async copy global -> shared, completing on an mbarrier (sm_90+ TMA
+// engine, 1-D: no tensor map)
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the buffer first
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(gsrc), "r"(bytes), "r"(b) : "memory");
+}
+
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(b), "r"(parity) : "memory");
+  }
+}
+
 constexpr int kTableOneCta = 16384;
 
 __device__ __forceinline__ void table_levels(int2* table, int ntile, int tlev) {
@@ -256,29 +288,48 @@ __device__ __forceinline__ void table_levels(int2* table, int ntile, int tlev) {
 
 // (sc != nullptr: the last block to finish also builds every level of the
 // tile-extreme sparse table -- k_table_all's work, one launch fewer)
-__global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int4* __restrict__ AP,
+__global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict__ AP,
                                                           int64_t N, int ntile, int2* __restrict__ lh1,
                                                           int2* __restrict__ lh2, int2* __restrict__ table0, Scalars* sc, int tlev) {
   pdl_enter();
-  extern __shared__ int2 smem[];
+  extern __shared__ __align__(128) unsigned char tsm[];
+  int4* buf0 = reinterpret_cast<int4*>(tsm);
+  int4* buf1 = reinterpret_cast<int4*>(tsm + kTileBytes);
+  int2* aux = reinterpret_cast<int2*>(tsm + 2 * kTileBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(aux + 2 * kTile + kSubLev * kNSub);  // 2 mbarriers
   TileSmem S;
-  S.raw = smem;
-  S.pre = smem + kTile;
-  S.suf = smem + 2 * kTile;
-  S.st = smem + 3 * kTile;
+  S.pre = aux;
+  S.suf = aux + kTile;
+  S.st = aux + 2 * kTile;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+  const int G = gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; i++) {
+      const uint32_t b = (uint32_t)__cvta_generic_to_shared(bars + i);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (blockIdx.x < ntile) bulk_load(buf0, AP + (int64_t)blockIdx.x * kTile, kTileBytes, bars);
+    if (blockIdx.x + G < ntile) bulk_load(buf1, AP + (int64_t)(blockIdx.x + G) * kTile, kTileBytes, bars + 1);
+  }
+  uint32_t parity = 0;  // bit b: phase of buffer b's barrier
+  int k = 0;
+  for (int tile = blockIdx.x; tile < ntile; tile += G, k++) {
+    const int b = k & 1;
+    const int4* T = b ? buf1 : buf0;
+    S.raw = T;
+    bar_wait(bars + b, (parity >> b) & 1u);
+    parity ^= 1u << b;
     const int64_t base = (int64_t)tile * kTile;
-    // 1. stage the tile; warp scans per 32-position sub-block
+    // 1. warp scans per 32-position sub-block (positions past N: filler)
     for (int sb = warp; sb < kNSub; sb += kTileThreads / 32) {
-      int p = sb * kSub + lane;
+      const int p = sb * kSub + lane;
       int2 x = filler();
-      if (base + p < N) {
-        int4 ap = __ldg(AP + base + p);
-        x = make_int2(ap.x, ap.y);
-      }
-      S.raw[p] = x;
+      if (base + p < N) x = S.val(p);
       int2 pr = x, su = x;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -293,29 +344,31 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(const int4* __restrict
     }
     __syncthreads();
     // 2. sparse table over the 128 sub-block extremes
-    for (int k = 1; k < kSubLev; k++) {
+    for (int lv = 1; lv < kSubLev; lv++) {
       if (threadIdx.x < kNSub) {
-        int i = threadIdx.x, j = i + (1 << (k - 1));
-        int2 a = S.st[(k - 1) * kNSub + i];
-        S.st[k * kNSub + i] = (j < kNSub) ? comb(a, S.st[(k - 1) * kNSub + j]) : a;
+        int i = threadIdx.x, j = i + (1 << (lv - 1));
+        int2 a = S.st[(lv - 1) * kNSub + i];
+        S.st[lv * kNSub + i] = (j < kNSub) ? comb(a, S.st[(lv - 1) * kNSub + j]) : a;
       }
       __syncthreads();
     }
     if (threadIdx.x == 0) table0[tile] = S.st[(kSubLev - 1) * kNSub];
     // 3. answer the queries that start or end here
     for (int p = threadIdx.x; p < kTile; p += kTileThreads) {
-      int64_t gp = base + p;
+      const int64_t gp = base + p;
       if (gp >= N) break;
-      int4 ap = __ldg(AP + gp);  // L1 hit: the tile was just staged
-      int2 q = make_int2(ap.z, ap.w);
+      const int4 ap = T[p];
+      const int2 q = make_int2(ap.z, ap.w);
       if (q.x >= 0) {  // entry position of v = q.x; partner = last[v]
-        int64_t rel = (int64_t)q.y - base;
+        const int64_t rel = (int64_t)q.y - base;
         lh1[q.x] = (rel < kTile) ? S.range(p, (int)rel) : S.to_end(p);
       } else if ((int64_t)q.y < base) {  // exit position of ~q.x, entry in an earlier tile
         lh2[~q.x] = S.from_start(p);
       }
     }
-    __syncthreads();
+    __syncthreads();  // buffer b and the scan arrays are free
+    if (threadIdx.x == 0 && tile + 2 * G < ntile)
+      bulk_load(b ? buf1 : buf0, AP + (int64_t)(tile + 2 * G) * kTile, kTileBytes, bars + b);
   }
   if (sc) {
     __shared__ bool last;
@@ -384,8 +437,8 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
   // (the table in k_tile's last block when it fits one CTA and a ticket word exists)
   Scalars* tsc = (sc && T.ntile <= kTableOneCta && T.tlev > 1) ? sc : nullptr;
-  launch(k_tile, grid_for(T.ntile, 1, 2), kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile, T.lh1,
-         T.lh2, T.table, tsc, T.tlev);
+  launch(k_tile, T.ntile < kNumSMs ? T.ntile : kNumSMs, kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile,
+         T.lh1, T.lh2, T.table, tsc, T.tlev);
   note(K_TILE);
   if (tsc) {
   } else if (T.ntile <= kTableOneCta) {
