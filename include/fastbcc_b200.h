@@ -50,6 +50,7 @@ extern "C" {
 #define FBCC_OP_COMPUTE_TAGS 4         /* a = n, b = m  */
 #define FBCC_OP_EXTRACT_BCCS 5         /* a = n         */
 #define FBCC_OP_SYMMETRIZE 6           /* a = k pairs, b = n */
+#define FBCC_OP_CLASSIFY_EDGES 7       /* a = n, b = m  */
 
 /* run flags */
 #define FBCC_FLAG_TIMING 1u   /* record per-stage CUDA-event times in stats   */
@@ -229,6 +230,16 @@ int fbcc_extract_bccs(const int32_t *label, const int32_t *head, int64_t n,
 int fbcc_symmetrize(const int64_t *u, const int64_t *v, int64_t k, int64_t n,
                     int64_t *offsets, uint32_t *edges, int64_t *m_out,
                     void *ws, size_t ws_bytes, void *stream);
+
+/* classify_edge(forest, tags, u, v) bcc.py:54-70 for every slot of the CSR
+   against a given rooted forest (parent/first/last) and its tags (low/high):
+   cls[m] = EdgeClass (bcc.py:45-51): 0 PLAIN_TREE, 1 FENCE_TREE, 2 BACK,
+   3 CROSS.  An endpoint outside [0, n) gives FBCC_ERR_RANGE. */
+int fbcc_classify_edges(const int64_t *offsets, const uint32_t *edges, int64_t n,
+                        int64_t m, const int32_t *parent, const int32_t *first,
+                        const int32_t *last, const int32_t *low,
+                        const int32_t *high, int8_t *cls, void *ws,
+                        size_t ws_bytes, void *stream);
 
 /* Name of a kernel kind reported in fbcc_stats.prof_kind. */
 const char *fbcc_kernel_name(int kind);

@@ -150,8 +150,10 @@ OP_BUILD_EULER_TOUR = 3
 OP_COMPUTE_TAGS = 4
 OP_EXTRACT_BCCS = 5
 OP_SYMMETRIZE = 6
+OP_CLASSIFY_EDGES = 7
 OP_EXPORTS = ("fbcc_op_workspace_bytes", "fbcc_connected_components", "fbcc_list_ranking",
-              "fbcc_build_euler_tour", "fbcc_compute_tags", "fbcc_extract_bccs", "fbcc_symmetrize")
+              "fbcc_build_euler_tour", "fbcc_compute_tags", "fbcc_extract_bccs", "fbcc_symmetrize",
+              "fbcc_classify_edges")
 
 
 def bind_ops(L):
@@ -165,6 +167,7 @@ def bind_ops(L):
     L.fbcc_compute_tags.argtypes = [P, P, I64, I64, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
     L.fbcc_extract_bccs.argtypes = [P, P, I64, P, P, ctypes.POINTER(I64), P, ctypes.c_size_t, P]
     L.fbcc_symmetrize.argtypes = [P, P, I64, I64, P, P, ctypes.POINTER(I64), P, ctypes.c_size_t, P]
+    L.fbcc_classify_edges.argtypes = [P, P, I64, I64, P, P, P, P, P, P, P, ctypes.c_size_t, P]
     for name in OP_EXPORTS[1:]:
         getattr(L, name).restype = ctypes.c_int
 

@@ -673,6 +673,8 @@ static size_t op_bytes(int op, int64_t a, int64_t b) {
       return kOpHead + op_extract_bytes(a);
     case FBCC_OP_SYMMETRIZE:  // a = k pairs
       return kOpHead + op_symmetrize_bytes(a);
+    case FBCC_OP_CLASSIFY_EDGES:  // a = n, b = m (error bits only)
+      return kOpHead;
     default:
       return 0;
   }
@@ -818,6 +820,24 @@ int fbcc_symmetrize(const int64_t* u, const int64_t* v, int64_t k, int64_t n, in
   int rc = op_finish(sc, st, &host);
   *m_out = 2 * (int64_t)host.num_edges;
   return rc;
+}
+
+int fbcc_classify_edges(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, const int32_t* parent,
+                        const int32_t* first, const int32_t* last, const int32_t* low, const int32_t* high,
+                        int8_t* cls, void* ws, size_t ws_bytes, void* stream) {
+  const Options opts = options_snapshot();
+  OptScope scope(&opts);
+  int rc = check_sizes(n, m);
+  if (rc) return rc;
+  if (n == 0 || m == 0) return FBCC_OK;
+  if (!offsets || !edges || !parent || !first || !last || !low || !high || !cls || !ws) return FBCC_ERR_ARG;
+  if (ws_bytes < op_bytes(FBCC_OP_CLASSIFY_EDGES, n, m)) return FBCC_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scalars* sc = op_start(ws, st);
+  Graph g{offsets, edges, (int)n, m, nullptr};
+  op_classify_edges(g, parent, first, last, low, high, cls, sc, st);
+  Scalars host;
+  return op_finish(sc, st, &host);
 }
 
 }  // extern "C"

@@ -517,3 +517,56 @@ int op_compute_tags(const Graph& g, const int* parent, const int* first, const i
 }
 
 }  // namespace fbcc
+
+// ---------------------------------------------------------------------------
+// classify_edge (bcc.py:54-70) for every slot, against a given rooted forest
+// and its tags: one thread per 8-arc chunk (its row by binary search over the
+// offsets, then galloping), EdgeClass codes PLAIN_TREE 0, FENCE_TREE 1,
+// BACK 2, CROSS 3 (bcc.py:45-51).
+// ---------------------------------------------------------------------------
+namespace fbcc {
+
+__global__ void k_classify(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int64_t m,
+                           const int* __restrict__ parent, const int* __restrict__ first,
+                           const int* __restrict__ last, const int* __restrict__ low, const int* __restrict__ high,
+                           int8_t* __restrict__ cls, Scalars* sc) {
+  pdl_enter();
+  const int64_t nchunks = (m + kItems - 1) / kItems;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nchunks; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a0 = q * kItems, a1 = a0 + kItems < m ? a0 + kItems : m;
+    int u = row_of(off, 0, n - 1, a0);
+    int64_t re = __ldg(off + u + 1);
+    for (int64_t a = a0; a < a1; a++) {
+      if (a >= re) {
+        u = next_row(off, u, n, a);
+        re = __ldg(off + u + 1);
+      }
+      const int v = (int)__ldg(adj + a);
+      if (v < 0 || v >= n) {
+        atomicOr(&sc->err, 1);
+        cls[a] = -1;
+        continue;
+      }
+      const int pu = __ldg(parent + u), pv = __ldg(parent + v);
+      int8_t c;
+      if (pv == u || pu == v) {  // tree edge (bcc.py:61-66)
+        const int ch = pv == u ? v : u, pa = pv == u ? u : v;
+        c = (__ldg(low + ch) >= __ldg(first + pa) && __ldg(high + ch) <= __ldg(last + pa)) ? 1 : 0;
+      } else {
+        const int fu = __ldg(first + u), lu = __ldg(last + u), fv = __ldg(first + v), lv = __ldg(last + v);
+        c = ((fu <= fv && lv <= lu) || (fv <= fu && lu <= lv)) ? 2 : 3;  // back / cross (bcc.py:67-70)
+      }
+      cls[a] = c;
+    }
+  }
+}
+
+int op_classify_edges(const Graph& g, const int* parent, const int* first, const int* last, const int* low,
+                      const int* high, int8_t* cls, Scalars* sc, cudaStream_t st) {
+  if (g.m == 0) return 0;
+  launch(k_classify, grid_for((g.m + kItems - 1) / kItems, 256), 256, 0, st, g.off, g.adj, g.n, g.m, parent, first,
+         last, low, high, cls, sc);
+  return 0;
+}
+
+}  // namespace fbcc

@@ -23,4 +23,7 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
 int op_compute_tags(const Graph& g, const int* parent, const int* first, const int* last, int* w1, int* w2, int* low,
                     int* high, void* ws, size_t ws_bytes, cudaStream_t st, bool dry, size_t* need);
 
+int op_classify_edges(const Graph& g, const int* parent, const int* first, const int* last, const int* low,
+                      const int* high, int8_t* cls, Scalars* sc, cudaStream_t st);
+
 }  // namespace fbcc

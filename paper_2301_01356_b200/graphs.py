@@ -175,8 +175,9 @@ def write_bin(g: Graph, path) -> None:
 
 
 def load_bin(path, device=None) -> Graph:
-    """Read a .bin CSR; with ``device`` set, the arrays go straight from a
-    pinned staging buffer to HBM and a device Graph is returned."""
+    """Read a .bin CSR (graphs.py:173-204).  With ``device`` set, the file is
+    read straight into page-locked staging buffers (no intermediate host
+    copy) and copied asynchronously to HBM; a device Graph is returned."""
     import warnings
 
     with open(path, "rb") as f:
@@ -185,11 +186,22 @@ def load_bin(path, device=None) -> Graph:
             raise ValueError(f"{path}: truncated header (need {_HEADER_BYTES} bytes)")
         n, m, size_field = (int(x) for x in header)
         want = expected_bin_size(n, m)
-        offsets = np.fromfile(f, dtype="<u8", count=n + 1)
-        edges = np.fromfile(f, dtype="<u4", count=m)
+        if device is None:
+            offsets = np.fromfile(f, dtype="<u8", count=n + 1)
+            edges = np.fromfile(f, dtype="<u4", count=m)
+            got_o, got_e = offsets.size, edges.size
+        else:
+            import torch
+
+            off_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+            adj_h = torch.empty(m, dtype=torch.int32, pin_memory=True)
+            offsets = off_h.numpy()
+            edges = adj_h.numpy().view(np.uint32)
+            got_o = f.readinto(memoryview(offsets).cast("B")) // 8
+            got_e = f.readinto(memoryview(edges).cast("B")) // 4 if m else 0
         extra = f.read(1)
-    if offsets.size != n + 1 or edges.size != m or extra:
-        have = _HEADER_BYTES + offsets.size * 8 + edges.size * 4 + len(extra)
+    if got_o != n + 1 or got_e != m or extra:
+        have = _HEADER_BYTES + got_o * 8 + got_e * 4 + len(extra)
         raise ValueError(f"{path}: size mismatch, expected {want} bytes for n={n} m={m}, "
                          f"got {have}{'+' if extra else ''}")
     if size_field != want:
@@ -201,8 +213,7 @@ def load_bin(path, device=None) -> Graph:
         raise ValueError(f"{path}: offsets must run from 0 to m")
     if device is None:
         return Graph(offsets.astype(np.int64), edges)
-    import torch
-
-    off_t = torch.from_numpy(offsets.view(np.int64)).pin_memory().to(device, non_blocking=True)
-    adj_t = torch.from_numpy(edges.view(np.int32)).pin_memory().to(device, non_blocking=True)
+    off_t = off_h.to(device, non_blocking=True)
+    adj_t = adj_h.to(device, non_blocking=True)
+    torch.cuda.current_stream(off_t.device).synchronize()  # the staging buffers may be reused after this
     return Graph.from_device(off_t, adj_t)

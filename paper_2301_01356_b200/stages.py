@@ -245,20 +245,20 @@ def skeleton_record(parent, first, last, low, high) -> np.ndarray:
 
 
 def classify_edges(g: Graph, forest: RootedForest, tags: VertexTags) -> np.ndarray:
-    """EdgeClass of every slot (bcc.py:54-70, vectorised): int8[m]."""
-    src = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(g.offsets))
-    dst = g.edges.astype(np.int64)
-    par, fst, lst = forest.parent, forest.first, forest.last
-    tree_down = par[dst] == src
-    tree_up = par[src] == dst
-    child = np.where(tree_down, dst, src)
-    pc = np.where(tree_down, src, dst)
-    fence = (tags.low[child] >= fst[pc]) & (tags.high[child] <= lst[pc])
-    anc = ((fst[src] <= fst[dst]) & (lst[dst] <= lst[src])) | ((fst[dst] <= fst[src]) & (lst[src] <= lst[dst]))
-    out = np.where(anc, EdgeClass.BACK, EdgeClass.CROSS).astype(np.int8)
-    tree = tree_down | tree_up
-    out[tree] = np.where(fence[tree], EdgeClass.FENCE_TREE, EdgeClass.PLAIN_TREE)
-    return out
+    """EdgeClass of every slot (classify_edge, bcc.py:54-70), computed on the
+    device (``fbcc_classify_edges``): int8[m] in CSR slot order."""
+    torch = _torch()
+    off, adj = _csr(g)
+    n, m = off.numel() - 1, adj.numel()
+    out = torch.empty(max(m, 1), dtype=torch.int8, device="cuda")
+    arrs = [_dev(a, torch.int32) for a in (forest.parent, forest.first, forest.last, tags.low, tags.high)]
+    ws = _ws(_lib.OP_CLASSIFY_EDGES, n, m)
+    rc = _lib.load().fbcc_classify_edges(off.data_ptr(), _ptr(adj), n, m, *[_ptr(a) for a in arrs],
+                                         out.data_ptr(), ws.data_ptr(), ws.numel(), _stream())
+    if rc == _lib.FBCC_ERR_RANGE:
+        raise ValueError("edge endpoint out of range")
+    _lib.check(rc)
+    return out[:m].cpu().numpy()
 
 
 def symmetrize_device(edges, n: int) -> Graph:

@@ -125,6 +125,61 @@ def corpus(fb):
     print(f"corpus: {len(names)} graphs, {int(np.sum(ns))} vertices, {int(np.sum(ms))} slots")
 
 
+def classify(fb):
+    """classify.npz: the reference's edge classes on the corpus, for the
+    reference's own rooted forest and tags stored in corpus.npz -- per upper
+    arc (u < v) in CSR order, EdgeClass values (bcc.py:45-51): PLAIN_TREE 0,
+    FENCE_TREE 1, BACK 2, CROSS 3.  Each class comes from bcc.classify_edge
+    (bcc.py:54-70) and is asserted equal to the first-principles
+    tests/oracles.py classify_edges_oracle (oracles.py:207-235)."""
+    import importlib.util
+
+    import oracles  # the reference's (its tests dir is on sys.path)
+    from fastbcc import bcc, euler_tour, graphs as rg, tagging
+
+    spec = importlib.util.spec_from_file_location("repo_conftest", REPO / "tests" / "conftest.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    c = mod.Corpus(HERE / "corpus.npz")
+    code = {"plain": 0, "fence": 1, "back": 2, "cross": 3}
+    cls_all, counts = [], []
+    for i, name, g in c.items():
+        n = g.n
+        gr = rg.Graph(g.offsets, g.edges)
+        parent, first, last = (c.get(i, k) for k in ("parent", "first", "last"))
+        roots = np.flatnonzero(parent == -1)
+        forest = euler_tour.RootedForest(parent, first, last, roots)
+        tags = tagging.VertexTags(*(c.get(i, k) for k in ("w1", "w2", "low", "high")))
+        want = oracles.classify_edges_oracle(gr, parent) if n else {}
+        out = []
+        for u in range(n):
+            for v in g.edges[g.offsets[u]:g.offsets[u + 1]]:
+                v = int(v)
+                if u > v:
+                    continue
+                k = int(bcc.classify_edge(forest, tags, u, v))
+                assert k == code[want[(u, v)]], (name, u, v)
+                out.append(k)
+        cls_all.append(np.array(out, np.int8))
+        counts.append(len(out))
+    np.savez_compressed(HERE / "classify.npz", cls=np.concatenate(cls_all), E=np.array(counts, np.int64))
+    print(f"classify: {len(counts)} graphs, {int(np.sum(counts))} edges")
+    # extract.npz: the reference's extract_bccs (bcc.py:199-219) on the
+    # reference's labeling of every corpus graph
+    verts, blens, nblocks = [], [], []
+    for i, name, g in c.items():
+        lab = bcc.BccLabeling(c.get(i, "label"), c.get(i, "head"), c.get(i, "num_bccs"),
+                              c.get(i, "num_components"), bcc.StepTimings())
+        blocks = bcc.extract_bccs(lab)
+        nblocks.append(len(blocks))
+        for b in blocks:
+            verts.append(np.asarray(b, np.int32))
+            blens.append(len(b))
+    np.savez_compressed(HERE / "extract.npz", verts=np.concatenate(verts) if verts else np.empty(0, np.int32),
+                        blen=np.array(blens, np.int64), nblocks=np.array(nblocks, np.int64))
+    print(f"extract: {int(np.sum(nblocks))} blocks")
+
+
 def listrank(fb):
     from fastbcc.euler_tour import list_ranking
 
@@ -199,8 +254,12 @@ if __name__ == "__main__":
     ap.add_argument("--skip-configs", action="store_true")
     ap.add_argument("--configs", default="1,2,3")
     ap.add_argument("--only-configs", action="store_true")
+    ap.add_argument("--only-classify", action="store_true")
     a = ap.parse_args()
     fb = import_reference()
+    if a.only_classify:
+        classify(fb)
+        sys.exit(0)
     if not a.only_configs:
         corpus(fb)
         listrank(fb)

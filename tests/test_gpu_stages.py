@@ -118,15 +118,22 @@ def test_compute_tags_on_reference_forest(corpus):
     assert got == {(0, 1): 1, (1, 2): 0, (2, 3): 0, (0, 3): 2}
 
 
-def test_extract_bccs_device_matches_host(corpus):
+def test_extract_bccs_device_matches_reference(corpus):
+    """fbcc_extract_bccs == the reference's extract_bccs (bcc.py:199-219) on
+    every corpus labeling (tests/golden/extract.npz, produced by running the
+    reference) -- and the host mirror agrees too."""
+    z = np.load(GOLDEN / "extract.npz")
+    bo = np.concatenate([[0], np.cumsum(z["nblocks"])])
+    vo = np.concatenate([[0], np.cumsum(z["blen"])])
     for i, name, g in corpus.items():
         lab = BccLabeling(corpus.get(i, "label"), corpus.get(i, "head"), corpus.get(i, "num_bccs"),
                           corpus.get(i, "num_components"), StepTimings())
-        want = extract_bccs(lab)
+        want = [z["verts"][vo[b]:vo[b + 1]] for b in range(bo[i], bo[i + 1])]
         got = stages.extract_bccs_device(lab.label, lab.head)
-        assert len(got) == len(want) == corpus.get(i, "num_bccs"), name
-        for a, b in zip(got, want):
-            assert np.array_equal(a, b), name
+        host = extract_bccs(lab)
+        assert len(got) == len(want) == len(host) == corpus.get(i, "num_bccs"), name
+        for a, b, c in zip(got, want, host):
+            assert np.array_equal(a, b) and np.array_equal(c, b), name
 
 
 def test_symmetrize_device(corpus):
@@ -171,3 +178,55 @@ def test_rmat_device_generator_matches_numpy():
     u1, v1 = workloads.rmat_pairs_device(scale=12, edge_factor=16, seed=0, chunk=5000)
     assert np.array_equal(u0, u1.cpu().numpy())
     assert np.array_equal(v0, v1.cpu().numpy())
+
+
+def test_classify_edges_device_matches_reference(corpus):
+    """fbcc_classify_edges == the reference's classify_edge (bcc.py:54-70) on
+    every edge of the corpus, for the reference's forest and tags
+    (tests/golden/classify.npz, made by tests/golden/make_golden.py); both
+    slots of an edge get the same class."""
+    z = np.load(GOLDEN / "classify.npz")
+    eo = np.concatenate([[0], np.cumsum(z["E"])])
+    for i, name, g in corpus.items():
+        forest = stages.RootedForest(corpus.get(i, "parent"), corpus.get(i, "first"), corpus.get(i, "last"),
+                                     np.flatnonzero(corpus.get(i, "parent") == -1))
+        tags = stages.VertexTags(*(corpus.get(i, k) for k in ("w1", "w2", "low", "high")))
+        cls = stages.classify_edges(g, forest, tags)
+        assert cls.shape == (g.m,), name
+        src = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(g.offsets))
+        dst = g.edges.astype(np.int64)
+        up = src < dst
+        assert np.array_equal(cls[up], z["cls"][eo[i]:eo[i + 1]]), name
+        # the reverse slot of every edge: same class
+        key_up = src[up] * (g.n + 1) + dst[up]
+        key_dn = dst[~up] * (g.n + 1) + src[~up]
+        order = np.argsort(key_up)
+        pos = order[np.searchsorted(key_up[order], key_dn)]
+        assert np.array_equal(cls[~up], cls[up][pos]), name
+
+
+def test_load_bin_to_device_roundtrip(tmp_path, config_meta):
+    """load_bin(path, device=...) (graphs.py:173-204): the .bin lands in
+    pinned staging buffers and goes straight to HBM; fast_bcc on the device
+    graph reproduces the reference's config-1 outputs."""
+    import hashlib
+
+    import torch
+
+    import workloads
+    from paper_2301_01356_b200 import fast_bcc
+    from paper_2301_01356_b200.graphs import load_bin, write_bin
+
+    g = workloads.make("1")
+    path = tmp_path / "config1.bin"
+    write_bin(g, path)
+    d = load_bin(path, device="cuda")
+    off, adj = d._dev
+    assert off.is_cuda and adj.is_cuda and off.dtype == torch.int64
+    assert np.array_equal(off.cpu().numpy(), g.offsets)
+    assert np.array_equal(adj.cpu().numpy().view(np.uint32), g.edges)
+    lab = fast_bcc(d)
+    meta = config_meta["1"]
+    assert lab.num_bccs == meta["num_bccs"] and lab.num_components == meta["num_components"]
+    assert hashlib.sha256(np.ascontiguousarray(lab.edge_label).tobytes()).hexdigest() == meta["edge_label_sha256"]
+    assert hashlib.sha256(np.ascontiguousarray(lab.label).tobytes()).hexdigest() == meta["label_sha256"]

@@ -153,3 +153,34 @@ def test_config_digests(oracle_mod, config_meta, name, parallel):
     assert _sha(r["head"]) == meta["head_sha256"]
     assert _sha(r["is_ap"]) == meta["is_ap_sha256"]
     assert _sha(r["edge_label"]) == meta["edge_label_sha256"]
+
+
+def _classes_from_definition(g, parent, first, last, low, high):
+    """classify_edge (bcc.py:54-70) restated in numpy, per slot -- the CPU
+    check of the classification fixtures (the product op runs on the GPU)."""
+    src = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(g.offsets))
+    dst = g.edges.astype(np.int64)
+    tree_down = parent[dst] == src
+    tree_up = parent[src] == dst
+    child = np.where(tree_down, dst, src)
+    pc = np.where(tree_down, src, dst)
+    fence = (low[child] >= first[pc]) & (high[child] <= last[pc])
+    anc = ((first[src] <= first[dst]) & (last[dst] <= last[src])) | ((first[dst] <= first[src]) & (last[src] <= last[dst]))
+    out = np.where(anc, 2, 3).astype(np.int8)
+    tree = tree_down | tree_up
+    out[tree] = np.where(fence[tree], 1, 0)
+    return src, dst, out
+
+
+def test_classify_fixtures_consistent(corpus):
+    """tests/golden/classify.npz holds the reference's classify_edge on its
+    own forest (cross-checked there against classify_edges_oracle): the
+    definition restated here agrees on every edge of the corpus."""
+    z = np.load(GOLDEN / "classify.npz")
+    eo = np.concatenate([[0], np.cumsum(z["E"])])
+    for i, name, g in corpus.items():
+        if g.m == 0:
+            continue
+        arrs = [corpus.get(i, k).astype(np.int64) for k in ("parent", "first", "last", "low", "high")]
+        src, dst, cls = _classes_from_definition(g, *arrs)
+        assert np.array_equal(cls[src < dst], z["cls"][eo[i]:eo[i + 1]]), name
