@@ -22,13 +22,15 @@ struct Scalars {
   int num_edges;   // E
   int nroots[16];  // roots after each sampling round's compress (stage 1: 0..7, stage 5: 8..15)
   int hooks[16];   // hooks accepted per sampling round (same split)
-  int nheavy[2];   // super-heavy rows deferred by k_link_rows (stage 1 / stage 5 slot)
+  int nheavy[2];   // super-heavy rows deferred by k_link_rows, CTA tier (stage 1 / stage 5 slot)
   int has_hubs;    // some row has >= kHubDeg slots (set by k_chunk_rows)
   unsigned ticket; // last-block detection (k_compress; reset by the last block)
   int giant_cnt;   // samples (of 1024) that fell in the giant at its pick
   unsigned tile_ticket;  // k_tile: last block builds the tile-extreme table (reset by it)
-  int eheavy;      // Stage 6: super-heavy non-giant rows deferred by k_edge_fix
-  int pad[20];
+  int eheavy;      // Stage 6: super-heavy non-giant rows deferred by k_edge_fix (CTA tier)
+  int nmega[2];    // ... grid tier of nheavy
+  int emega;       // ... grid tier of eheavy
+  int pad[17];
 };
 
 // ---------------------------------------------------------------------------
@@ -299,6 +301,43 @@ constexpr int kRowChunks = FBCC_ROW_CHUNKS;
 // (see k_root_flags)
 constexpr int kHubDeg = 1024;
 constexpr int kHubWays = 32;
+
+// Long rows deferred by a row-parallel pass (one lane or warp per row) to a
+// second kernel, in two tiers so that neither tier costs every thread a pass
+// over every listed row: rows up to kMegaRow arcs are owned by one CTA each
+// (CTA b takes rows b, b + gridDim.x, ...), longer ones are strided over the
+// whole grid.  Tier 1 fills list[0..) and tier 2 list[cap-1] downwards.
+constexpr int kMegaRow = 1 << 16;
+struct LongRows {
+  int* list;
+  int cap;
+  int* nblock;  // tier-1 count
+  int* ngrid;   // tier-2 count
+  __device__ __forceinline__ void defer(int v, int64_t len) const {
+    if (len > kMegaRow) list[cap - 1 - atomicAdd(ngrid, 1)] = v;
+    else list[atomicAdd(nblock, 1)] = v;
+  }
+  // f(v) per row for the row words, then g(v, a) per arc, by the calling CTA
+  // (tier 1) or the whole grid (tier 2)
+  template <class Row, class Arc>
+  __device__ __forceinline__ void visit(const int64_t* __restrict__ off, Row&& row, Arc&& arc) const {
+    const int HB = *nblock, HG = *ngrid;
+    for (int h = blockIdx.x; h < HB; h += gridDim.x) {
+      const int v = list[h];
+      const int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+      row(v, rs);
+      for (int64_t a = rs + threadIdx.x; a < re; a += blockDim.x) arc(v, a);
+    }
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int h = 0; h < HG; h++) {
+      const int v = list[cap - 1 - h];
+      const int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
+      if (rs + tid >= re) continue;
+      row(v, rs);
+      for (int64_t a = rs + tid; a < re; a += stride) arc(v, a);
+    }
+  }
+};
 
 // Block-reduced counter add: every thread of the block must call it (after
 // its grid-stride loop) with its private count; one atomic per block.

@@ -588,7 +588,7 @@ __global__ void k_find_giant(const int* __restrict__ comp, int n, Scalars* sc, b
 // graph, so the 4m bytes of targets are mostly never read).  Rows of <= 32
 // arcs are linked by their own lane; longer rows are linked by the whole warp
 // striding over the arcs (a non-giant hub cannot serialise one thread).
-constexpr int kSuperRow = 8192;
+constexpr int kSuperRow = 2048;
 
 // 4-arc batches at 32 registers (full occupancy) measured best across
 // configs 2/3/4b/4c/5 (8-arc batches at 64 registers: 4b/4c +4 %)
@@ -603,7 +603,7 @@ constexpr int kLinkBatch = FBCC_LR_BATCH;
 template <int kPred, bool kRecord>
 __global__ void __launch_bounds__(256, FBCC_LR_MINB) k_link_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                    int n, int* comp, int2* fe, PredData pd, const Scalars* sc,
-                                                   int* heavy_list, int* nheavy) {
+                                                   LongRows heavy) {
   pdl_enter();
   const int giant = sc->giant;
   const int lane = threadIdx.x & 31;
@@ -619,9 +619,10 @@ __global__ void __launch_bounds__(256, FBCC_LR_MINB) k_link_rows(const int64_t* 
       re = __ldg(off + v + 1);
     }
     // rows longer than kSuperRow (RMAT hubs outside the skeleton giant reach
-    // 638k arcs) go to a list that k_link_heavy spreads over the whole grid
+    // 638k arcs) go to k_link_heavy: a CTA per row, or the whole grid for the
+    // longest (LongRows)
     if (re - rs > kSuperRow) {
-      heavy_list[atomicAdd(nheavy, 1)] = v;
+      heavy.defer(v, re - rs);
       rs = re = 0;
     }
     const bool heavy = re - rs > 32;
@@ -676,28 +677,21 @@ __global__ void __launch_bounds__(256, FBCC_LR_MINB) k_link_rows(const int64_t* 
   }
 }
 
-// The deferred super-heavy rows: every block strides over every listed row,
-// so one hub's arcs are spread over the whole grid.
+// The deferred super-heavy rows (LongRows: a CTA per row up to kMegaRow
+// arcs, the whole grid per longer row).
 template <int kPred, bool kRecord>
 __global__ void __launch_bounds__(256) k_link_heavy(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                                    int* comp, int2* fe, PredData pd, const int* __restrict__ heavy_list,
-                                                    const int* __restrict__ nheavy) {
+                                                    int* comp, int2* fe, PredData pd, LongRows heavy) {
   pdl_enter();
-  const int H = *nheavy;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int h = 0; h < H; h++) {
-    const int v = heavy_list[h];
-    const int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
-    if (rs + tid >= re) continue;
-    int4 rv;
-    if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
-    for (int64_t a = rs + tid; a < re; a += stride) {
-      int w = (int)__ldg(adj + a);
-      if (!keep<kPred>(pd, v, rv, w, a)) continue;
-      link<kRecord>(v, w, comp, fe);
-    }
-  }
+  int4 rv;
+  heavy.visit(
+      off, [&](int v, int64_t) {
+        if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
+      },
+      [&](int v, int64_t a) {
+        const int w = (int)__ldg(adj + a);
+        if (keep<kPred>(pd, v, rv, w, a)) link<kRecord>(v, w, comp, fe);
+      });
 }
 
 // The schedule shared by Stage 1 (no predicate, forest recorded), Stage 5
@@ -772,18 +766,16 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     note(K_FIND_GIANT);
   }
   if (g.m > 0) {
-    // the proposal words are dead after the last accept: reuse them as the
-    // super-heavy row list
-    int* heavy = reinterpret_cast<int*>(prop);
-    int* nheavy = sc->nheavy + (slot ? 1 : 0);
-    launch(k_link_rows<kPred, kRecord>, grid_for(g.n, B, 32), B, 0, st, g.off, g.adj, g.n, comp, fe, pd, sc, heavy,
-                                                                    nheavy);
+    // the proposal words (2n ints) are dead after the last accept: reuse them
+    // as the super-heavy row lists
+    LongRows heavy{reinterpret_cast<int*>(prop), 2 * g.n, sc->nheavy + (slot ? 1 : 0), sc->nmega + (slot ? 1 : 0)};
+    launch(k_link_rows<kPred, kRecord>, grid_for(g.n, B, 32), B, 0, st, g.off, g.adj, g.n, comp, fe, pd, sc, heavy);
     note(K_LINK_ROWS);
     // always launched: whether a super-heavy row exists is a property of the
     // buffer contents, which a replayed plan must not bake in (an empty list
     // costs one ~2 us launch that exits at once)
     launch(k_link_heavy<kPred, kRecord>, grid_for((int64_t)kNumSMs * 2048, B), B, 0, st, g.off, g.adj, comp, fe,
-           pd, heavy, nheavy);
+           pd, heavy);
     note(K_LINK_HEAVY);
   }
   launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0, 0,

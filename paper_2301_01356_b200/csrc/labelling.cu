@@ -101,7 +101,7 @@ __global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict
 // processed, blocks are written unmarked and k_edge_final maps all E.
 // ---------------------------------------------------------------------------
 constexpr int kEdgeMark = (int)0x80000000;
-constexpr int kEdgeSuperRow = 8192;
+constexpr int kEdgeSuperRow = 2048;
 
 __device__ __forceinline__ int big_giant(const int* label, const Scalars* sc) {
   return sc->giant_cnt >= 256 ? giant_label(label, sc) : -1;
@@ -255,7 +255,7 @@ struct EdgeFix {
 __global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                   int n, const int* __restrict__ label, const int* __restrict__ head,
                                                   const int* __restrict__ uoff, const int* __restrict__ nlow,
-                                                  int* edge_label, int* bmin, int* __restrict__ heavy,
+                                                  int* edge_label, int* bmin, LongRows heavy,
                                                   int* __restrict__ sreq, Scalars* sc) {
   pdl_enter();
   EdgeFix f;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ of
       }
     }
     if (re - rs > kEdgeSuperRow) {
-      heavy[atomicAdd(&sc->eheavy, 1)] = v;
+      heavy.defer(v, re - rs);
       rs = re = 0;
     }
     bool req = false;
@@ -305,40 +305,41 @@ __global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ of
   f.flush();
 }
 
-// The deferred work: (a) rows over kEdgeSuperRow arcs, every thread of the
-// grid striding over each (their one lower-arc fix inline); (b) the lower-arc
-// fixes k_edge_fix flagged, one per thread.  Disjoint rows: no ordering
-// between the two.
+// The deferred work: (a) rows over kEdgeSuperRow arcs (LongRows: a CTA per
+// row, the whole grid per row over kMegaRow; their one lower-arc fix
+// inline), (b) the lower-arc fixes k_edge_fix flagged, one per thread.
+// Disjoint rows: no ordering between the two.
 __global__ void __launch_bounds__(256) k_edge_search(const int64_t* __restrict__ off,
                                                      const uint32_t* __restrict__ adj, int n,
                                                      const int* __restrict__ label, const int* __restrict__ head,
                                                      const int* __restrict__ uoff, const int* __restrict__ nlow,
-                                                     int* edge_label, int* bmin, const int* __restrict__ heavy,
+                                                     int* edge_label, int* bmin, LongRows heavy,
                                                      int* sreq, int* spos, Scalars* sc) {
   pdl_enter();
   EdgeFix f;
   f.init(off, adj, label, head, uoff, nlow, edge_label, bmin, sc);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
-  const int H = sc->eheavy;
-  for (int h = 0; h < H; h++) {
-    const int v = __ldg(heavy + h);
-    const int64_t rs = __ldg(off + v), re = __ldg(off + v + 1);
-    const int lu = __ldg(label + v);
-    int hl, ebase;
-    bool row_u0;
-    f.row_words(v, lu, rs, hl, row_u0, ebase);
-    for (int64_t a = rs + tid; a < re; a += stride)
-      if (f.arc(v, lu, hl, row_u0, ebase, a, (int)__ldg(adj + a))) {
-        spos[v] = f.fix_lower(v, lu, hl);  // (k_edge_final maps it; a repeat below is idempotent)
-        sreq[v] = 1;
-      }
-    f.flush();
-  }
+  int lu = 0, hl = 0, ebase = 0;
+  bool row_u0 = false;
+  heavy.visit(
+      off,
+      [&](int v, int64_t rs) {
+        f.flush();  // (a new row: the previous row's run ends)
+        lu = __ldg(label + v);
+        f.row_words(v, lu, rs, hl, row_u0, ebase);
+      },
+      [&](int v, int64_t a) {
+        if (f.arc(v, lu, hl, row_u0, ebase, a, (int)__ldg(adj + a))) {
+          spos[v] = f.fix_lower(v, lu, hl);  // (k_edge_final maps it; a repeat below is idempotent)
+          sreq[v] = 1;
+        }
+      });
+  f.flush();
   if (f.G < 0) return;  // (no lower-arc fixes without a giant)
   for (int64_t v = tid; v < n; v += stride)
     if (sreq[v]) {
-      const int lu = __ldg(label + v);
-      spos[v] = f.fix_lower((int)v, lu, __ldg(head + lu));
+      const int lv = __ldg(label + v);
+      spos[v] = f.fix_lower((int)v, lv, __ldg(head + lv));
     }
 }
 
@@ -353,7 +354,7 @@ __device__ __forceinline__ void edge_map(int* edge_label, const int* bmin, int e
 __global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ off, int n,
                                                     const int* __restrict__ label, const int* __restrict__ uoff,
                                                     const int* __restrict__ nlow, int* edge_label,
-                                                    const int* __restrict__ bmin, const int* __restrict__ heavy,
+                                                    const int* __restrict__ bmin, LongRows heavy,
                                                     const int* __restrict__ sreq, const int* __restrict__ spos,
                                                     const Scalars* sc) {
   pdl_enter();
@@ -386,12 +387,13 @@ __global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ 
         for (int e = h0 + lane; e < h1; e += 32) edge_map(edge_label, bmin, e);
       }
     }
-    const int H = sc->eheavy;
-    for (int h = 0; h < H; h++) {
-      const int v = __ldg(heavy + h);
-      const int e0 = __ldg(uoff + v), e1 = __ldg(uoff + v + 1);
-      for (int64_t e = e0 + tid; e < e1; e += stride) edge_map(edge_label, bmin, (int)e);
-    }
+    int eb = 0;  // (the deferred rows' upper arcs: edge ids eb + a)
+    heavy.visit(
+        off, [&](int v, int64_t rs) { eb = __ldg(uoff + v) - (int)(rs + __ldg(nlow + v)); },
+        [&](int v, int64_t a) {
+          const int e = eb + (int)a;
+          if (e >= __ldg(uoff + v)) edge_map(edge_label, bmin, e);
+        });
     return;
   }
   if ((reinterpret_cast<uintptr_t>(edge_label) & 15) == 0) {
@@ -453,14 +455,15 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
     note(K_GIANT_MIN);
     launch(k_edge_fill, grid_for(g.m / 8 + 1, B), B, 0, st, n, label, uoff, bmin, edge_label, sc);
     note(K_EDGE_FILL);
-    launch(k_edge_fix, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin,
-           heavy, sreq, sc);
+    LongRows hv{heavy, n, &sc->eheavy, &sc->emega};  // (a dead n-int Stage-2 array, see api.cu)
+    launch(k_edge_fix, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin, hv,
+           sreq, sc);
     note(K_EDGE_BLOCKS);
     launch(k_edge_search, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin,
-           (const int*)heavy, sreq, spos, sc);
+           hv, sreq, spos, sc);
     note(K_EDGE_SEARCH);
-    launch(k_edge_final, grid_for(n, B, 32), B, 0, st, g.off, n, label, uoff, nlow, edge_label, bmin,
-           (const int*)heavy, (const int*)sreq, (const int*)spos, (const Scalars*)sc);
+    launch(k_edge_final, grid_for(n, B, 32), B, 0, st, g.off, n, label, uoff, nlow, edge_label, bmin, hv,
+           (const int*)sreq, (const int*)spos, (const Scalars*)sc);
     note(K_EDGE_FINAL);
   }
   if (side) cudaStreamWaitEvent(st, side->ev[3], 0);  // join the articulation flags
