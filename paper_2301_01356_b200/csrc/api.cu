@@ -96,8 +96,8 @@ struct Layout {
     lhead = take(4 * n);
     hsub = take(4 * (m / 16 + 64));
     nexto = take(4 * N0);
-    nxt = take(4 * N0);
     own0 = take(8 * N0);
+    nxt = N0 * 8 > (64ll << 20) ? 0 : take(4 * N0);  // (large tours: level 0 runs in place in own0)
     rank0 = take(4 * N0);
     for (int l = 1; l <= nlev; l++) {
       lsucc[l] = take(4 * K[l]);
@@ -157,7 +157,7 @@ struct Pipeline {
     R.hsub = (int*)at(lay.hsub);
     R.hoff = offsets;
     R.nexto = (int*)at(lay.nexto);
-    R.nxt = (int*)at(lay.nxt);
+    R.nxt = lay.nxt ? (int*)at(lay.nxt) : nullptr;  // (nullptr: level 0 in place in own0)
     R.own0 = (int2*)at(lay.own0);
     R.rank0 = (int*)at(lay.rank0);
     R.nlev = lay.nlev;

@@ -64,8 +64,8 @@ struct Rooting {
   int* hsub;       // [m/16 + 64] hub sub-list heads (nullptr: no hub split)
   const int64_t* hoff;  // CSR offsets the hubs are chosen from (nullptr: no hub split)
   int* nexto;      // [2n]  next out-arc of the same vertex
-  int* nxt;        // [2n]  unified tour list successor
-  int2* own0;      // [2n]  (segment, offset) per list element
+  int* nxt;        // (unused: level 0's successors live in own0[e].x until the walk replaces them)
+  int2* own0;      // [2n]  per list element: (successor, 0) from k_link_tour, then (segment, offset)
   int* rank0;      // [2n]  tour position of each list element
   // ruling-set levels 1..nlev: element counts and arrays
   int nlev;

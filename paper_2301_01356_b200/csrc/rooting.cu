@@ -189,7 +189,7 @@ __device__ __forceinline__ int flag_succ(int s, int sh, int N) {
 __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict__ fe,
                             const int* __restrict__ lhead, const int* __restrict__ hsub, const int* __restrict__ nexto,
                             const int* __restrict__ rootidx, const int* __restrict__ rlist, int n,
-                            int* __restrict__ nxt, const Scalars* sc, int sh0) {
+                            int* __restrict__ nxt, int2* __restrict__ own0, const Scalars* sc, int sh0) {
   pdl_enter();
   const int c = sc->ncomp;
   const int64_t N = 2 * (int64_t)n;
@@ -219,11 +219,19 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
         else out = h <= -2 ? hub_next(hsub, -2 - h, 0) : h;
       }
     }
-    nxt[e] = flag_succ(out, sh0, (int)N);
+    // in place (nxt == nullptr): the successor goes into the element's
+    // (segment, offset) slot, which the level-0 walker reads and then
+    // overwrites (one sector per visited element instead of a successor
+    // sector plus a partial write -- the win when the walk is DRAM-bound)
+    if (nxt) nxt[e] = flag_succ(out, sh0, (int)N);
+    else own0[e] = make_int2(flag_succ(out, sh0, (int)N), 0);
   }
 }
 
-template <bool kWeighted>
+// kInPlace (level 0 of large tours): the successors sit in own[e].x (written
+// by k_link_tour) and are replaced by (segment, offset) as the walk passes --
+// every element is read and then written by its own walker only.
+template <bool kWeighted, bool kInPlace = false>
 __global__ void __launch_bounds__(256) k_walk(int K, int sh, int N, const int* __restrict__ succ,
                                               const int* __restrict__ w, int2* __restrict__ own,
                                               int* __restrict__ succ_next, int* __restrict__ w_next, int sh_next) {
@@ -233,9 +241,14 @@ __global__ void __launch_bounds__(256) k_walk(int K, int sh, int N, const int* _
     int acc = 0;
     int s;
     while (true) {
-      own[e] = make_int2(j, acc);
+      // (read-only path: an element is read strictly before its one write)
+      s = kInPlace ? __ldg(reinterpret_cast<const int*>(own) + 2 * (int64_t)e) : __ldg(succ + e);
+      // in place: the store must not reach L2 while the same sector's fill is
+      // still pending (store-behind-miss on one sector ran ~9x slower), so
+      // the stored value is made to depend on the loaded one (s == INT_MIN
+      // never occurs: successors are >= -1 or flagged ~e with e >= 1)
+      own[e] = make_int2(kInPlace ? (s == (int)0x80000000 ? -1 : j) : j, acc);
       acc += kWeighted ? __ldg(w + e) : 1;
-      s = __ldg(succ + e);
       if (s < 0) break;
       e = s;
     }
@@ -424,11 +437,17 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
   // levels 1..nlev-1 are walked again (their successors carry splitter flags
   // for the next windowing); level nlev goes to the one-CTA final kernel
   auto sh_after = [&](int l) { return l < R.nlev ? shift(R.S[l]) : -1; };
-  launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.hsub, R.nexto, R.rootidx, R.rlist, n, R.nxt, sc,
+  // level 0 in place once the tour outgrows L2 (own0 > 64 MB): DRAM-bound
+  // walks gain (config 5 walk0 1.65 -> 0.92 ms), L2-resident ones lose
+  // (config 2: the next element often shares the stored sector)
+  const bool inplace = (int64_t)N0 * 8 > (64ll << 20) || !R.nxt;
+  launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.hsub, R.nexto, R.rootidx, R.rlist, n,
+         inplace ? (int*)nullptr : R.nxt, R.own0, sc,
                                              shift(R.S[0]));
   note(K_LINK_TOUR);
   // ruling-set levels
-  launch(k_walk<false>, grid_for(R.K[1], B, 64), B, 0, st, (int)R.K[1], shift(R.S[0]), N0, R.nxt, nullptr, R.own0,
+  launch(inplace ? k_walk<false, true> : k_walk<false, false>, grid_for(R.K[1], B, 64), B, 0, st, (int)R.K[1],
+         shift(R.S[0]), N0, (const int*)R.nxt, (const int*)nullptr, R.own0,
                                                        R.succ[1], R.wgt[1], sh_after(1));
   note(K_WALK0);
   for (int l = 1; l < R.nlev; l++) {
