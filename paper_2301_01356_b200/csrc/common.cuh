@@ -297,10 +297,29 @@ __device__ __forceinline__ void visit_arc_chunks(const int64_t* __restrict__ off
 #endif
 constexpr int kRowChunks = FBCC_ROW_CHUNKS;
 
-// rows of at least kHubDeg slots get kHubWays out-list heads in rooting
-// (see k_root_flags)
+// rows of at least kHubDeg slots get several out-list heads in rooting (see
+// k_root_flags): W = 2^lw ways, W = max(32, deg/64) rounded down to a power
+// of two, at most 2^14 -- about 64 tree children per way on the RMAT hubs
+// (deg 638k: 8192 ways), whose list inserts otherwise queue on 32 addresses.
+// The marker lhead[v] = -2 - (base | (lw - 5) << 27) carries the sub-list
+// base (off[v] >> 4; ways [base, base + W) stay inside the row's share
+// deg/16 of the hsub array) and the way count.
 constexpr int kHubDeg = 1024;
-constexpr int kHubWays = 32;
+constexpr int kHubWays = 32;  // minimum ways of a hub
+constexpr int kHubBaseBits = 27;
+#ifndef FBCC_HUB_WAY_SHIFT
+#define FBCC_HUB_WAY_SHIFT 7  // W ~ deg / 128 (deg/32, deg/64, deg/128 on config 5: 16.21, 16.00, 15.89 ms)
+#endif
+
+__device__ __forceinline__ int hub_log_ways(int64_t deg) {
+  int64_t w = deg >> FBCC_HUB_WAY_SHIFT;
+  int lw = 5;
+  while (lw < 14 && ((int64_t)2 << lw) <= w) lw++;
+  return lw;
+}
+__device__ __forceinline__ int hub_marker(int base, int lw) { return -2 - (base | ((lw - 5) << kHubBaseBits)); }
+__device__ __forceinline__ int hub_base(int h) { return (-2 - h) & ((1 << kHubBaseBits) - 1); }
+__device__ __forceinline__ int hub_ways(int h) { return 1 << (((-2 - h) >> kHubBaseBits) + 5); }
 
 // Long rows deferred by a row-parallel pass (one lane or warp per row) to a
 // second kernel, in two tiers so that neither tier costs every thread a pass

@@ -43,8 +43,9 @@ __device__ __forceinline__ void root_init(const RootInit& ri, const int64_t* hof
     const int64_t rs = __ldg(hoff + v);
     if (__ldg(hoff + v + 1) - rs >= kHubDeg) {
       const int base = (int)(rs >> 4);
-      for (int j = 0; j < kHubWays; j++) ri.hsub[base + j] = -1;
-      h = -2 - base;
+      const int lw = hub_log_ways(__ldg(hoff + v + 1) - rs);
+      for (int j = 0; j < (1 << lw); j++) ri.hsub[base + j] = -1;
+      h = hub_marker(base, lw);
     }
   }
   ri.lhead[v] = h;
