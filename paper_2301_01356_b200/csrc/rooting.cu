@@ -90,9 +90,11 @@ void scan_upper_degrees(const int64_t* off, const int* nlow, int n, int* uoff, v
 // Hub split: every forest edge inserts its two arcs at the heads of its
 // endpoints' lists with atomicExch, so a vertex of tree degree d serialises d
 // returning atomics on one address (RMAT hubs: ~1e5, 2 ms).  Vertices of
-// CSR degree >= kHubDeg instead get 32 sub-lists (the inserting edge x picks
-// x & 31), whose heads live at hsub[(off[v] >> 4) + j] -- disjoint for rows
-// of >= 527 slots -- and lhead[v] = -2 - (off[v] >> 4) marks the vertex.
+// CSR degree >= kHubDeg instead get W sub-lists (the inserting edge x picks
+// x & (W - 1); W = 32 .. 16384 by degree, see hub_log_ways: on RMAT the
+// biggest hubs' inserts queued on 32 addresses -- out_lists 1.15 -> 0.58 ms),
+// whose heads live at hsub[(off[v] >> 4) + j] -- disjoint, W <= deg/16 --
+// and lhead[v] = hub_marker(base, log2 W) marks the vertex.
 // The tour walks a hub's sub-lists in order (k_link_tour).
 
 __global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restrict__ flags, int* __restrict__ lhead,
@@ -107,8 +109,9 @@ __global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restric
         const int64_t rs = __ldg(off + v);
         if (__ldg(off + v + 1) - rs >= kHubDeg) {
           const int base = (int)(rs >> 4);
-          for (int j = 0; j < kHubWays; j++) hsub[base + j] = -1;
-          h = -2 - base;
+          const int lw = hub_log_ways(__ldg(off + v + 1) - rs);
+          for (int j = 0; j < (1 << lw); j++) hsub[base + j] = -1;
+          h = hub_marker(base, lw);
         }
       }
       lhead[v] = h;
@@ -130,7 +133,7 @@ __global__ void k_root_list(const int* __restrict__ comp, const int* __restrict_
 __device__ __forceinline__ int* list_head(int* lhead, int* hsub, int t, int x, bool split) {
   if (split) {
     const int h = ld_relaxed(lhead + t);  // concurrent exchanges leave non-hubs >= -1
-    if (h <= -2) return hsub + (-2 - h) + (x & (kHubWays - 1));
+    if (h <= -2) return hsub + hub_base(h) + (x & (hub_ways(h) - 1));
   }
   return lhead + t;
 }
@@ -155,10 +158,11 @@ __global__ void k_out_lists(const int* __restrict__ comp, const int2* __restrict
 }
 
 // first non-empty hub sub-list head at or after way j (-1: none)
-__device__ __forceinline__ int hub_next(const int* __restrict__ hsub, int base, int j) {
-  for (; j < kHubWays; j++) {
-    const int h = __ldg(hsub + base + j);
-    if (h >= 0) return h;
+__device__ __forceinline__ int hub_next(const int* __restrict__ hsub, int h, int j) {
+  const int base = hub_base(h), W = hub_ways(h);
+  for (; j < W; j++) {
+    const int head = __ldg(hsub + base + j);
+    if (head >= 0) return head;
   }
   return -1;
 }
@@ -199,7 +203,7 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
     if (__ldg(comp + x) == x) {  // enter(x) / exit(x)
       if ((e & 1) == 0) {
         int h = __ldg(lhead + x);
-        if (h <= -2) h = hub_next(hsub, -2 - h, 0);
+        if (h <= -2) h = hub_next(hsub, h, 0);
         out = h >= 0 ? h : (int)e + 1;
       } else {
         int ri = __ldg(rootidx + x);
@@ -213,10 +217,10 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
         out = nx;
       } else {  // end of t's list (of a hub's sub-list: the next non-empty one)
         const int h = __ldg(lhead + t);
-        if (h <= -2) nx = hub_next(hsub, -2 - h, (x & (kHubWays - 1)) + 1);
+        if (h <= -2) nx = hub_next(hsub, h, (x & (hub_ways(h) - 1)) + 1);
         if (nx >= 0) out = nx;
         else if (__ldg(comp + t) == t) out = 2 * t + 1;
-        else out = h <= -2 ? hub_next(hsub, -2 - h, 0) : h;
+        else out = h <= -2 ? hub_next(hsub, h, 0) : h;
       }
     }
     // in place (nxt == nullptr): the successor goes into the element's
