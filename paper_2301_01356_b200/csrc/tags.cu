@@ -28,6 +28,10 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#ifndef FBCC_WSTORE_CS
+#define FBCC_WSTORE_CS 1
+#endif
+
 namespace fbcc {
 
 __device__ __forceinline__ int2 comb(int2 a, int2 b) { return make_int2(min(a.x, b.x), max(a.y, b.y)); }
@@ -60,8 +64,14 @@ __device__ __forceinline__ void w_arc(int v, int pv, int w, const int4* __restri
   m2 = max(m2, f);
 }
 
+// (streaming store, evict-first: the tour-indexed records are scattered over
+// 32n bytes and must not evict the first[] lines the gathers live on)
 __device__ __forceinline__ void w_store(int4* AP, int fv, int m1, int m2) {
+#if FBCC_WSTORE_CS
+  __stcs(reinterpret_cast<int2*>(AP + fv), make_int2(min(fv, m1), max(fv, m2)));
+#else
   *reinterpret_cast<int2*>(AP + fv) = make_int2(min(fv, m1), max(fv, m2));
+#endif
 }
 
 __device__ __forceinline__ void w_atomic(int4* AP, int fv, int m1, int m2) {
