@@ -52,8 +52,8 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: Path | None
         return LIB
     nvcc = _nvcc()
     bdir.mkdir(parents=True, exist_ok=True)
-    objs = []
-    for src in sources():
+
+    def compile_one(src):
         obj = bdir / (src.stem + ".o")
         cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -62,7 +62,12 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: Path | None
         (bdir / (src.stem + ".ptxas.txt")).write_text(r.stderr)
         if verbose:
             sys.stderr.write(r.stderr)
-        objs.append(str(obj))
+        return str(obj)
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:  # one nvcc per translation unit
+        objs = list(ex.map(compile_one, sources()))
     lib.parent.mkdir(parents=True, exist_ok=True)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]

@@ -241,7 +241,9 @@ def _hostgen_lib():
     so = tools / "libhostgen.so"
     src = tools / "hostgen.c"
     if not so.exists() or so.stat().st_mtime < src.stat().st_mtime:
-        tmp = so.with_suffix(".so.tmp")
+        import os
+
+        tmp = so.with_suffix(f".so.{os.getpid()}.tmp")  # concurrent ranks may build at once
         subprocess.run(["gcc", "-O3", "-march=x86-64-v2", "-fopenmp", "-shared", "-fPIC", "-o", str(tmp), str(src)],
                        check=True)
         tmp.replace(so)
