@@ -36,7 +36,7 @@ static std::atomic<int> g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*gi
                       /*giant pick folded into the last compress*/ 1,
                       /*warp-staged edge-block pass with the giant bitmap*/ 1,
                       /*... plus adaptive rounds up to (skip_round)*/ 3, /*Stage 5 cap (0: same)*/ 0,
-                      /*accept folded into the following compress (config 2 +3.8 %, 4b -3.6 %: off)*/ 0, 0};
+                      /*accept folded into the following compress: 2 = auto (n >= 2^22; config 5 -1.3 %, 4b -4.3 %, config 2 +6 % if forced)*/ 2, 0};
 thread_local const Options* t_opt = nullptr;
 
 int option_default(int key) { return g_opt[key].load(std::memory_order_relaxed); }

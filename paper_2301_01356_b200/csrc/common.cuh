@@ -87,7 +87,7 @@ enum Option : int {
   OPT_EB_STAGED = 15,     // (retired: the warp-staged bitmap edge pass)
   OPT_MAX_ROUNDS = 16,    // adaptive sampling rounds beyond OPT_SAMPLE_ROUNDS, up to this many (see skip_round)
   OPT_SKEL_MAX_ROUNDS = 17,  // Stage 5's cap instead (0: OPT_MAX_ROUNDS)
-  OPT_ACCEPT_FOLD = 18,   // a sampling round's accept runs inside the compress that follows it
+  OPT_ACCEPT_FOLD = 18,   // a sampling round's accept runs inside the compress that follows it (2: auto by size)
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 20
 };

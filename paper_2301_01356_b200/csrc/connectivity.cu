@@ -733,8 +733,12 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   }
   for (int r = 0; r < kRounds; r++) {
     const bool flat = r == 0 || ((cmask >> (r - 1)) & 1);
-    // a round followed by a compress folds its accept into it (OPT_ACCEPT_FOLD)
-    const bool fold = r > 0 && ((cmask >> r) & 1) && opt(OPT_ACCEPT_FOLD);
+    // a round followed by a compress folds its accept into it (OPT_ACCEPT_FOLD:
+    // 1 always, 2 = auto: graphs of >= 2^22 vertices -- configs 4a/4b/4c/5
+    // -1 to -4 %, while config 2 gains +6 % from the two-level trees a folded
+    // accept can leave)
+    const int af = opt(OPT_ACCEPT_FOLD);
+    const bool fold = r > 0 && ((cmask >> r) & 1) && (af == 1 || (af == 2 && g.n >= (1 << 22)));
     if (r > 0) {
       launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat,
              ((opt(OPT_SKEL_PARENT) >> r) & 1) != 0, kBase);
