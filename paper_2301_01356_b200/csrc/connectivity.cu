@@ -351,13 +351,16 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
         if (s >= __ldg(off + v + 1)) continue;
         w = (int)__ldg(adj + s);
       }
-      if (!keep<kPred>(pd, v, rv, w, s)) continue;
     }
     // flat after a compress; otherwise (rounds >= 1 hook root -> root only,
     // so trees stay shallow) find with halving
     int ru = flat ? ldp(comp + v) : find_halve(comp, v);
     int rw = flat ? ldp(comp + w) : find_halve(comp, w);
     if (ru == rw) continue;
+    // the predicate only for arcs that would join two sets: under the
+    // skeleton predicate it gathers w's 16-byte record, and by the last
+    // rounds most sampled arcs already lie inside one set
+    if (!(kPred == PRED_SKEL && skel_parent) && !keep<kPred>(pd, v, rv, w, s)) continue;
     int hi = ru > rw ? ru : rw;
     int lo = ru + rw - hi;
     // any proposal is a valid hook, so lanes aiming at the same root send one
