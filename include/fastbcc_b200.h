@@ -176,6 +176,8 @@ int fbcc_plan_destroy(fbcc_plan plan);
     17  Stage 5's cap for key 16 instead (0 = key 16; 4: config 3 -3 %, config 2 +1 %)
     18  fold each round's accept into the following compress (0/1/2 = auto: on for
         n >= 2^22; 2: configs 4a/4b/4c/5 -1 to -4 %, config 2 would be +6 %)
+    19  isolated vertices (but vertex 0) stay off the Euler-tour list and out of
+        the tile pass; their tour positions follow the list's (0/1; 1)
    Keys 2, 5, 6, 7, 9, 10 are retired experiments: accepted and ignored. */
 int fbcc_set_option(int key, int value);
 int fbcc_get_option(int key);

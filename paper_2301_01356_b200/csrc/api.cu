@@ -36,7 +36,8 @@ static std::atomic<int> g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*gi
                       /*giant pick folded into the last compress*/ 1,
                       /*warp-staged edge-block pass with the giant bitmap*/ 1,
                       /*... plus adaptive rounds up to (skip_round)*/ 3, /*Stage 5 cap (0: same)*/ 0,
-                      /*accept folded into the following compress: 2 = auto (n >= 2^22; config 5 -1.3 %, 4b -4.3 %, config 2 +6 % if forced)*/ 2, 0};
+                      /*accept folded into the following compress: 2 = auto (n >= 2^22; config 5 -1.3 %, 4b -4.3 %, config 2 +6 % if forced)*/ 2,
+                      /*isolated vertices off the Euler-tour list and the tile pass*/ 1};
 thread_local const Options* t_opt = nullptr;
 
 int option_default(int key) { return g_opt[key].load(std::memory_order_relaxed); }
@@ -83,6 +84,7 @@ struct Layout {
     tlev = 1;
     while ((1 << tlev) <= ntile) tlev++;
     cub_bytes = scan_temp_bytes(n + 1);
+    if (scan_roots_temp_bytes(n + 1) > cub_bytes) cub_bytes = scan_roots_temp_bytes(n + 1);
     if (scan_upper_temp_bytes((int)n) > cub_bytes) cub_bytes = scan_upper_temp_bytes((int)n);
 
     sc = take(sizeof(Scalars));
@@ -91,7 +93,7 @@ struct Layout {
     fe = take(8 * n);
     prop = take(8 * n);
     flags = take(4 * (n + 1));
-    rootidx = take(4 * (n + 1));
+    rootidx = take(8 * (n + 1));
     rlist = take(4 * n);
     lhead = take(4 * n);
     hsub = take(4 * (m / 16 + 64));
@@ -151,7 +153,7 @@ struct Pipeline {
     fe = (int2*)at(lay.fe);
     prop = (unsigned long long*)at(lay.prop);
     R.flags = (int*)at(lay.flags);
-    R.rootidx = (int*)at(lay.rootidx);
+    R.rootidx = (unsigned long long*)at(lay.rootidx);
     R.rlist = (int*)at(lay.rlist);
     R.lhead = (int*)at(lay.lhead);
     R.hsub = (int*)at(lay.hsub);
@@ -186,6 +188,7 @@ struct Pipeline {
     T.table = (int2*)at(lay.table);
     T.ntile = lay.ntile;
     T.tlev = lay.tlev;
+    T.tour_len = &sc->tour_len;  // (k_out_lists publishes it)
     cnt = (int*)at(lay.cnt);
     uoff = (int*)at(lay.uoff);
     nlow = (int*)at(lay.nlow);
@@ -229,6 +232,7 @@ struct Pipeline {
     ri.hsub = R.hsub;
     ri.off = R.hoff;
     ri.sc = sc;
+    ri.detach = opts.v[OPT_DETACH] != 0;
     return ri;
   }
 
@@ -246,7 +250,7 @@ struct Pipeline {
     // Stage 2's root list / root ranks / out-list links are dead by Stage 6:
     // its deferred rows, search flags and searched positions
     stage6_labelling(g, R.rec, out.label, out.head, out.is_ap, out.edge_label, cnt, uoff, nlow, bmin, R.rlist,
-                     R.rootidx, R.nexto,
+                     reinterpret_cast<int*>(R.rootidx), R.nexto,
                      R.cub_tmp, R.cub_bytes, sc, st, heads_done, side);
     mk(6);
   }
@@ -434,7 +438,7 @@ int fbcc_run(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && dbg)
     export_debug(P.g, P.fe, P.R.rec, P.T.AP, dbg->forest, dbg->parent, dbg->first, dbg->last, dbg->w1, dbg->w2,
-                 dbg->fence, st);
+                 dbg->fence, st, P.T.tour_len);
   Scalars host;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&host, P.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -30,7 +30,9 @@ struct Scalars {
   int eheavy;      // Stage 6: super-heavy non-giant rows deferred by k_edge_fix (CTA tier)
   int nmega[2];    // ... grid tier of nheavy
   int emega;       // ... grid tier of eheavy
-  int pad[17];
+  int nlisted;     // roots on the Euler-tour list (code 1)
+  int tour_len;    // list elements = 2 (n - detached roots); detached positions follow
+  int pad[15];
 };
 
 // ---------------------------------------------------------------------------
@@ -88,6 +90,7 @@ enum Option : int {
   OPT_MAX_ROUNDS = 16,    // adaptive sampling rounds beyond OPT_SAMPLE_ROUNDS, up to this many (see skip_round)
   OPT_SKEL_MAX_ROUNDS = 17,  // Stage 5's cap instead (0: OPT_MAX_ROUNDS)
   OPT_ACCEPT_FOLD = 18,   // a sampling round's accept runs inside the compress that follows it (2: auto by size)
+  OPT_DETACH = 19,        // isolated vertices stay off the Euler-tour list and out of the tile pass
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
   OPT_NUM = 20
 };

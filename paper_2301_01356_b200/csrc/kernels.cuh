@@ -34,10 +34,14 @@ struct RootInit {
   int* hsub = nullptr;
   const int64_t* off = nullptr;  // hub split source (nullptr: none)
   const Scalars* sc = nullptr;
+  bool detach = false;           // isolated vertices (but 0) stay off the Euler tour (code 2)
 };
 
+// Root codes (Rooting::flags): 0 non-root, 1 root on the tour list, 2 root
+// kept off the list -- an isolated vertex other than 0, whose positions
+// follow the list's (k_positions).  RMAT s25: 16.5 M of the 33.5 M vertices.
 __device__ __forceinline__ void root_init(const RootInit& ri, const int64_t* hoff, int v, bool root) {
-  ri.flags[v] = root ? 1 : 0;
+  ri.flags[v] = root ? ((ri.detach && v != 0 && __ldg(ri.off + v + 1) == __ldg(ri.off + v)) ? 2 : 1) : 0;
   int h = -1;
   if (hoff) {
     const int64_t rs = __ldg(hoff + v);
@@ -58,9 +62,9 @@ __device__ __forceinline__ void root_init(const RootInit& ri, const int64_t* hof
 constexpr int kFinalMax = FBCC_FINAL_MAX;  // list-ranking level finished in one CTA
 
 struct Rooting {
-  int* flags;      // [n+1] comp[v] == v
-  int* rootidx;    // [n+1] exclusive scan of flags (rank among roots)
-  int* rlist;      // [n]   roots in id order
+  int* flags;      // [n+1] root code (root_init): 0 non-root, 1 listed root, 2 detached
+  unsigned long long* rootidx;  // [n+1] exclusive scan: low 32 bits listed roots before v, high 32 detached ones
+  int* rlist;      // [n]   listed roots in id order
   int* lhead;      // [n]   first out-arc of each vertex (-1: none; <= -2: hub, see rooting.cu)
   int* hsub;       // [m/16 + 64] hub sub-list heads (nullptr: no hub split)
   const int64_t* hoff;  // CSR offsets the hubs are chosen from (nullptr: no hub split)
@@ -91,6 +95,7 @@ struct Tags {
   int2* table;     // [tlev * ntile] sparse table over tile extremes
   int ntile;
   int tlev;
+  const int* tour_len = nullptr;  // device count of list positions (pipeline: Scalars::tour_len); nullptr: 2n
 };
 
 #ifndef FBCC_TILE
@@ -143,7 +148,7 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
                       cudaEvent_t heads_done = nullptr, const Side* side = nullptr);
 void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* AP, int* forest,
                   int* parent, int* first, int* last, int* w1, int* w2, uint8_t* fence,
-                  cudaStream_t st);
+                  cudaStream_t st, const int* tour_len = nullptr);
 
 size_t scan_temp_bytes(int64_t items);
 // uoff[v] = sum over u < v of (deg(u) - nlow[u]), v in [0, n] (uoff[n] = E)
@@ -152,5 +157,9 @@ void scan_upper_degrees(const int64_t* off, const int* nlow, int n, int* uoff, v
                         cudaStream_t st);
 void exclusive_scan(const int* in, int* out, int64_t items, void* tmp, size_t tmp_bytes,
                     cudaStream_t st);
+// rootidx from the root codes (items = n + 1)
+size_t scan_roots_temp_bytes(int64_t items);
+void scan_roots(const int* flags, unsigned long long* out, int64_t items, void* tmp, size_t tmp_bytes,
+                cudaStream_t st);
 
 }  // namespace fbcc

@@ -86,9 +86,9 @@ __global__ void k_ap(int n, const int* __restrict__ label, const int* __restrict
 //     otherwise blk | MARK.  An edge (x, v), x < v, between a G row x and a
 //     non-G row v is G's unless v's component hangs off x (x =
 //     head[label[v]]); the row flags that case (sreq[v]) for
-//  4. k_edge_search: binary search of v in x's upper arcs (spos[v] = e), one
-//     request per thread -- inline, the ~10 dependent loads serialised whole
-//     warps of the row pass.  Also the rows over 8192 arcs that k_edge_fix
+//  4. k_edge_search: binary search of v in x's upper arcs (spos[v] = e), the
+//     requests packed 32 per warp -- inline, the ~10 dependent loads
+//     serialised whole warps of the row pass.  Also the rows over 8192 arcs that k_edge_fix
 //     deferred (a non-giant RMAT hub: 638k arcs), over the whole grid.
 //     Per-block minima: atomicMin from the block's minimum-vertex row only
 //     (one uncontended address per block; one atomic per run of a block).
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ of
 
 // The deferred work: (a) rows over kEdgeSuperRow arcs (LongRows: a CTA per
 // row, the whole grid per row over kMegaRow; their one lower-arc fix
-// inline), (b) the lower-arc fixes k_edge_fix flagged, one per thread.
+// inline), (b) the lower-arc fixes k_edge_fix flagged, 32 per warp.
 // Disjoint rows: no ordering between the two.
 __global__ void __launch_bounds__(256) k_edge_search(const int64_t* __restrict__ off,
                                                      const uint32_t* __restrict__ adj, int n,
@@ -336,11 +336,35 @@ __global__ void __launch_bounds__(256) k_edge_search(const int64_t* __restrict__
       });
   f.flush();
   if (f.G < 0) return;  // (no lower-arc fixes without a giant)
-  for (int64_t v = tid; v < n; v += stride)
-    if (sreq[v]) {
-      const int lv = __ldg(label + v);
-      spos[v] = f.fix_lower((int)v, lv, __ldg(head + lv));
+  // Warp-compacted: the rows with a request (RMAT: ~1 in 10) are packed into
+  // a per-warp queue and searched 32 at a time.  One request per lane of a
+  // row-strided loop left most lanes idle through every ~20-step dependent
+  // search, so the pass took as many search latencies as there were warps
+  // with any request (config 5: 1.18 ms).
+  __shared__ int squeue[256 / 32][64];
+  const int lane = threadIdx.x & 31;
+  int* wq = squeue[threadIdx.x >> 5];
+  int cnt = 0;  // warp-uniform
+  auto search = [&](int v) {
+    const int lv = __ldg(label + v);
+    spos[v] = f.fix_lower(v, lv, __ldg(head + lv));
+  };
+  const int64_t warps = stride >> 5;
+  for (int64_t base = (tid >> 5) * 32; base < n; base += warps * 32) {
+    const int64_t v = base + lane;
+    const bool r = v < n && sreq[v];  // (plain load: the deferred rows above set theirs)
+    const unsigned b = __ballot_sync(0xffffffffu, r);
+    if (r) wq[cnt + __popc(b & ((1u << lane) - 1))] = (int)v;
+    cnt += __popc(b);
+    __syncwarp();
+    if (cnt >= 32) {
+      cnt -= 32;
+      const int sv = wq[cnt + lane];
+      __syncwarp();  // (read before the next appends overwrite the slot)
+      search(sv);
     }
+  }
+  if (lane < cnt) search(wq[lane]);
 }
 
 __device__ __forceinline__ void edge_map(int* edge_label, const int* bmin, int e) {
@@ -473,8 +497,9 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
 // intermediate exports (parity rungs 1-4)
 // ---------------------------------------------------------------------------
 __global__ void k_export(int n, const int4* __restrict__ rec, const int4* __restrict__ AP, int* parent, int* first,
-                         int* last, int* w1, int* w2, uint8_t* fence) {
+                         int* last, int* w1, int* w2, uint8_t* fence, const int* tlen) {
   pdl_enter();
+  const int N = tlen ? *tlen : 2 * n;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
     if (parent) parent[v] = r.z;
@@ -482,7 +507,8 @@ __global__ void k_export(int n, const int4* __restrict__ rec, const int4* __rest
     if (last) last[v] = r.y;
     if (fence) fence[v] = (uint8_t)r.w;
     if (w1 || w2) {
-      int4 a = AP[r.x];
+      // (a detached root has no AP entry: w1 = w2 = first)
+      int4 a = r.x < N ? AP[r.x] : make_int4(r.x, r.x, 0, 0);
       if (w1) w1[v] = a.x;
       if (w2) w2[v] = a.y;
     }
@@ -490,10 +516,10 @@ __global__ void k_export(int n, const int4* __restrict__ rec, const int4* __rest
 }
 
 void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* AP, int* forest, int* parent,
-                  int* first, int* last, int* w1, int* w2, uint8_t* fence, cudaStream_t st) {
+                  int* first, int* last, int* w1, int* w2, uint8_t* fence, cudaStream_t st, const int* tour_len) {
   if (forest) cudaMemcpyAsync(forest, fe, sizeof(int2) * g.n, cudaMemcpyDeviceToDevice, st);
   if (parent || first || last || w1 || w2 || fence)
-    launch(k_export, grid_for(g.n, 256), 256, 0, st, g.n, rec, AP, parent, first, last, w1, w2, fence);
+    launch(k_export, grid_for(g.n, 256), 256, 0, st, g.n, rec, AP, parent, first, last, w1, w2, fence, tour_len);
 }
 
 }  // namespace fbcc

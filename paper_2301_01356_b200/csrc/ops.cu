@@ -13,6 +13,8 @@
 // (vertex, pair) keys), which is the slot order of the reference's counting
 // sort (_tree_csr euler_tour.py:68-89) -- so parent/first/last are identical
 // to the reference's, not just a valid rooting.
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -386,7 +388,7 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   OpSpace L;
   const int64_t N0 = 2 * n;
   size_t o_comp = L.take(4 * n), o_fe = L.take(8 * n), o_flags = L.take(4 * (n + 1)), o_nrank = L.take(4 * (n + 1));
-  size_t o_rootidx = L.take(4 * (n + 1)), o_rlist = L.take(4 * n), o_lhead = L.take(4 * n),
+  size_t o_rootidx = L.take(8 * (n + 1)), o_rlist = L.take(4 * n), o_lhead = L.take(4 * n),
          o_nexto = L.take(4 * N0), o_nxt = L.take(4 * N0), o_own0 = L.take(8 * N0), o_rank0 = L.take(4 * N0),
          o_rec = L.take(16 * n), o_ap = L.take(16 * (size_t)(N0 + kTile));
   size_t o_keys = L.take(8 * 2 * k + 8), o_keys2 = L.take(8 * 2 * k + 8), o_vals = L.take(4 * 2 * k + 4),
@@ -405,7 +407,7 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   size_t o_lev[8][4];
   for (int l = 1; l <= nlev; l++)
     for (int j = 0; j < 4; j++) o_lev[l][j] = L.take((j == 2 ? 8 : 4) * K[l]);
-  size_t scan_b = scan_temp_bytes(n + 1), sort_b = 0;
+  size_t scan_b = std::max(scan_temp_bytes(n + 1), scan_roots_temp_bytes(n + 1)), sort_b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
                                   (int*)nullptr, (int*)nullptr, (int)(2 * k));
   size_t o_tmp = L.take(scan_b > sort_b ? scan_b : sort_b);
@@ -420,7 +422,7 @@ int op_build_euler_tour(int64_t n, const int2* pairs, int64_t k, const int* labe
   int2* fe = (int2*)at(o_fe);
   Rooting R;
   R.flags = (int*)at(o_flags);
-  R.rootidx = (int*)at(o_rootidx);
+  R.rootidx = (unsigned long long*)at(o_rootidx);
   R.rlist = (int*)at(o_rlist);
   R.lhead = (int*)at(o_lhead);
   R.hsub = nullptr;  // pairs input: no CSR, no hub split

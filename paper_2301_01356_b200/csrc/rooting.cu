@@ -58,6 +58,39 @@ void exclusive_scan(const int* in, int* out, int64_t items, void* tmp, size_t tm
   cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int)items, st);
 }
 
+// rootidx: one 64-bit scan gives both ranks of a root -- among the listed
+// roots (low word) and among the detached ones (high word)
+struct RootCode {
+  __host__ __device__ unsigned long long operator()(int c) const {
+    return c == 1 ? 1ull : (c == 2 ? (1ull << 32) : 0ull);
+  }
+};
+using RootIt = cub::TransformInputIterator<unsigned long long, RootCode, const int*>;
+
+size_t scan_roots_temp_bytes(int64_t items) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, RootIt(nullptr, RootCode{}), (unsigned long long*)nullptr,
+                                (int)items);
+  return bytes;
+}
+
+void scan_roots(const int* flags, unsigned long long* out, int64_t items, void* tmp, size_t tmp_bytes,
+                cudaStream_t st) {
+  size_t bytes = tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(tmp, bytes, RootIt(flags, RootCode{}), out, (int)items, st);
+}
+
+__device__ __forceinline__ int lo32(unsigned long long x) { return (int)(uint32_t)x; }
+__device__ __forceinline__ int hi32(unsigned long long x) { return (int)(x >> 32); }
+
+// list / component counts from rootidx[n]
+__device__ __forceinline__ void publish_roots(const unsigned long long* rootidx, int n, Scalars* sc) {
+  const unsigned long long t = rootidx[n];
+  sc->ncomp = lo32(t) + hi32(t);
+  sc->nlisted = lo32(t);
+  sc->tour_len = 2 * (n - hi32(t));
+}
+
 struct UpperDegree {
   const int64_t* off;
   const int* nlow;
@@ -119,14 +152,14 @@ __global__ void k_root_flags(const int* __restrict__ comp, int n, int* __restric
   }
 }
 
-// rlist[rank among roots] = root;  sc->ncomp = c
-__global__ void k_root_list(const int* __restrict__ comp, const int* __restrict__ rootidx, int n,
+// rlist[rank among roots] = root;  sc->ncomp = c (every root listed: codes 0/1)
+__global__ void k_root_list(const int* __restrict__ comp, const unsigned long long* __restrict__ rootidx, int n,
                             int* __restrict__ rlist, Scalars* sc) {
   pdl_enter();
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid == 0) sc->ncomp = rootidx[n];
+  if (tid == 0) publish_roots(rootidx, n, sc);
   for (int r = (int)tid; r < n; r += gridDim.x * blockDim.x)
-    if (__ldg(comp + r) == r) rlist[__ldg(rootidx + r)] = r;
+    if (__ldg(comp + r) == r) rlist[lo32(__ldg(rootidx + r))] = r;
 }
 
 // out-arc lists: arc 2x = u->v is an out-arc of u, 2x+1 = v->u of v
@@ -141,14 +174,15 @@ __device__ __forceinline__ int* list_head(int* lhead, int* hsub, int t, int x, b
 // (rootidx != nullptr: also k_root_list's work -- roots placed in id order,
 // c published -- in the same pass over the vertices)
 __global__ void k_out_lists(const int* __restrict__ comp, const int2* __restrict__ fe, int n, int* lhead,
-                            int* __restrict__ nexto, int* hsub, Scalars* sc, const int* __restrict__ rootidx,
+                            int* __restrict__ nexto, int* hsub, Scalars* sc,
+                            const unsigned long long* __restrict__ rootidx, const int* __restrict__ flags,
                             int* __restrict__ rlist) {
   pdl_enter();
   const bool split = hsub != nullptr && sc->has_hubs;
-  if (rootidx && blockIdx.x == 0 && threadIdx.x == 0) sc->ncomp = rootidx[n];
+  if (rootidx && blockIdx.x == 0 && threadIdx.x == 0) publish_roots(rootidx, n, sc);
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     if (__ldg(comp + x) == x) {
-      if (rootidx) rlist[__ldg(rootidx + x)] = x;
+      if (rootidx && __ldg(flags + x) == 1) rlist[lo32(__ldg(rootidx + x))] = x;
       continue;
     }
     int2 e = __ldg(fe + x);
@@ -190,23 +224,30 @@ __device__ __forceinline__ int flag_succ(int s, int sh, int N) {
   return (s >= 0 && sh >= 0 && is_split(s, sh, N)) ? ~s : s;
 }
 
+// A detached root's pair is no list element: both end at once (-1).  Should
+// the hash pick one as a splitter, its walker stops there and leaves a
+// detached element on the next level -- unreachable from the head, never
+// read back (k_positions places detached roots from rootidx).
 __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict__ fe,
                             const int* __restrict__ lhead, const int* __restrict__ hsub, const int* __restrict__ nexto,
-                            const int* __restrict__ rootidx, const int* __restrict__ rlist, int n,
+                            const unsigned long long* __restrict__ rootidx, const int* __restrict__ flags,
+                            const int* __restrict__ rlist, int n,
                             int* __restrict__ nxt, int2* __restrict__ own0, const Scalars* sc, int sh0) {
   pdl_enter();
-  const int c = sc->ncomp;
+  const int c = sc->nlisted;
   const int64_t N = 2 * (int64_t)n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
     int x = (int)(e >> 1);
     int out;
     if (__ldg(comp + x) == x) {  // enter(x) / exit(x)
-      if ((e & 1) == 0) {
+      if (__ldg(flags + x) == 2) {
+        out = -1;
+      } else if ((e & 1) == 0) {
         int h = __ldg(lhead + x);
         if (h <= -2) h = hub_next(hsub, h, 0);
         out = h >= 0 ? h : (int)e + 1;
       } else {
-        int ri = __ldg(rootidx + x);
+        int ri = lo32(__ldg(rootidx + x));
         out = (ri + 1 < c) ? 2 * __ldg(rlist + ri + 1) : -1;
       }
     } else {  // arc e arrives at t; leave through the out-arc after e^1
@@ -337,15 +378,22 @@ __global__ void __launch_bounds__(kFinalThreads) k_final_rank(int K, const int* 
     VS[t] = v;
     __syncthreads();
   }
-  for (int j = t; j < K; j += kFinalThreads) offs[j] = VS[S[j]] + W[j];
+  // (an element no walker reached -- a detached one -- keeps its successor
+  // in S: its offset is never read, but must not index out of VS)
+  for (int j = t; j < K; j += kFinalThreads) {
+    const int o = S[j];
+    offs[j] = (o >= 0 && o < kFinalThreads) ? VS[o] + W[j] : 0;
+  }
 }
 
-__global__ void k_expand(int64_t K, const int2* __restrict__ own, const int* __restrict__ offs_up,
+// (own[j] of an element no walker reached -- detached, see k_link_tour --
+// was never written: clamp the index, the value is never read)
+__global__ void k_expand(int64_t K, const int2* __restrict__ own, const int* __restrict__ offs_up, int64_t K_up,
                          int* __restrict__ offs) {
   pdl_enter();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < K; j += (int64_t)gridDim.x * blockDim.x) {
     int2 o = own[j];
-    offs[j] = __ldg(offs_up + o.x) + o.y;
+    offs[j] = ((uint32_t)o.x < (uint64_t)K_up) ? __ldg(offs_up + o.x) + o.y : 0;
   }
 }
 
@@ -363,24 +411,36 @@ __device__ __forceinline__ void place(int v, int f, int l, int par, int4* rec, i
 
 // level-0 ranks, coalesced over elements (the offs1 gathers hit L2 here,
 // instead of competing with the positions kernel's scattered stores)
-__global__ void k_rank0(int64_t N, const int2* __restrict__ own0, const int* __restrict__ offs1,
+__global__ void k_rank0(int64_t N, const int2* __restrict__ own0, const int* __restrict__ offs1, int64_t K1,
                         int* __restrict__ rank0) {
   pdl_enter();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
     int2 o = __ldg(own0 + e);
-    rank0[e] = __ldg(offs1 + o.x) + o.y;
+    rank0[e] = ((uint32_t)o.x < (uint64_t)K1) ? __ldg(offs1 + o.x) + o.y : 0;  // (detached: unread)
   }
 }
 
 // (own0 != nullptr: the level-0 ranks are expanded here -- rank(e) =
 // offs1[own0[e].seg] + own0[e].off, one 16-byte load for both elements of x
 // -- instead of by k_rank0)
+// A detached root x (code 2) is no list element: its tree is x alone, at
+// positions tour_len + 2 d and + 1 (d = its rank among the detached, the
+// high word of rootidx) -- one coalesced record, no AP entries (the tile
+// pass stops at tour_len and Stage 4 answers low = high = first for it).
 __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict__ fe,
                             const int2* __restrict__ rank0, int n, int4* __restrict__ rec,
                             int4* __restrict__ AP, int* __restrict__ firsts, const int4* __restrict__ own0,
-                            const int* __restrict__ offs1) {
+                            const int* __restrict__ offs1, const int* __restrict__ flags,
+                            const unsigned long long* __restrict__ rootidx, const Scalars* sc) {
   pdl_enter();
+  const int tour_len = sc->tour_len;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    if (__ldg(flags + x) == 2) {
+      const int f = tour_len + 2 * hi32(__ldg(rootidx + x));
+      rec[x] = make_int4(f, f + 1, -1, 0);
+      if (firsts) firsts[x] = f;
+      continue;
+    }
     int2 r;
     if (own0) {
       const int4 o = __ldg(own0 + x);  // (seg, off) of elements 2x and 2x+1
@@ -404,7 +464,7 @@ void rooting_roots(int n, const int* comp, Rooting& R, Scalars* sc, cudaStream_t
   const int gv = grid_for(n + 1, B);
   launch(k_root_flags, gv, B, 0, st, comp, n, R.flags, R.lhead, R.hoff, R.hoff ? R.hsub : nullptr, sc);
   note(K_ROOT_FLAGS);
-  exclusive_scan(R.flags, R.rootidx, n + 1, R.cub_tmp, R.cub_bytes, st);
+  scan_roots(R.flags, R.rootidx, n + 1, R.cub_tmp, R.cub_bytes, st);
   note(K_SCAN);
   launch(k_root_list, gv, B, 0, st, comp, R.rootidx, n, R.rlist, sc);
   note(K_ROOT_LIST);
@@ -416,7 +476,7 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
   // Euler circuit: out-arc lists in atomicExch order (any order is a valid
   // tour; the final outputs do not depend on it)
   launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto, R.hoff ? R.hsub : nullptr, sc,
-         (const int*)nullptr, (int*)nullptr);
+         (const unsigned long long*)nullptr, (const int*)nullptr, (int*)nullptr);
   note(K_OUT_LISTS);
   rooting_tour(g.n, comp, fe, R, AP, sc, st);
 }
@@ -424,10 +484,10 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
 void stage2_rooting_fused(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc,
                           cudaStream_t st) {
   // R.flags / R.lhead / R.hsub were written by Stage 1's final compress
-  exclusive_scan(R.flags, R.rootidx, g.n + 1, R.cub_tmp, R.cub_bytes, st);
+  scan_roots(R.flags, R.rootidx, g.n + 1, R.cub_tmp, R.cub_bytes, st);
   note(K_SCAN);
   launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto, R.hoff ? R.hsub : nullptr, sc,
-         (const int*)R.rootidx, R.rlist);
+         (const unsigned long long*)R.rootidx, (const int*)R.flags, R.rlist);
   note(K_OUT_LISTS);
   rooting_tour(g.n, comp, fe, R, AP, sc, st);
 }
@@ -445,7 +505,8 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
   // walks gain (config 5 walk0 1.65 -> 0.92 ms), L2-resident ones lose
   // (config 2: the next element often shares the stored sector)
   const bool inplace = (int64_t)N0 * 8 > (64ll << 20) || !R.nxt;
-  launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.hsub, R.nexto, R.rootidx, R.rlist, n,
+  launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.hsub, R.nexto,
+         (const unsigned long long*)R.rootidx, (const int*)R.flags, R.rlist, n,
          inplace ? (int*)nullptr : R.nxt, R.own0, sc,
                                              shift(R.S[0]));
   note(K_LINK_TOUR);
@@ -465,7 +526,7 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
                                                       R.offs[R.nlev]);
   note(K_FINAL_RANK);
   for (int l = R.nlev - 1; l >= 1; l--) {
-    launch(k_expand, grid_for(R.K[l], B), B, 0, st, R.K[l], R.own[l], R.offs[l + 1], R.offs[l]);
+    launch(k_expand, grid_for(R.K[l], B), B, 0, st, R.K[l], R.own[l], R.offs[l + 1], R.K[l + 1], R.offs[l]);
     note(K_EXPAND);
   }
 #ifndef FBCC_FUSED_RANK0
@@ -473,13 +534,15 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
 #endif
   if (FBCC_FUSED_RANK0) {
     launch(k_positions, gv, B, 0, st, comp, fe, (const int2*)nullptr, n, R.rec, AP, R.firsts,
-           reinterpret_cast<const int4*>(R.own0), (const int*)R.offs[1]);
+           reinterpret_cast<const int4*>(R.own0), (const int*)R.offs[1], (const int*)R.flags,
+           (const unsigned long long*)R.rootidx, (const Scalars*)sc);
     note(K_POSITIONS);
   } else {
-    launch(k_rank0, grid_for(N0, B), B, 0, st, N0, R.own0, R.offs[1], R.rank0);
+    launch(k_rank0, grid_for(N0, B), B, 0, st, N0, R.own0, R.offs[1], R.K[1], R.rank0);
     note(K_RANK0);
     launch(k_positions, gv, B, 0, st, comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP, R.firsts,
-           (const int4*)nullptr, (const int*)nullptr);
+           (const int4*)nullptr, (const int*)nullptr, (const int*)R.flags, (const unsigned long long*)R.rootidx,
+           (const Scalars*)sc);
     note(K_POSITIONS);
   }
 }

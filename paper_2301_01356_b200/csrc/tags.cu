@@ -283,25 +283,34 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 
 constexpr int kTableOneCta = 16384;
 
-__device__ __forceinline__ void table_levels(int2* table, int ntile, int tlev) {
+// (levels laid out with stride ntile; entries at and past nt -- tiles past
+// the list -- are neither built nor queried)
+__device__ __forceinline__ void table_levels(int2* table, int ntile, int nt, int tlev) {
   for (int k = 1; k < tlev; k++) {
     const int2* prev = table + (int64_t)(k - 1) * ntile;
     int2* cur = table + (int64_t)k * ntile;
     const int half = 1 << (k - 1);
-    for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
       int2 a = prev[i];
-      cur[i] = (i + half < ntile) ? comb(a, prev[i + half]) : a;
+      cur[i] = (i + half < nt) ? comb(a, prev[i + half]) : a;
     }
     __syncthreads();
   }
 }
 
+// tiles holding list positions: the pipeline's tour stops at tour_len
+// (detached roots have no AP entries)
+__device__ __forceinline__ int64_t list_positions(const int* tlen, int64_t N) { return tlen ? *tlen : N; }
+
 // (sc != nullptr: the last block to finish also builds every level of the
 // tile-extreme sparse table -- k_table_all's work, one launch fewer)
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict__ AP,
                                                           int64_t N, int ntile, int2* __restrict__ lh1,
-                                                          int2* __restrict__ lh2, int2* __restrict__ table0, Scalars* sc, int tlev) {
+                                                          int2* __restrict__ lh2, int2* __restrict__ table0, Scalars* sc, int tlev,
+                                                          const int* tlen) {
   pdl_enter();
+  N = list_positions(tlen, N);
+  const int nt = (int)((N + kTile - 1) / kTile);
   extern __shared__ __align__(128) unsigned char tsm[];
   int4* buf0 = reinterpret_cast<int4*>(tsm);
   int4* buf1 = reinterpret_cast<int4*>(tsm + kTileBytes);
@@ -323,12 +332,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (blockIdx.x < ntile) bulk_load(buf0, AP + (int64_t)blockIdx.x * kTile, kTileBytes, bars);
-    if (blockIdx.x + G < ntile) bulk_load(buf1, AP + (int64_t)(blockIdx.x + G) * kTile, kTileBytes, bars + 1);
+    if (blockIdx.x < nt) bulk_load(buf0, AP + (int64_t)blockIdx.x * kTile, kTileBytes, bars);
+    if (blockIdx.x + G < nt) bulk_load(buf1, AP + (int64_t)(blockIdx.x + G) * kTile, kTileBytes, bars + 1);
   }
   uint32_t parity = 0;  // bit b: phase of buffer b's barrier
   int k = 0;
-  for (int tile = blockIdx.x; tile < ntile; tile += G, k++) {
+  for (int tile = blockIdx.x; tile < nt; tile += G, k++) {
     const int b = k & 1;
     const int4* T = b ? buf1 : buf0;
     S.raw = T;
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict
       }
     }
     __syncthreads();  // buffer b and the scan arrays are free
-    if (threadIdx.x == 0 && tile + 2 * G < ntile)
+    if (threadIdx.x == 0 && tile + 2 * G < nt)
       bulk_load(b ? buf1 : buf0, AP + (int64_t)(tile + 2 * G) * kTile, kTileBytes, bars + b);
   }
   if (sc) {
@@ -389,7 +398,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict
     __syncthreads();
     if (last) {
       __threadfence();
-      table_levels(table0, ntile, tlev);
+      table_levels(table0, ntile, nt, tlev);
       if (threadIdx.x == 0) sc->tile_ticket = 0;
     }
   }
@@ -399,19 +408,20 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict
 // published to the block by __syncthreads; every level is tiny next to a
 // launch when ntile <= kTableOneCta)
 
-__global__ void __launch_bounds__(1024) k_table_all(int2* table, int ntile, int tlev) {
+__global__ void __launch_bounds__(1024) k_table_all(int2* table, int ntile, int tlev, const int* tlen) {
   pdl_enter();
-  table_levels(table, ntile, tlev);
+  table_levels(table, ntile, (int)((list_positions(tlen, (int64_t)ntile * kTile) + kTile - 1) / kTile), tlev);
 }
 
-__global__ void k_table_level(int2* table, int ntile, int k) {
+__global__ void k_table_level(int2* table, int ntile, int k, const int* tlen) {
   pdl_enter();
+  const int nt = (int)((list_positions(tlen, (int64_t)ntile * kTile) + kTile - 1) / kTile);
   const int2* prev = table + (int64_t)(k - 1) * ntile;
   int2* cur = table + (int64_t)k * ntile;
   const int half = 1 << (k - 1);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ntile; i += gridDim.x * blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += gridDim.x * blockDim.x) {
     int2 a = prev[i];
-    cur[i] = (i + half < ntile) ? comb(a, prev[i + half]) : a;
+    cur[i] = (i + half < nt) ? comb(a, prev[i + half]) : a;
   }
 }
 
@@ -448,17 +458,17 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
   // (the table in k_tile's last block when it fits one CTA and a ticket word exists)
   Scalars* tsc = (sc && T.ntile <= kTableOneCta && T.tlev > 1) ? sc : nullptr;
   launch(k_tile, T.ntile < kNumSMs ? T.ntile : kNumSMs, kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile,
-         T.lh1, T.lh2, T.table, tsc, T.tlev);
+         T.lh1, T.lh2, T.table, tsc, T.tlev, T.tour_len);
   note(K_TILE);
   if (tsc) {
   } else if (T.ntile <= kTableOneCta) {
     if (T.tlev > 1) {
-      launch(k_table_all, 1, 1024, 0, st, T.table, T.ntile, T.tlev);
+      launch(k_table_all, 1, 1024, 0, st, T.table, T.ntile, T.tlev, T.tour_len);
       note(K_TABLE);
     }
   } else {
     for (int k = 1; k < T.tlev; k++) {
-      launch(k_table_level, grid_for(T.ntile, B), B, 0, st, T.table, T.ntile, k);
+      launch(k_table_level, grid_for(T.ntile, B), B, 0, st, T.table, T.ntile, k, T.tour_len);
       note(K_TABLE);
     }
   }
@@ -469,13 +479,19 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
 // ---------------------------------------------------------------------------
 __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const int2* __restrict__ lh2,
                         const int2* __restrict__ table, int ntile, int* low_out, int* high_out,
-                        int* __restrict__ head, int* __restrict__ cnt, int* __restrict__ bmin) {
+                        int* __restrict__ head, int* __restrict__ cnt, int* __restrict__ bmin, const int* tlen) {
   pdl_enter();
+  const int64_t N = list_positions(tlen, 2 * (int64_t)n);
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
     int ta = r.x / kTile, tb = r.y / kTile;
-    int2 res = lh1[v];
-    if (ta != tb) {
+    int2 res;
+    if (r.x >= N) {  // detached root: {v} alone, low = high = first
+      res = make_int2(r.x, r.x);
+    } else {
+      res = lh1[v];
+    }
+    if (r.x < N && ta != tb) {
       res = comb(res, lh2[v]);
       if (tb - ta > 1) {
         int i = ta + 1, j = tb - 1;
@@ -505,7 +521,7 @@ void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out,
                   int* bmin, cudaStream_t st) {
   const int B = 256;
   launch(k_fence, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out, head,
-                                          cnt, bmin);
+                                          cnt, bmin, T.tour_len);
   note(K_FENCE);
 }
 

@@ -68,7 +68,7 @@ def test_mid_graph_rungs(name, oracle_mod):
     lab1, _, ncomp = oracle_mod.connected_components(g.offsets, g.edges)
     assert np.array_equal(r["comp"], lab1), "rung 1: component labels"
     pairs = _check_forest(g, r["comp"], d["forest"][:2 * n])
-    _check_rooting(n, r["comp"], pairs, d, oracle_mod)
+    _check_rooting(n, r["comp"], pairs, d, oracle_mod, np.diff(g.offsets))
     p, f, l = d["parent"][:n], d["first"][:n], d["last"][:n]
     w1, w2 = oracle_mod.compute_w(g.offsets, g.edges, p, f)
     assert np.array_equal(d["w1"][:n], w1), "rung 3: w1"
@@ -96,7 +96,7 @@ def test_mid_graph_rungs(name, oracle_mod):
 OPTION_VARIANTS = [{"eb_staged": 0}, {"max_rounds": 6}, {"max_rounds": 8, "sample_rounds": 2}, {"pdl": 0},
                    {"sample_rounds": 1}, {"giant_skip": 0}, {"s0": 8, "sl": 4}, {"accept_fold": 1},
                    {"accept_fold": 1, "max_rounds": 5}, {"skel_parent": 131}, {"skel_max_rounds": 4},
-                   {"compress_mask": 0}]
+                   {"compress_mask": 0}, {"detach": 0}, {"detach": 0, "s0": 8, "sl": 4}]
 
 
 @pytest.mark.parametrize("name", ["rmat_s16", "isolated_mix", "star_mid_20k", "uniform_64k_d3", "chain_300k",

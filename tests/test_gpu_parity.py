@@ -63,7 +63,7 @@ def _check_forest(g, comp, forest2):
     return pairs
 
 
-def _check_rooting(n, comp, pairs, dbg, oracle):
+def _check_rooting(n, comp, pairs, dbg, oracle, deg=None):
     # rung 2: parents are the unique rooting of the GPU forest at min-id roots
     parent_o, _, _ = oracle.root_forest(n, comp, pairs)
     assert np.array_equal(dbg["parent"][:n], parent_o)
@@ -74,8 +74,20 @@ def _check_rooting(n, comp, pairs, dbg, oracle):
     nr = p >= 0
     assert np.all(first[p[nr]] < first[nr]) and np.all(last[nr] < last[p[nr]])
     roots = np.flatnonzero(~nr)
+    listed = roots
+    if deg is not None:
+        from paper_2301_01356_b200 import _lib
+
+        if _lib.get_option("detach"):
+            # isolated roots (but vertex 0) are off the list: they follow it,
+            # in id order (rooting.cu k_positions)
+            off_list = (deg[roots] == 0) & (roots != 0)
+            det, listed = roots[off_list], roots[~off_list]
+            L = 2 * (n - len(det))
+            assert np.array_equal(first[det], L + 2 * np.arange(len(det)))
+            assert np.all(first[listed] < L)
     # trees are laid out in root-id order, root at both ends (euler_tour.py:12-17)
-    assert np.all(np.diff(first[roots]) > 0)
+    assert np.all(np.diff(first[listed]) > 0)
 
 
 def test_corpus_all_rungs(corpus, oracle_mod):
@@ -88,7 +100,7 @@ def test_corpus_all_rungs(corpus, oracle_mod):
         # rung 1
         assert np.array_equal(r["comp"], corpus.get(i, "cc_label")), name
         pairs = _check_forest(g, r["comp"], d["forest"][:2 * n])
-        _check_rooting(n, r["comp"], pairs, d, oracle_mod)
+        _check_rooting(n, r["comp"], pairs, d, oracle_mod, np.diff(g.offsets))
         # rung 3/4: oracle tags on the GPU's own rooted forest
         w1, w2 = oracle_mod.compute_w(g.offsets, g.edges, d["parent"][:n], d["first"][:n])
         assert np.array_equal(d["w1"][:n], w1), name
