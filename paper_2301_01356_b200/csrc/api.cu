@@ -19,7 +19,8 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "chunk_rows", "hook_min", "iota", "propose", "accept", "compress", "find_giant", "link_rows", "link_heavy",
     "root_flags", "scan", "root_list", "out_lists", "link_tour", "walk0", "walk_level", "final_rank", "expand", "rank0",
     "positions", "firsts", "w_gather", "tile", "table", "fence", "heads", "count_blocks", "ap", "set_edges",
-    "edge_blocks", "edge_final", "memset", "export", "widen", "giant_min", "edge_fill", "edge_search"};
+    "edge_blocks", "edge_final", "memset", "export", "widen", "giant_min", "edge_fill", "edge_search", "jump_local",
+    "jump_list"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -205,7 +206,7 @@ struct Pipeline {
     mk(0);
     const bool round0 = build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, comp, fe, prop, nlow, w0);
     w0_valid = round0;
-    stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args(), round0 ? w0 : nullptr);
+    stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args(), round0 ? w0 : nullptr, R.nexto);
     mk(1);
     enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
   }

@@ -32,7 +32,9 @@ struct Scalars {
   int emega;       // ... grid tier of eheavy
   int nlisted;     // roots on the Euler-tour list (code 1)
   int tour_len;    // list elements = 2 (n - detached roots); detached positions follow
-  int pad[15];
+  int near[2];     // round-0 hooks to a vertex within kNear ids (stage 1 / stage 5): id-ordered chains (meshes)
+  int jlist_n[2];  // exit targets listed by k_jump_local (same split)
+  int pad[11];
 };
 
 // ---------------------------------------------------------------------------
@@ -43,7 +45,8 @@ enum KernelKind : int {  // one kind per kernel function (names: api.cu kKernelN
   K_CHUNK_ROWS = 0, K_HOOK_MIN, K_IOTA, K_PROPOSE, K_ACCEPT, K_COMPRESS, K_FIND_GIANT, K_LINK_ROWS, K_LINK_HEAVY,
   K_ROOT_FLAGS, K_SCAN, K_ROOT_LIST, K_OUT_LISTS, K_LINK_TOUR, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_RANK0,
   K_POSITIONS, K_FIRSTS, K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_COUNT_BLOCKS, K_AP, K_SET_EDGES,
-  K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_WIDEN, K_GIANT_MIN, K_EDGE_FILL, K_EDGE_SEARCH, K_NUM_KINDS
+  K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_WIDEN, K_GIANT_MIN, K_EDGE_FILL, K_EDGE_SEARCH, K_JUMP_LOCAL,
+  K_JUMP_LIST, K_NUM_KINDS
 };
 
 struct LaunchLog {

@@ -190,6 +190,7 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int near = 0;  // round-0 hooks within kNear ids (see k_jump_local)
   for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n; base += warps * 32) {
     const int v = (int)base + lane;
     int q0 = 0, q1 = 0;
@@ -204,6 +205,7 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
           int first = v;
           c = round0_target(adj, v, rs, re, &first);
           if (c < v) fe[v] = make_int2(v, c);
+          near += c < v && v - c <= kNear;
           w0[v] = first;  // Stage 5's round-0 arc (coalesced; saves it a cold sector per row)
         }
         // arcs 1 and 2 for the sampling rounds of Stages 1 and 5 (same
@@ -228,6 +230,7 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
       for (int q = h0 + lane; q < h1; q += 32) crow[q] = hv;
     }
   }
+  if (comp) block_count_add(&sc->near[0], near);
 }
 
 bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp, int2* fe,
@@ -417,6 +420,12 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
 // without reaching a root the thread switches to L2 reads with stores
 // (doubling), for the deep chains of path-like graphs.
 constexpr int kL1Steps = 8;
+#ifndef FBCC_JUMP_EARLY_STORE
+#define FBCC_JUMP_EARLY_STORE 0
+#endif
+#ifndef FBCC_JUMP_BLOCK
+#define FBCC_JUMP_BLOCK 256
+#endif
 
 __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable);
 
@@ -465,7 +474,7 @@ __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, boo
       }
     }
     const bool root = c == v;
-    const int mem = c;  // what comp[v] holds now
+    int mem = c;  // what comp[v] holds now
     if (kJump) {
       // Pointer jumping inside the block's id range (after sampling round 0
       // only): chains of consecutive ids -- round 0's left-neighbour hooks on
@@ -487,6 +496,14 @@ __global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, boo
         }
       }
       __syncthreads();  // sp is rewritten next step
+#if FBCC_JUMP_EARLY_STORE
+      // publish the in-block result before the global climb: a neighbouring
+      // block's climb through this block then takes one hop, not the raw chain
+      if (v < n && c != mem) {
+        __stcg(comp + v, c);
+        mem = c;
+      }
+#endif
     }
     if (v >= n) continue;
     roots += root;
@@ -697,6 +714,183 @@ __global__ void __launch_bounds__(256) k_link_heavy(const int64_t* __restrict__ 
       });
 }
 
+// ---------------------------------------------------------------------------
+// Round-0 compress of id-ordered forests (large meshes and paths: configs 4a,
+// 4c).  Round 0's near rule hooks each vertex to its left neighbour, so the
+// forest is made of chains of consecutive ids -- 10^4 per torus row, 10^8 on
+// the path -- and k_compress<kJump> alone spends its time on waves of blocks
+// each waiting for its left neighbour (4a 1.6 ms, 4c 1.9 ms for 0.8 GB of
+// traffic).  When at least 3/4 of the vertices made a near hook:
+//   1. k_jump_local: every 2048-id tile is flattened on its own (8 ids per
+//      thread in registers, then pointer doubling in shared memory), stored,
+//      and the tile's distinct exit targets -- the only vertices that can still
+//      be interior to a chain -- are appended to a list;
+//   2. k_jump_list: pointer doubling over the listed vertices only (tens of
+//      thousands, all resident), which flattens every chain's interior;
+//   3. the ordinary k_compress<kJump> then finds every vertex at most two
+//      hops from its root.
+// Any other graph (fewer near hooks, or more exit targets than the list
+// holds) leaves both kernels at once and k_compress does all the work as
+// before; both are launched only for n >= kJumpListMinN.
+// ---------------------------------------------------------------------------
+constexpr int kJumpTile = 2048;
+constexpr int kJumpPer = kJumpTile / 256;
+constexpr int kJumpListCap = 1 << 18;     // <= resident threads (148 x 2048)
+constexpr int kJumpListMinN = 1 << 22;
+
+__device__ __forceinline__ bool jump_mode(const Scalars* sc, int slot, int n) {
+  return (int64_t)sc->near[slot] * 4 >= (int64_t)n * 3;
+}
+
+__global__ void __launch_bounds__(256) k_jump_local(int* comp, int n, Scalars* sc, int slot, int* __restrict__ list) {
+  pdl_enter();
+  if (!jump_mode(sc, slot, n)) return;
+  __shared__ int sp[kJumpTile];
+  __shared__ int wsum[8];
+  __shared__ int lbase;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(comp) & 15) == 0;
+  for (int64_t base = (int64_t)blockIdx.x * kJumpTile; base < n; base += (int64_t)gridDim.x * kJumpTile) {
+    const int v0 = (int)base + t * kJumpPer;
+    int c[kJumpPer], c_in[kJumpPer];
+    if (vec_ok && v0 + kJumpPer <= n) {
+      const int4 a = __ldcg(reinterpret_cast<const int4*>(comp + v0));
+      const int4 b = __ldcg(reinterpret_cast<const int4*>(comp + v0) + 1);
+      c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < kJumpPer; i++) c[i] = v0 + i < n ? __ldcg(comp + v0 + i) : v0 + i;
+    }
+#pragma unroll
+    for (int i = 0; i < kJumpPer; i++) c_in[i] = c[i];
+    // Runs of consecutive ids, each hooked to its left neighbour, collapse in
+    // one segmented copy-scan: an id whose pointer is not v - 1 (or the tile's
+    // first id) heads a run, and every member takes its head's pointer.
+    // Thread: sweep its 8 ids with the carry of the ids before them; the carry
+    // is the pointer of the last head in the preceding threads (warp shuffles,
+    // then the 8 warp totals through shared memory).
+    bool has = false;  // this thread holds a head
+    int hv = 0;        // ... the last one's pointer
+#pragma unroll
+    for (int i = 0; i < kJumpPer; i++) {
+      const bool head = c[i] != v0 + i - 1 || (t == 0 && i == 0);
+      if (head) { has = true; hv = c[i]; }
+    }
+    bool ihas = has;  // inclusive scan over the lanes: (has, hv) of the last head at or before this thread
+    int ihv = hv;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ph = __shfl_up_sync(0xffffffffu, (int)ihas, o), pv = __shfl_up_sync(0xffffffffu, ihv, o);
+      if (lane >= o && !ihas) { ihas = ph != 0; ihv = pv; }
+    }
+    if (lane == 31) { wsum[warp] = ihas ? 1 : 0; sp[warp] = ihv; }
+    __syncthreads();
+    // exclusive carry: the previous lane's inclusive value, else the last head of the earlier warps
+    int carry = __shfl_up_sync(0xffffffffu, ihv, 1);
+    bool chas = __shfl_up_sync(0xffffffffu, (int)ihas, 1) != 0 && lane > 0;
+    if (!chas) {
+      for (int w = warp - 1; w >= 0; w--)
+        if (wsum[w]) { carry = sp[w]; chas = true; break; }
+    }
+    __syncthreads();  // (wsum / sp are rewritten below)
+#pragma unroll
+    for (int i = 0; i < kJumpPer; i++) {
+      const bool head = c[i] != v0 + i - 1 || (t == 0 && i == 0);
+      if (head) carry = c[i];
+      else c[i] = carry;  // (a member always has a head before it in the tile: id base is one)
+    }
+    // (id r of the tile lives at sp[jslot(r)]: the 8 ids of a thread sit 256
+    // words apart, so the warp's stores and the chain case's loads -- every
+    // thread reading its left neighbour's last id -- are free of bank conflicts)
+#pragma unroll
+    for (int i = 0; i < kJumpPer; i++) sp[i * 256 + t] = c[i];
+    __syncthreads();
+    // pointer doubling inside the tile (equal neighbours -- a run hooked to
+    // one target -- share one load)
+    for (int r = 0; r < 12; r++) {
+      bool moved = false;
+      int last_c = -1, last_nc = -1;
+#pragma unroll
+      for (int i = 0; i < kJumpPer; i++) {
+        const int rel = c[i] - (int)base;
+        if (rel >= 0 && rel < kJumpTile) {
+          const int nc = c[i] == last_c ? last_nc : sp[(rel & (kJumpPer - 1)) * 256 + (rel >> 3)];
+          last_c = c[i];
+          last_nc = nc;
+          moved |= nc != c[i];
+          c[i] = nc;
+        }
+      }
+      if (!__syncthreads_or(moved)) break;
+#pragma unroll
+      for (int i = 0; i < kJumpPer; i++) sp[i * 256 + t] = c[i];
+      __syncthreads();
+    }
+    bool changed = false;
+#pragma unroll
+    for (int i = 0; i < kJumpPer; i++) changed |= c[i] != c_in[i];
+    if (changed) {
+      if (vec_ok && v0 + kJumpPer <= n) {
+        __stcg(reinterpret_cast<int4*>(comp + v0), make_int4(c[0], c[1], c[2], c[3]));
+        __stcg(reinterpret_cast<int4*>(comp + v0) + 1, make_int4(c[4], c[5], c[6], c[7]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < kJumpPer; i++)
+          if (v0 + i < n) __stcg(comp + v0 + i, c[i]);
+      }
+    }
+    // the tile's exit targets (pointers leaving the tile), runs of equal
+    // targets listed once; duplicates across tiles are harmless
+    const int prev = t > 0 ? sp[(kJumpPer - 1) * 256 + t - 1] : -1;  // (sp holds the final values: the last round moved nothing)
+    int cnt = 0;
+    bool ex[kJumpPer];
+#pragma unroll
+    for (int i = 0; i < kJumpPer; i++) {
+      ex[i] = v0 + i < n && c[i] < (int)base && c[i] != (i ? c[i - 1] : prev);
+      cnt += ex[i];
+    }
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (t == 0) {
+      int tot = 0;
+      for (int w = 0; w < 8; w++) { const int x = wsum[w]; wsum[w] = tot; tot += x; }
+      lbase = tot ? atomicAdd(&sc->jlist_n[slot], tot) : 0;
+    }
+    __syncthreads();
+    int pos = lbase + wsum[warp] + incl - cnt;
+#pragma unroll
+    for (int i = 0; i < kJumpPer; i++)
+      if (ex[i]) {
+        if (pos < kJumpListCap) list[pos] = c[i];
+        pos++;
+      }
+    __syncthreads();  // sp / wsum / lbase are rewritten by the next tile
+  }
+}
+
+// (grid: all kJumpListCap threads resident -- each entry rides the others' progress)
+__global__ void __launch_bounds__(256) k_jump_list(int* comp, int n, const Scalars* sc, int slot,
+                                                   const int* __restrict__ list) {
+  pdl_enter();
+  if (!jump_mode(sc, slot, n)) return;
+  const int cnt = sc->jlist_n[slot];
+  if (cnt > kJumpListCap) return;  // too many interior vertices: k_compress does the work
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const int u = list[i];
+    int c = __ldcg(comp + u);
+    while (true) {
+      const int cc = __ldcg(comp + c);
+      if (cc == c) break;
+      __stcg(comp + u, cc);
+      c = cc;
+    }
+  }
+}
+
 // The schedule shared by Stage 1 (no predicate, forest recorded), Stage 5
 // (skeleton predicate) and the masked stand-alone op.  `slot` picks the
 // sampling counters (0 / 8) in Scalars.
@@ -704,7 +898,7 @@ __global__ void __launch_bounds__(256) k_link_heavy(const int64_t* __restrict__ 
 // ri: the final compress also writes Stage 2's root flags / list heads.
 template <int kPred, bool kRecord>
 static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop, PredData pd, Scalars* sc,
-                   int slot, cudaStream_t st, bool round0_done = false, RootInit ri = RootInit{}) {
+                   int slot, cudaStream_t st, bool round0_done = false, RootInit ri = RootInit{}, int* jlist = nullptr) {
   const int B = 256;
   const int kBase = opt(OPT_SAMPLE_ROUNDS);
   // adaptive rounds kBase .. kRounds-1 (skip_round); Stage 5 may cap them separately
@@ -760,7 +954,16 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
                opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase, prop, hooks + r, fe, g.off, g.adj,
                pd.warc);
       } else {
-        launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
+        if (r == 0 && jlist && g.n >= kJumpListMinN) {  // id-ordered chains (see k_jump_local)
+          launch(k_jump_local, grid_for((g.n + kJumpTile - 1) / kJumpTile, 1, 8), 256, 0, st, comp, g.n, sc, slot ? 1 : 0,
+                 jlist);
+          note(K_JUMP_LOCAL);
+          launch(k_jump_list, grid_for(kJumpListCap, B, 2048 / B), B, 0, st, comp, g.n, (const Scalars*)sc,
+                 slot ? 1 : 0, (const int*)jlist);
+          note(K_JUMP_LIST);
+        }
+        const int JB = r == 0 ? FBCC_JUMP_BLOCK : B;
+        launch(r == 0 ? k_compress<true> : k_compress<false>, r == 0 ? grid_for(g.n, JB, 2048 / JB) : gres, JB, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
                last_round ? sc : nullptr, opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase,
                (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
                (const uint32_t*)nullptr, (const int*)nullptr);
@@ -863,10 +1066,10 @@ void widen_offsets(const int* src, int64_t* dst, int64_t n, cudaStream_t st) {
 }
 
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st,
-                   bool round0_done, RootInit ri, const int* warc) {
+                   bool round0_done, RootInit ri, const int* warc, int* jlist) {
   PredData pd{};
   pd.warc = warc;
-  run_cc<PRED_NONE, true>(g, comp, fe, prop, pd, sc, 0, st, round0_done, ri);
+  run_cc<PRED_NONE, true>(g, comp, fe, prop, pd, sc, 0, st, round0_done, ri, round0_done ? jlist : nullptr);
 }
 
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,

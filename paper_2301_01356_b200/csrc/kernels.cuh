@@ -109,7 +109,8 @@ void masked_cc(const Graph& g, const uint8_t* mask, int* comp, int2* fe, unsigne
                cudaStream_t st);
 // (warc: [3][n] targets of each row's arcs 0-2 recorded by k_chunk_rows, or nullptr)
 void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop, Scalars* sc, cudaStream_t st,
-                   bool round0_done = false, RootInit ri = RootInit{}, const int* warc = nullptr);
+                   bool round0_done = false, RootInit ri = RootInit{}, const int* warc = nullptr,
+                   int* jlist = nullptr);  // (jlist: >= 2^18 ints of scratch for k_jump_local's exit list)
 // Stage 1 over a streamed edge array (fbcc_run_host): identity init, one link
 // pass per arrived chunk range [q0, q1) of kItems-arc chunks, final compress
 void stage1_stream_begin(const Graph& g, int* comp, cudaStream_t st);
