@@ -420,12 +420,6 @@ __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __rest
 // without reaching a root the thread switches to L2 reads with stores
 // (doubling), for the deep chains of path-like graphs.
 constexpr int kL1Steps = 8;
-#ifndef FBCC_JUMP_EARLY_STORE
-#define FBCC_JUMP_EARLY_STORE 0
-#endif
-#ifndef FBCC_JUMP_BLOCK
-#define FBCC_JUMP_BLOCK 256
-#endif
 
 __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable);
 
@@ -441,89 +435,142 @@ __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable)
 // the next round's proposals then verify their target is still a root
 // (accept below), k_link_rows' giant test looks two levels up and falls back
 // to linking, and the final compress (no kAccept) makes the labels flat.
+// Each thread owns kCPer vertices per step (base + i * blockDim + t: coalesced),
+// so kCPer loads, then kCPer independent climbs, are in flight together -- at
+// one vertex per thread the kernel waited on its single load, then on its
+// single gather (config 5: 62 % of the stall samples on those two lines).
+#ifndef FBCC_CPER
+#define FBCC_CPER 4
+#endif
+constexpr int kCPer = FBCC_CPER;
+// resident blocks per SM the register budget is set for; the grid is exactly
+// that many (k_compress wants every block resident: a thread climbing through
+// the range of a block not yet scheduled walks its raw chains)
+#ifndef FBCC_CBLOCKS
+#define FBCC_CBLOCKS 8  // (4 vertices per thread fit 32 registers; 4 blocks at 64 registers measured slower)
+#endif
+constexpr int kCBlocks = FBCC_CBLOCKS;
+
 template <bool kJump, bool kAccept = false, bool kRecord = false>
-__global__ void k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable, RootInit ri,
-                           const int* hooks, int round, int rbase, unsigned long long* prop = nullptr,
-                           int* hooks_out = nullptr, int2* fe = nullptr, const int64_t* __restrict__ off = nullptr,
-                           const uint32_t* __restrict__ adj = nullptr, const int* __restrict__ warc = nullptr) {
+__global__ void __launch_bounds__(256, kCBlocks) k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable,
+                                                  RootInit ri, const int* hooks, int round, int rbase,
+                                                  unsigned long long* prop = nullptr, int* hooks_out = nullptr,
+                                                  int2* fe = nullptr, const int64_t* __restrict__ off = nullptr,
+                                                  const uint32_t* __restrict__ adj = nullptr,
+                                                  const int* __restrict__ warc = nullptr) {
   pdl_enter();
   int roots = 0;
   int hooked = 0;
   const int n_work = (hooks && skip_round(hooks, round, rbase, n)) ? 0 : n;
   const int64_t* hoff = (ri.flags && ri.off && ri.sc->has_hubs) ? ri.off : nullptr;
   if (ri.flags && blockIdx.x == 0 && threadIdx.x == 0) ri.flags[n] = 0;
-  __shared__ int sp[kJump ? 1024 : 1];
-  // block-uniform trip count (kJump): each step the block owns blockDim.x
+  __shared__ int sp[kJump ? 256 * kCPer : 1];
+  const int t = threadIdx.x;
+  const int tile = (int)blockDim.x * kCPer;
+  // block-uniform trip count (kJump): each step the block owns `tile`
   // consecutive vertices and may first shorten their chains in shared memory
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_work; base += (int64_t)gridDim.x * blockDim.x) {
-    const int v = (int)base + threadIdx.x;
-    int c = v < n ? __ldcg(comp + v) : v;
-    if (kAccept && v < n) {
-      const unsigned long long key = prop[v];
-      if (key != ~0ull) {
-        prop[v] = ~0ull;  // ready for the next round
-        if (c == v) {     // still a root (a stale proposal is dropped)
-          c = (int)(key >> 32);
-          comp[v] = c;
+  for (int64_t base = (int64_t)blockIdx.x * tile; base < n_work; base += (int64_t)gridDim.x * tile) {
+    int v[kCPer], c[kCPer], mem[kCPer];
+    bool root[kCPer];
+#pragma unroll
+    for (int i = 0; i < kCPer; i++) {
+      v[i] = (int)base + i * (int)blockDim.x + t;
+      c[i] = v[i] < n ? __ldcg(comp + v[i]) : v[i];
+    }
+    if (kAccept) {
+      unsigned long long key[kCPer];
+#pragma unroll
+      for (int i = 0; i < kCPer; i++) key[i] = v[i] < n ? prop[v[i]] : ~0ull;
+#pragma unroll
+      for (int i = 0; i < kCPer; i++) {
+        if (key[i] == ~0ull) continue;
+        prop[v[i]] = ~0ull;  // ready for the next round
+        if (c[i] == v[i]) {  // still a root (a stale proposal is dropped)
+          c[i] = (int)(key[i] >> 32);
+          comp[v[i]] = c[i];
           hooked++;
           if (kRecord) {
-            const int u = (int)(key & 0xffffffffull);
-            fe[v] = make_int2(u, sampled_arc(off, adj, warc, n, round, u));
+            const int u = (int)(key[i] & 0xffffffffull);
+            fe[v[i]] = make_int2(u, sampled_arc(off, adj, warc, n, round, u));
           }
         }
       }
     }
-    const bool root = c == v;
-    int mem = c;  // what comp[v] holds now
+#pragma unroll
+    for (int i = 0; i < kCPer; i++) {
+      root[i] = c[i] == v[i];
+      mem[i] = c[i];  // what comp[v] holds now
+    }
     if (kJump) {
       // Pointer jumping inside the block's id range (after sampling round 0
       // only): chains of consecutive ids -- round 0's left-neighbour hooks on
       // meshes, a path's v -> v-1 -- then leave the block in one step instead
-      // of up to blockDim global climbs (config 4a: 10^4-vertex row chains,
+      // of up to `tile` global climbs (config 4a: 10^4-vertex row chains,
       // S1 5.6 -> 3.9 ms).  A block with no in-range pointer pays one
       // barrier.  Every value is an ancestor, so the climb below stays exact.
-      sp[threadIdx.x] = c;
-      int rel = c - (int)base;
-      if (__syncthreads_or(!root && rel >= 0 && rel < (int)blockDim.x)) {
-        for (int r = 0; r < 10; r++) {
-          const int nc = (rel >= 0 && rel < (int)blockDim.x) ? sp[rel] : c;
-          const bool moved = nc != c;
+      bool in = false;
+#pragma unroll
+      for (int i = 0; i < kCPer; i++) {
+        sp[i * blockDim.x + t] = c[i];
+        in |= !root[i] && (unsigned)(c[i] - (int)base) < (unsigned)tile;
+      }
+      if (__syncthreads_or(in)) {
+        for (int r = 0; r < 12; r++) {
+          int nc[kCPer];
+          bool moved = false;
+#pragma unroll
+          for (int i = 0; i < kCPer; i++) {
+            const unsigned rel = (unsigned)(c[i] - (int)base);
+            nc[i] = rel < (unsigned)tile ? sp[rel] : c[i];
+            moved |= nc[i] != c[i];
+          }
           __syncthreads();
-          sp[threadIdx.x] = nc;
-          c = nc;
-          rel = c - (int)base;
+#pragma unroll
+          for (int i = 0; i < kCPer; i++) {
+            sp[i * blockDim.x + t] = nc[i];
+            c[i] = nc[i];
+          }
           if (!__syncthreads_or(moved)) break;
         }
       }
       __syncthreads();  // sp is rewritten next step
-#if FBCC_JUMP_EARLY_STORE
-      // publish the in-block result before the global climb: a neighbouring
-      // block's climb through this block then takes one hop, not the raw chain
-      if (v < n && c != mem) {
-        __stcg(comp + v, c);
-        mem = c;
+    }
+    bool done[kCPer];
+#pragma unroll
+    for (int i = 0; i < kCPer; i++) {
+      done[i] = root[i] || v[i] >= n;
+      if (v[i] < n) {
+        roots += root[i];
+        if (ri.flags) root_init(ri, hoff, v[i], root[i]);
       }
-#endif
     }
-    if (v >= n) continue;
-    roots += root;
-    if (ri.flags) root_init(ri, hoff, v, root);
-    if (root) continue;
-    bool done = false;
-    for (int i = 0; i < kL1Steps; i++) {
-      int x = __ldca(comp + c);
-      if (x == c) { done = true; break; }
-      c = x;
+    // (fully unrolled: as a rolled loop -- the warp reconverging at every
+    // step -- this climb ran 5x slower on config 4b's deep hook chains)
+#pragma unroll
+    for (int s = 0; s < kL1Steps; s++) {
+      int x[kCPer];
+      bool all = true;
+#pragma unroll
+      for (int i = 0; i < kCPer; i++) x[i] = done[i] ? c[i] : __ldca(comp + c[i]);
+#pragma unroll
+      for (int i = 0; i < kCPer; i++) {
+        if (x[i] == c[i]) done[i] = true;
+        else c[i] = x[i];
+        all &= done[i];
+      }
+      if (all) break;
     }
-    bool stored = false;
-    while (!done) {
-      if (__ldca(comp + c) == c) break;  // root (stable during compress)
-      int cc = __ldcg(comp + c);           // c's current pointer
-      __stcg(comp + v, cc);
-      stored = true;
-      c = cc;
+#pragma unroll
+    for (int i = 0; i < kCPer; i++) {
+      while (!done[i]) {
+        if (__ldca(comp + c[i]) == c[i]) break;  // root (stable during compress)
+        const int cc = __ldcg(comp + c[i]);      // c's current pointer
+        __stcg(comp + v[i], cc);
+        mem[i] = cc;
+        c[i] = cc;
+      }
+      if (c[i] != mem[i]) __stcg(comp + v[i], c[i]);  // (already-flat entries are not rewritten)
     }
-    if (stored || c != mem) __stcg(comp + v, c);  // (already-flat entries are not rewritten)
   }
   if (nroots) block_count_add(nroots, roots);
   if (kAccept) block_count_add(hooks_out, hooked);
@@ -909,7 +956,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   // k_compress relies on concurrent threads advancing each other's pointers:
   // its grid must be fully resident (2048 threads/SM), or grid-stride
   // threads chase pointers owned by blocks that cannot be scheduled yet
-  const int gres = grid_for(g.n, B, 2048 / B);
+  const int gres = grid_for((g.n + kCPer - 1) / kCPer, B, kCBlocks);
   int* nroots = sc->nroots + slot;  // device addresses (sc is a device pointer)
   int* hooks = sc->hooks + slot;
   // compress after round 0 (flattens the deep min-neighbour forest) and after
@@ -962,8 +1009,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
                  slot ? 1 : 0, (const int*)jlist);
           note(K_JUMP_LIST);
         }
-        const int JB = r == 0 ? FBCC_JUMP_BLOCK : B;
-        launch(r == 0 ? k_compress<true> : k_compress<false>, r == 0 ? grid_for(g.n, JB, 2048 / JB) : gres, JB, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
+        launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
                last_round ? sc : nullptr, opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase,
                (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
                (const uint32_t*)nullptr, (const int*)nullptr);
@@ -1048,7 +1094,7 @@ void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2
 
 void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st, RootInit ri) {
   const int B = 256;
-  launch(k_compress<true>, grid_for(g.n, B, 2048 / B), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
+  launch(k_compress<true>, grid_for((g.n + kCPer - 1) / kCPer, B, kCBlocks), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
          (const int*)nullptr, 0, 0, (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr,
          (const int64_t*)nullptr, (const uint32_t*)nullptr, (const int*)nullptr);
   note(K_COMPRESS);

@@ -7,6 +7,6 @@ for c in $cfgs; do
   for v in $vars; do
     echo "### config $c variant $v"
     if [ "$v" = base ]; then unset FBCC_LIB; else export FBCC_LIB=$PWD/paper_2301_01356_b200/_variants/$v.so; fi
-    python tools/tune.py --config $c "$@" 2>&1 | grep -v "^   " | tail -4
+    python tools/tune.py --config $c "$@" 2>&1 | tail -7
   done
 done
