@@ -276,60 +276,29 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
 // kInPlace (level 0 of large tours): the successors sit in own[e].x (written
 // by k_link_tour) and are replaced by (segment, offset) as the walk passes --
 // every element is read and then written by its own walker only.
-// kWalkers independent walks per thread, stepped together: a walk is a chain
-// of dependent loads (one L2 / DRAM round trip per element), so one walker
-// per thread leaves the memory system idle between a thread's steps; with
-// kWalkers of them every thread keeps that many loads in flight.
-#ifndef FBCC_WALKERS
-#define FBCC_WALKERS 2
-#endif
-constexpr int kWalkers = FBCC_WALKERS;
-
 template <bool kWeighted, bool kInPlace = false>
 __global__ void __launch_bounds__(256) k_walk(int K, int sh, int N, const int* __restrict__ succ,
                                               const int* __restrict__ w, int2* __restrict__ own,
                                               int* __restrict__ succ_next, int* __restrict__ w_next, int sh_next) {
   pdl_enter();
-  const int Kq = (K + kWalkers - 1) / kWalkers;  // walker i of a thread: j + i * Kq
-  for (int j0 = blockIdx.x * blockDim.x + threadIdx.x; j0 < Kq; j0 += gridDim.x * blockDim.x) {
-    int j[kWalkers], e[kWalkers], acc[kWalkers], s[kWalkers], wt[kWalkers];
-    bool act[kWalkers];
-#pragma unroll
-    for (int i = 0; i < kWalkers; i++) {
-      j[i] = j0 + i * Kq;
-      act[i] = j[i] < K;
-      e[i] = act[i] ? split_elem(j[i], sh, N) : 0;
-      acc[i] = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K; j += gridDim.x * blockDim.x) {
+    int e = split_elem(j, sh, N);
+    int acc = 0;
+    int s;
+    while (true) {
+      // (read-only path: an element is read strictly before its one write)
+      s = kInPlace ? __ldg(reinterpret_cast<const int*>(own) + 2 * (int64_t)e) : __ldg(succ + e);
+      // in place: the store must not reach L2 while the same sector's fill is
+      // still pending (store-behind-miss on one sector ran ~9x slower), so
+      // the stored value is made to depend on the loaded one (s == INT_MIN
+      // never occurs: successors are >= -1 or flagged ~e with e >= 1)
+      own[e] = make_int2(kInPlace ? (s == (int)0x80000000 ? -1 : j) : j, acc);
+      acc += kWeighted ? __ldg(w + e) : 1;
+      if (s < 0) break;
+      e = s;
     }
-    bool any = true;
-    while (any) {
-      any = false;
-#pragma unroll
-      for (int i = 0; i < kWalkers; i++) {
-        if (!act[i]) continue;
-        // (read-only path: an element is read strictly before its one write)
-        s[i] = kInPlace ? __ldg(reinterpret_cast<const int*>(own) + 2 * (int64_t)e[i]) : __ldg(succ + e[i]);
-        wt[i] = kWeighted ? __ldg(w + e[i]) : 1;
-      }
-#pragma unroll
-      for (int i = 0; i < kWalkers; i++) {
-        if (!act[i]) continue;
-        // in place: the store must not reach L2 while the same sector's fill is
-        // still pending (store-behind-miss on one sector ran ~9x slower), so
-        // the stored value is made to depend on the loaded one (s == INT_MIN
-        // never occurs: successors are >= -1 or flagged ~e with e >= 1)
-        own[e[i]] = make_int2(kInPlace ? (s[i] == (int)0x80000000 ? -1 : j[i]) : j[i], acc[i]);
-        acc[i] += wt[i];
-        if (s[i] < 0) {
-          act[i] = false;
-          succ_next[j[i]] = (s[i] == -1) ? -1 : flag_succ((~s[i]) >> sh, sh_next, K);
-          w_next[j[i]] = acc[i];
-        } else {
-          e[i] = s[i];
-          any = true;
-        }
-      }
-    }
+    succ_next[j] = (s == -1) ? -1 : flag_succ((~s) >> sh, sh_next, K);
+    w_next[j] = acc;
   }
 }
 
@@ -542,12 +511,12 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
                                              shift(R.S[0]));
   note(K_LINK_TOUR);
   // ruling-set levels
-  launch(inplace ? k_walk<false, true> : k_walk<false, false>, grid_for((R.K[1] + kWalkers - 1) / kWalkers, B, 64), B, 0, st, (int)R.K[1],
+  launch(inplace ? k_walk<false, true> : k_walk<false, false>, grid_for(R.K[1], B, 64), B, 0, st, (int)R.K[1],
          shift(R.S[0]), N0, (const int*)R.nxt, (const int*)nullptr, R.own0,
                                                        R.succ[1], R.wgt[1], sh_after(1));
   note(K_WALK0);
   for (int l = 1; l < R.nlev; l++) {
-    launch(k_walk<true>, grid_for((R.K[l + 1] + kWalkers - 1) / kWalkers, B, 64), B, 0, st, (int)R.K[l + 1], shift(R.S[l]), (int)R.K[l], R.succ[l],
+    launch(k_walk<true>, grid_for(R.K[l + 1], B, 64), B, 0, st, (int)R.K[l + 1], shift(R.S[l]), (int)R.K[l], R.succ[l],
                                                             R.wgt[l], R.own[l], R.succ[l + 1], R.wgt[l + 1],
                                                             sh_after(l + 1));
     note(K_WALKL);
