@@ -320,6 +320,17 @@ __device__ __forceinline__ bool skip_round(const int* hooks, int round, int rbas
   return round > 2 && (int64_t)h1 * 20 < (int64_t)hooks[round - 2];
 }
 
+// Sets left at the start of sampling round `round` (>= 1): the roots counted
+// by round 0's compress minus the later hooks.  One set left (a connected
+// graph that round 0 already joined: the tori, the chain) means no arc can
+// join anything any more -- the remaining rounds and the link pass return at
+// once (4a / 4c: propose + folded compress + link_rows, 0.54 ms of Stage 1).
+__device__ __forceinline__ int64_t sets_left(const int* nroots, const int* hooks, int round) {
+  int64_t R = nroots[0];
+  for (int i = 1; i < round; i++) R -= hooks[i];
+  return R;
+}
+
 template <int kPred>
 __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round,
                           int* comp, unsigned long long* prop, PredData pd, const int* __restrict__ nroots,
@@ -330,8 +341,8 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
   // roots at round start = roots counted after round 0 minus later hooks
   uint32_t thr = 1u << 24;
   if (round > 0) {
-    int64_t R = nroots[0];
-    for (int i = 1; i < round; i++) R -= hooks[i];
+    const int64_t R = sets_left(nroots, hooks, round);
+    if (R <= 1) return;
     uint64_t t = ((uint64_t)kPerRoot * (uint64_t)(R > 0 ? R : 0) << 24) / (uint64_t)n;
     if (t < thr) thr = (uint32_t)t;
   }
@@ -382,9 +393,10 @@ __device__ __forceinline__ int sampled_arc(const int64_t* __restrict__ off, cons
 
 template <bool kRecord>
 __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
-                         unsigned long long* prop, int2* fe, int* hooks, int rbase, const int* __restrict__ warc) {
+                         unsigned long long* prop, int2* fe, int* hooks, int rbase, const int* __restrict__ warc,
+                         const int* __restrict__ nroots) {
   pdl_enter();
-  if (skip_round(hooks, round, rbase, n)) return;
+  if (skip_round(hooks, round, rbase, n) || sets_left(nroots, hooks, round) <= 1) return;
   int hooked = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     unsigned long long key = prop[v];
@@ -457,11 +469,16 @@ __global__ void __launch_bounds__(256, kCBlocks) k_compress(int* comp, int n, in
                                                   unsigned long long* prop = nullptr, int* hooks_out = nullptr,
                                                   int2* fe = nullptr, const int64_t* __restrict__ off = nullptr,
                                                   const uint32_t* __restrict__ adj = nullptr,
-                                                  const int* __restrict__ warc = nullptr) {
+                                                  const int* __restrict__ warc = nullptr,
+                                                  const int* __restrict__ roots0 = nullptr,
+                                                  const int* __restrict__ hooks0 = nullptr) {
   pdl_enter();
   int roots = 0;
   int hooked = 0;
-  const int n_work = (hooks && skip_round(hooks, round, rbase, n)) ? 0 : n;
+  // (roots0: the compress after sampling round `round` >= 1 -- nothing was
+  // proposed when a single set was left, see sets_left)
+  const int n_work = ((hooks && skip_round(hooks, round, rbase, n)) ||
+                      (roots0 && sets_left(roots0, hooks0, round) <= 1)) ? 0 : n;
   const int64_t* hoff = (ri.flags && ri.off && ri.sc->has_hubs) ? ri.off : nullptr;
   if (ri.flags && blockIdx.x == 0 && threadIdx.x == 0) ri.flags[n] = 0;
   __shared__ int sp[kJump ? 256 * kCPer : 1];
@@ -670,8 +687,10 @@ constexpr int kLinkBatch = FBCC_LR_BATCH;
 template <int kPred, bool kRecord>
 __global__ void __launch_bounds__(256, FBCC_LR_MINB) k_link_rows(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                    int n, int* comp, int2* fe, PredData pd, const Scalars* sc,
-                                                   LongRows heavy) {
+                                                   LongRows heavy, const int* __restrict__ nroots,
+                                                   const int* __restrict__ hooks, int rounds) {
   pdl_enter();
+  if (rounds > 0 && sets_left(nroots, hooks, rounds) <= 1) return;  // one set: nothing left to join
   const int giant = sc->giant;
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -964,6 +983,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   // between only hook roots under roots and their proposers find() instead
   int cmask = opt(OPT_COMPRESS_MASK);
   if (cmask == 0) cmask = 1 | (kRounds > 0 ? 1 << (kRounds - 1) : 0);
+  cmask |= 1;  // bit 0 always honoured: round 0's compress counts the roots the later rounds start from
   if (kRounds > 0 && round0_done) {
     // (k_chunk_rows)
   } else if (kRounds > 0) {
@@ -988,7 +1008,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
              ((opt(OPT_SKEL_PARENT) >> r) & 1) != 0, kBase);
       note(K_PROPOSE);
       if (!fold) {
-        launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase, pd.warc);
+        launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase, pd.warc,
+               (const int*)nroots);
         note(K_ACCEPT);
       }
     }
@@ -999,7 +1020,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       if (fold) {
         launch(k_compress<false, true, kRecord>, gres, B, 0, st, comp, g.n, (int*)nullptr, last_round ? sc : nullptr,
                opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase, prop, hooks + r, fe, g.off, g.adj,
-               pd.warc);
+               pd.warc, (const int*)nroots, (const int*)hooks);
       } else {
         if (r == 0 && jlist && g.n >= kJumpListMinN) {  // id-ordered chains (see k_jump_local)
           launch(k_jump_local, grid_for((g.n + kJumpTile - 1) / kJumpTile, 1, 8), 256, 0, st, comp, g.n, sc, slot ? 1 : 0,
@@ -1012,7 +1033,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
         launch(r == 0 ? k_compress<true> : k_compress<false>, gres, B, 0, st, comp, g.n, r == 0 ? nroots : nullptr,
                last_round ? sc : nullptr, opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase,
                (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
-               (const uint32_t*)nullptr, (const int*)nullptr);
+               (const uint32_t*)nullptr, (const int*)nullptr, r > 0 ? (const int*)nroots : (const int*)nullptr,
+               (const int*)hooks);
       }
       note(K_COMPRESS);
     }
@@ -1025,7 +1047,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     // the proposal words (2n ints) are dead after the last accept: reuse them
     // as the super-heavy row lists
     LongRows heavy{reinterpret_cast<int*>(prop), 2 * g.n, sc->nheavy + (slot ? 1 : 0), sc->nmega + (slot ? 1 : 0)};
-    launch(k_link_rows<kPred, kRecord>, grid_for(g.n, B, 32), B, 0, st, g.off, g.adj, g.n, comp, fe, pd, sc, heavy);
+    launch(k_link_rows<kPred, kRecord>, grid_for(g.n, B, 32), B, 0, st, g.off, g.adj, g.n, comp, fe, pd, sc, heavy,
+           (const int*)nroots, (const int*)hooks, ((cmask & 1) && kRounds > 0) ? kRounds : 0);
     note(K_LINK_ROWS);
     // always launched: whether a super-heavy row exists is a property of the
     // buffer contents, which a replayed plan must not bake in (an empty list
@@ -1036,7 +1059,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   }
   launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0, 0,
          (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
-         (const uint32_t*)nullptr, (const int*)nullptr);  // final root count (= components)
+         (const uint32_t*)nullptr, (const int*)nullptr, (const int*)nullptr,
+         (const int*)nullptr);  // final root count (= components)
   note(K_COMPRESS);
 }
 
@@ -1096,7 +1120,8 @@ void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t s
   const int B = 256;
   launch(k_compress<true>, grid_for((g.n + kCPer - 1) / kCPer, B, kCBlocks), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
          (const int*)nullptr, 0, 0, (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr,
-         (const int64_t*)nullptr, (const uint32_t*)nullptr, (const int*)nullptr);
+         (const int64_t*)nullptr, (const uint32_t*)nullptr, (const int*)nullptr, (const int*)nullptr,
+         (const int*)nullptr);
   note(K_COMPRESS);
 }
 
