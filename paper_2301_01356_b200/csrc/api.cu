@@ -20,7 +20,7 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "root_flags", "scan", "root_list", "out_lists", "link_tour", "walk0", "walk_level", "final_rank", "expand", "rank0",
     "positions", "firsts", "w_gather", "tile", "table", "fence", "heads", "count_blocks", "ap", "set_edges",
     "edge_blocks", "edge_final", "memset", "export", "widen", "giant_min", "edge_fill", "edge_search", "jump_local",
-    "jump_list"};
+    "jump_list", "scan_tiles"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -49,12 +49,15 @@ Options options_snapshot() {
   return o;
 }
 
+#ifndef FBCC_ROOT_SCAN_FUSED
+#define FBCC_ROOT_SCAN_FUSED 1
+#endif
 constexpr int kFinalMaxHost = kFinalMax;
 constexpr int kMaxStreamChunks = 64;
 
 struct Layout {
   size_t total = 0;
-  size_t sc, crow, comp, fe, prop, flags, rootidx, rlist, lhead, hsub, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
+  size_t sc, sdesc, sdesc_bytes, crow, comp, fe, prop, flags, rootidx, rlist, lhead, hsub, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
       nlow, bmin, w0, cub;
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
@@ -89,6 +92,9 @@ struct Layout {
     if (scan_upper_temp_bytes((int)n) > cub_bytes) cub_bytes = scan_upper_temp_bytes((int)n);
 
     sc = take(sizeof(Scalars));
+    // root counts of the final compress's 256 x 4-vertex tiles (RootInit::sdesc)
+    sdesc_bytes = 8 * ((size_t)n / 1024 + 2);
+    sdesc = take(sdesc_bytes);
     crow = take(4 * ((m + kItems - 1) / kItems + 1));
     comp = take(4 * n);
     fe = take(8 * n);
@@ -183,6 +189,7 @@ struct Pipeline {
     R.nlow = (int*)at(lay.nlow);
     R.cub_tmp = at(lay.cub);
     R.cub_bytes = lay.cub_bytes;
+    R.tile_roots = FBCC_ROOT_SCAN_FUSED ? (unsigned long long*)at(lay.sdesc) : nullptr;  // (root_init_args: the final compress of Stage 1 ranks the roots)
     T.AP = (int4*)at(lay.AP);
     T.lh1 = (int2*)at(lay.lh1);
     T.lh2 = (int2*)at(lay.lh2);
@@ -234,6 +241,9 @@ struct Pipeline {
     ri.off = R.hoff;
     ri.sc = sc;
     ri.detach = opts.v[OPT_DETACH] != 0;
+    if (!FBCC_ROOT_SCAN_FUSED) return ri;
+    ri.rootidx = R.rootidx;
+    ri.sdesc = (unsigned long long*)((char*)sc + (lay.sdesc - lay.sc));
     return ri;
   }
 

@@ -46,7 +46,7 @@ enum KernelKind : int {  // one kind per kernel function (names: api.cu kKernelN
   K_ROOT_FLAGS, K_SCAN, K_ROOT_LIST, K_OUT_LISTS, K_LINK_TOUR, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_RANK0,
   K_POSITIONS, K_FIRSTS, K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_COUNT_BLOCKS, K_AP, K_SET_EDGES,
   K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_WIDEN, K_GIANT_MIN, K_EDGE_FILL, K_EDGE_SEARCH, K_JUMP_LOCAL,
-  K_JUMP_LIST, K_NUM_KINDS
+  K_JUMP_LIST, K_SCAN_TILES, K_NUM_KINDS
 };
 
 struct LaunchLog {

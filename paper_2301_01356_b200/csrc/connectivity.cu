@@ -447,6 +447,17 @@ __device__ void giant_of_block(const int* comp, int n, Scalars* sc, bool enable)
 // the next round's proposals then verify their target is still a root
 // (accept below), k_link_rows' giant test looks two levels up and falls back
 // to linking, and the final compress (no kAccept) makes the labels flat.
+// ---------------------------------------------------------------------------
+// Root ranks inside the final compress (kScan): the exclusive scan of the
+// root codes (Rooting::rootidx: roots on the tour list before v in the low
+// word, detached roots in the high word) in two levels.  The compress writes
+// each root's rank inside its 1024-vertex tile and the tile's root counts;
+// k_scan_tiles (rooting.cu, one CTA) turns the tile counts into prefixes and
+// k_out_lists adds them in as it places the roots.  No waiting between
+// blocks: a single-pass scan with decoupled look-back inside this kernel,
+// whose blocks run in lockstep waves, spent ~17 us per wave walking back
+// through the wave's aggregates (4a: final compress 0.23 -> 2.03 ms).
+// ---------------------------------------------------------------------------
 // Each thread owns kCPer vertices per step (base + i * blockDim + t: coalesced),
 // so kCPer loads, then kCPer independent climbs, are in flight together -- at
 // one vertex per thread the kernel waited on its single load, then on its
@@ -463,8 +474,13 @@ constexpr int kCPer = FBCC_CPER;
 #endif
 constexpr int kCBlocks = FBCC_CBLOCKS;
 
-template <bool kJump, bool kAccept = false, bool kRecord = false>
-__global__ void __launch_bounds__(256, kCBlocks) k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable,
+static_assert(kCPer == 4, "the fused root scan assumes 256 x 4-vertex tiles (api.cu sizes its descriptors for them)");
+#ifndef FBCC_CBLOCKS_SCAN
+#define FBCC_CBLOCKS_SCAN 6
+#endif
+constexpr int kCBlocksScan = FBCC_CBLOCKS_SCAN;  // (the scan variants: 40 registers instead of spilling at 32)
+template <bool kJump, bool kAccept = false, bool kRecord = false, bool kScan = false>
+__global__ void __launch_bounds__(256, kScan ? kCBlocksScan : kCBlocks) k_compress(int* comp, int n, int* nroots, Scalars* giant_sc, bool giant_enable,
                                                   RootInit ri, const int* hooks, int round, int rbase,
                                                   unsigned long long* prop = nullptr, int* hooks_out = nullptr,
                                                   int2* fe = nullptr, const int64_t* __restrict__ off = nullptr,
@@ -486,6 +502,8 @@ __global__ void __launch_bounds__(256, kCBlocks) k_compress(int* comp, int n, in
   const int tile = (int)blockDim.x * kCPer;
   // block-uniform trip count (kJump): each step the block owns `tile`
   // consecutive vertices and may first shorten their chains in shared memory
+  __shared__ unsigned s_wc[kScan ? 64 : 1];  // per (i, warp) root counts: detached << 16 | listed (two tiles' worth)
+  int wbuf = 0;
   for (int64_t base = (int64_t)blockIdx.x * tile; base < n_work; base += (int64_t)gridDim.x * tile) {
     int v[kCPer], c[kCPer], mem[kCPer];
     bool root[kCPer];
@@ -553,12 +571,20 @@ __global__ void __launch_bounds__(256, kCBlocks) k_compress(int* comp, int n, in
       __syncthreads();  // sp is rewritten next step
     }
     bool done[kCPer];
+    unsigned pre[kCPer];  // kScan: root code << 30 | roots before this vertex in its warp (detached << 16 | listed)
 #pragma unroll
     for (int i = 0; i < kCPer; i++) {
       done[i] = root[i] || v[i] >= n;
+      int code = 0;
       if (v[i] < n) {
         roots += root[i];
-        if (ri.flags) root_init(ri, hoff, v[i], root[i]);
+        if (ri.flags) code = root_init(ri, hoff, v[i], root[i]);
+      }
+      if (kScan) {
+        const unsigned b1 = __ballot_sync(0xffffffffu, code == 1), b2 = __ballot_sync(0xffffffffu, code == 2);
+        const unsigned lt = (1u << (t & 31)) - 1;
+        pre[i] = ((unsigned)code << 30) | (__popc(b2 & lt) << 16) | __popc(b1 & lt);
+        if ((t & 31) == 0) s_wc[32 * wbuf + i * 8 + (t >> 5)] = (__popc(b2) << 16) | __popc(b1);
       }
     }
     // (fully unrolled: as a rolled loop -- the warp reconverging at every
@@ -587,6 +613,30 @@ __global__ void __launch_bounds__(256, kCBlocks) k_compress(int* comp, int n, in
         c[i] = cc;
       }
       if (c[i] != mem[i]) __stcg(comp + v[i], c[i]);  // (already-flat entries are not rewritten)
+    }
+    if (kScan) {
+      // one barrier per tile, after the climb (mid-tile it held every warp's
+      // climb behind the slowest warp's loads): every warp then scans the 32
+      // (i, warp) counts itself (vertex order); the count buffer alternates
+      // between tiles
+      __syncthreads();
+      const unsigned* wc = s_wc + 32 * wbuf;
+      const unsigned x = wc[t & 31];
+      unsigned incl = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((t & 31) >= o) incl += y;
+      }
+      if (t == 31) ri.sdesc[base / tile] = ((unsigned long long)(incl >> 16) << 32) | (incl & 0xffffu);  // tile counts
+      const unsigned excl = incl - x;
+#pragma unroll
+      for (int i = 0; i < kCPer; i++) {
+        const unsigned e = __shfl_sync(0xffffffffu, excl, i * 8 + (t >> 5));
+        if ((pre[i] >> 30) == 0) continue;  // only the roots' ranks are ever read
+        const unsigned w = e + (pre[i] & 0x3fffffffu);
+        ri.rootidx[v[i]] = ((unsigned long long)(w >> 16) << 32) | (w & 0xffffu);  // rank inside the tile
+      }
+      wbuf ^= 1;
     }
   }
   if (nroots) block_count_add(nroots, roots);
@@ -1057,7 +1107,9 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
            pd, heavy);
     note(K_LINK_HEAVY);
   }
-  launch(k_compress<false>, gres, B, 0, st, comp, g.n, nroots + 7, nullptr, false, ri, (const int*)nullptr, 0, 0,
+  launch(ri.rootidx ? k_compress<false, false, false, true> : k_compress<false>,
+         ri.rootidx ? grid_for((g.n + kCPer - 1) / kCPer, B, kCBlocksScan) : gres, B, 0, st, comp, g.n, nroots + 7,
+         nullptr, false, ri, (const int*)nullptr, 0, 0,
          (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
          (const uint32_t*)nullptr, (const int*)nullptr, (const int*)nullptr,
          (const int*)nullptr);  // final root count (= components)
@@ -1118,7 +1170,9 @@ void stage1_stream_range(const Graph& g, int64_t q0, int64_t q1, int* comp, int2
 
 void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t st, RootInit ri) {
   const int B = 256;
-  launch(k_compress<true>, grid_for((g.n + kCPer - 1) / kCPer, B, kCBlocks), B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
+  launch(ri.rootidx ? k_compress<true, false, false, true> : k_compress<true>,
+         grid_for((g.n + kCPer - 1) / kCPer, B, ri.rootidx ? kCBlocksScan : kCBlocks),
+         B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
          (const int*)nullptr, 0, 0, (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr,
          (const int64_t*)nullptr, (const uint32_t*)nullptr, (const int*)nullptr, (const int*)nullptr,
          (const int*)nullptr);

@@ -35,13 +35,19 @@ struct RootInit {
   const int64_t* off = nullptr;  // hub split source (nullptr: none)
   const Scalars* sc = nullptr;
   bool detach = false;           // isolated vertices (but 0) stay off the Euler tour (code 2)
+  // the same compress also ranks the roots inside each of its 1024-vertex
+  // tiles (Rooting::rootidx at the roots) and counts each tile's roots
+  // (tile_roots); k_scan_tiles and k_out_lists finish the exclusive scan
+  unsigned long long* rootidx = nullptr;
+  unsigned long long* sdesc = nullptr;  // [ceil(n / 1024)] tile root counts: detached << 32 | listed
 };
 
 // Root codes (Rooting::flags): 0 non-root, 1 root on the tour list, 2 root
 // kept off the list -- an isolated vertex other than 0, whose positions
 // follow the list's (k_positions).  RMAT s25: 16.5 M of the 33.5 M vertices.
-__device__ __forceinline__ void root_init(const RootInit& ri, const int64_t* hoff, int v, bool root) {
-  ri.flags[v] = root ? ((ri.detach && v != 0 && __ldg(ri.off + v + 1) == __ldg(ri.off + v)) ? 2 : 1) : 0;
+__device__ __forceinline__ int root_init(const RootInit& ri, const int64_t* hoff, int v, bool root) {
+  const int code = root ? ((ri.detach && v != 0 && __ldg(ri.off + v + 1) == __ldg(ri.off + v)) ? 2 : 1) : 0;
+  ri.flags[v] = code;
   int h = -1;
   if (hoff) {
     const int64_t rs = __ldg(hoff + v);
@@ -53,6 +59,7 @@ __device__ __forceinline__ void root_init(const RootInit& ri, const int64_t* hof
     }
   }
   ri.lhead[v] = h;
+  return code;
 }
 
 // Device arrays for the rooting / tags stages (see api.cu for the layout).
@@ -64,6 +71,8 @@ constexpr int kFinalMax = FBCC_FINAL_MAX;  // list-ranking level finished in one
 struct Rooting {
   int* flags;      // [n+1] root code (root_init): 0 non-root, 1 listed root, 2 detached
   unsigned long long* rootidx;  // [n+1] exclusive scan: low 32 bits listed roots before v, high 32 detached ones
+  unsigned long long* tile_roots = nullptr;  // the pipeline: Stage 1's final compress ranked the roots inside its
+                                             // 1024-vertex tiles (RootInit::rootidx / sdesc); [tiles] root counts
   int* rlist;      // [n]   listed roots in id order
   int* lhead;      // [n]   first out-arc of each vertex (-1: none; <= -2: hub, see rooting.cu)
   int* hsub;       // [m/16 + 64] hub sub-list heads (nullptr: no hub split)

@@ -83,6 +83,16 @@ void scan_roots(const int* flags, unsigned long long* out, int64_t items, void* 
 __device__ __forceinline__ int lo32(unsigned long long x) { return (int)(uint32_t)x; }
 __device__ __forceinline__ int hi32(unsigned long long x) { return (int)(x >> 32); }
 
+// ranks of root x: rootidx[x], plus its tile's prefix when the scan was split
+// between Stage 1's final compress (ranks inside 1024-vertex tiles) and
+// k_scan_tiles (tile prefixes) -- the prefixes are n / 1024 words, L2-resident
+constexpr int kRootTile = 1024;  // vertices per compress tile (256 threads x 4)
+__device__ __forceinline__ unsigned long long root_rank(const unsigned long long* __restrict__ rootidx,
+                                                        const unsigned long long* __restrict__ tile_pre, int x) {
+  const unsigned long long r = __ldg(rootidx + x);
+  return tile_pre ? r + __ldg(tile_pre + x / kRootTile) : r;
+}
+
 // list / component counts from rootidx[n]
 __device__ __forceinline__ void publish_roots(const unsigned long long* rootidx, int n, Scalars* sc) {
   const unsigned long long t = rootidx[n];
@@ -162,6 +172,55 @@ __global__ void k_root_list(const int* __restrict__ comp, const unsigned long lo
     if (__ldg(comp + r) == r) rlist[lo32(__ldg(rootidx + r))] = r;
 }
 
+// Second level of the root scan fused into Stage 1's final compress (see
+// k_compress<kScan>): tile root counts -> exclusive prefixes, in place, by
+// one CTA (n / 1024 entries: 33 k on config 5, 98 k at n = 1e8); also the
+// totals (rootidx[n]) and the counts derived from them.
+__global__ void __launch_bounds__(1024) k_scan_tiles(unsigned long long* __restrict__ tiles, int ntiles,
+                                                     unsigned long long* __restrict__ rootidx, int n, Scalars* sc) {
+  pdl_enter();
+  __shared__ unsigned long long wtot[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  // each warp owns one contiguous segment (a multiple of 32 counts): lane
+  // sums, the 32 segment totals scanned by warp 0, then a shuffle scan per
+  // 32 counts along the segment -- two barriers in all, every access coalesced
+  const int seg = ((ntiles + 1023) / 1024) * 32;
+  const int lo = min(warp * seg, ntiles), hi = min(lo + seg, ntiles);
+  unsigned long long sum = 0;
+#pragma unroll 4
+  for (int i = lo + lane; i < hi; i += 32) sum += tiles[i];
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) wtot[warp] = sum;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long x = wtot[lane];
+    unsigned long long w = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    wtot[lane] = w - x;
+    if (lane == 31) {
+      rootidx[n] = w;
+      publish_roots(rootidx, n, sc);
+    }
+  }
+  __syncthreads();
+  unsigned long long run = wtot[warp];
+  unsigned long long nxt = lo + lane < hi ? tiles[lo + lane] : 0ull;
+  for (int i0 = lo; i0 < hi; i0 += 32) {
+    const unsigned long long x = nxt;
+    if (i0 + 32 < hi) nxt = i0 + 32 + lane < hi ? tiles[i0 + 32 + lane] : 0ull;  // (in flight under this step's scan)
+    unsigned long long incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (i0 + lane < hi) tiles[i0 + lane] = run + incl - x;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
 // out-arc lists: arc 2x = u->v is an out-arc of u, 2x+1 = v->u of v
 __device__ __forceinline__ int* list_head(int* lhead, int* hsub, int t, int x, bool split) {
   if (split) {
@@ -176,13 +235,13 @@ __device__ __forceinline__ int* list_head(int* lhead, int* hsub, int t, int x, b
 __global__ void k_out_lists(const int* __restrict__ comp, const int2* __restrict__ fe, int n, int* lhead,
                             int* __restrict__ nexto, int* hsub, Scalars* sc,
                             const unsigned long long* __restrict__ rootidx, const int* __restrict__ flags,
-                            int* __restrict__ rlist) {
+                            int* __restrict__ rlist, const unsigned long long* __restrict__ tile_pre) {
   pdl_enter();
   const bool split = hsub != nullptr && sc->has_hubs;
-  if (rootidx && blockIdx.x == 0 && threadIdx.x == 0) publish_roots(rootidx, n, sc);
+  if (rootidx && !tile_pre && blockIdx.x == 0 && threadIdx.x == 0) publish_roots(rootidx, n, sc);
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     if (__ldg(comp + x) == x) {
-      if (rootidx && __ldg(flags + x) == 1) rlist[lo32(__ldg(rootidx + x))] = x;
+      if (rootidx && __ldg(flags + x) == 1) rlist[lo32(root_rank(rootidx, tile_pre, x))] = x;
       continue;
     }
     int2 e = __ldg(fe + x);
@@ -232,7 +291,8 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
                             const int* __restrict__ lhead, const int* __restrict__ hsub, const int* __restrict__ nexto,
                             const unsigned long long* __restrict__ rootidx, const int* __restrict__ flags,
                             const int* __restrict__ rlist, int n,
-                            int* __restrict__ nxt, int2* __restrict__ own0, const Scalars* sc, int sh0) {
+                            int* __restrict__ nxt, int2* __restrict__ own0, const Scalars* sc, int sh0,
+                            const unsigned long long* __restrict__ tile_pre) {
   pdl_enter();
   const int c = sc->nlisted;
   const int64_t N = 2 * (int64_t)n;
@@ -247,7 +307,7 @@ __global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict
         if (h <= -2) h = hub_next(hsub, h, 0);
         out = h >= 0 ? h : (int)e + 1;
       } else {
-        int ri = lo32(__ldg(rootidx + x));
+        int ri = lo32(root_rank(rootidx, tile_pre, x));
         out = (ri + 1 < c) ? 2 * __ldg(rlist + ri + 1) : -1;
       }
     } else {  // arc e arrives at t; leave through the out-arc after e^1
@@ -431,12 +491,13 @@ __global__ void k_positions(const int* __restrict__ comp, const int2* __restrict
                             const int2* __restrict__ rank0, int n, int4* __restrict__ rec,
                             int4* __restrict__ AP, int* __restrict__ firsts, const int4* __restrict__ own0,
                             const int* __restrict__ offs1, const int* __restrict__ flags,
-                            const unsigned long long* __restrict__ rootidx, const Scalars* sc) {
+                            const unsigned long long* __restrict__ rootidx, const Scalars* sc,
+                            const unsigned long long* __restrict__ tile_pre) {
   pdl_enter();
   const int tour_len = sc->tour_len;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     if (__ldg(flags + x) == 2) {
-      const int f = tour_len + 2 * hi32(__ldg(rootidx + x));
+      const int f = tour_len + 2 * hi32(root_rank(rootidx, tile_pre, x));
       rec[x] = make_int4(f, f + 1, -1, 0);
       if (firsts) firsts[x] = f;
       continue;
@@ -476,18 +537,24 @@ void stage2_rooting(const Graph& g, const int* comp, const int2* fe, Rooting& R,
   // Euler circuit: out-arc lists in atomicExch order (any order is a valid
   // tour; the final outputs do not depend on it)
   launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto, R.hoff ? R.hsub : nullptr, sc,
-         (const unsigned long long*)nullptr, (const int*)nullptr, (int*)nullptr);
+         (const unsigned long long*)nullptr, (const int*)nullptr, (int*)nullptr, (const unsigned long long*)nullptr);
   note(K_OUT_LISTS);
   rooting_tour(g.n, comp, fe, R, AP, sc, st);
 }
 
 void stage2_rooting_fused(const Graph& g, const int* comp, const int2* fe, Rooting& R, int4* AP, Scalars* sc,
                           cudaStream_t st) {
-  // R.flags / R.lhead / R.hsub were written by Stage 1's final compress
-  scan_roots(R.flags, R.rootidx, g.n + 1, R.cub_tmp, R.cub_bytes, st);
-  note(K_SCAN);
+  // R.flags / R.lhead / R.hsub were written by Stage 1's final compress --
+  // and the roots' ranks, when the scan ran inside it
+  if (R.tile_roots) {
+    launch(k_scan_tiles, 1, 1024, 0, st, R.tile_roots, (g.n + kRootTile - 1) / kRootTile, R.rootidx, g.n, sc);
+    note(K_SCAN_TILES);
+  } else {
+    scan_roots(R.flags, R.rootidx, g.n + 1, R.cub_tmp, R.cub_bytes, st);
+    note(K_SCAN);
+  }
   launch(k_out_lists, grid_for(g.n, 256), 256, 0, st, comp, fe, g.n, R.lhead, R.nexto, R.hoff ? R.hsub : nullptr, sc,
-         (const unsigned long long*)R.rootidx, (const int*)R.flags, R.rlist);
+         (const unsigned long long*)R.rootidx, (const int*)R.flags, R.rlist, (const unsigned long long*)R.tile_roots);
   note(K_OUT_LISTS);
   rooting_tour(g.n, comp, fe, R, AP, sc, st);
 }
@@ -507,8 +574,7 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
   const bool inplace = (int64_t)N0 * 8 > (64ll << 20) || !R.nxt;
   launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.hsub, R.nexto,
          (const unsigned long long*)R.rootidx, (const int*)R.flags, R.rlist, n,
-         inplace ? (int*)nullptr : R.nxt, R.own0, sc,
-                                             shift(R.S[0]));
+         inplace ? (int*)nullptr : R.nxt, R.own0, sc, shift(R.S[0]), (const unsigned long long*)R.tile_roots);
   note(K_LINK_TOUR);
   // ruling-set levels
   launch(inplace ? k_walk<false, true> : k_walk<false, false>, grid_for(R.K[1], B, 64), B, 0, st, (int)R.K[1],
@@ -535,14 +601,14 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
   if (FBCC_FUSED_RANK0) {
     launch(k_positions, gv, B, 0, st, comp, fe, (const int2*)nullptr, n, R.rec, AP, R.firsts,
            reinterpret_cast<const int4*>(R.own0), (const int*)R.offs[1], (const int*)R.flags,
-           (const unsigned long long*)R.rootidx, (const Scalars*)sc);
+           (const unsigned long long*)R.rootidx, (const Scalars*)sc, (const unsigned long long*)R.tile_roots);
     note(K_POSITIONS);
   } else {
     launch(k_rank0, grid_for(N0, B), B, 0, st, N0, R.own0, R.offs[1], R.K[1], R.rank0);
     note(K_RANK0);
     launch(k_positions, gv, B, 0, st, comp, fe, reinterpret_cast<const int2*>(R.rank0), n, R.rec, AP, R.firsts,
            (const int4*)nullptr, (const int*)nullptr, (const int*)R.flags, (const unsigned long long*)R.rootidx,
-           (const Scalars*)sc);
+           (const Scalars*)sc, (const unsigned long long*)R.tile_roots);
     note(K_POSITIONS);
   }
 }
