@@ -352,8 +352,8 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
     int w;
     int64_t s = -1;
     int4 rv;
-    if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
     if (kPred == PRED_SKEL && skel_parent) {  // this round samples the plain parent edge
+      rv = __ldg(pd.rec + v);
       if (rv.z < 0 || rv.w != 0) continue;
       w = rv.z;
     } else {
@@ -374,7 +374,12 @@ __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __res
     // the predicate only for arcs that would join two sets: under the
     // skeleton predicate it gathers w's 16-byte record, and by the last
     // rounds most sampled arcs already lie inside one set
-    if (!(kPred == PRED_SKEL && skel_parent) && !keep<kPred>(pd, v, rv, w, s)) continue;
+    // (v's own record is loaded here too: rows with no sampled arc -- RMAT's
+    // isolated half -- and arcs inside one set never read it)
+    if (!(kPred == PRED_SKEL && skel_parent)) {
+      if (kPred == PRED_SKEL) rv = __ldg(pd.rec + v);
+      if (!keep<kPred>(pd, v, rv, w, s)) continue;
+    }
     int hi = ru > rw ? ru : rw;
     int lo = ru + rw - hi;
     // any proposal is a valid hook, so lanes aiming at the same root send one
