@@ -130,7 +130,22 @@ BIG = {
     "uniform_1p55m_d4": lambda: workloads.uniform(1_550_000, 4, seed=7),   # shared-memory bitmap, near its limit
     "uniform_1p8m_d4": lambda: workloads.uniform(1_800_000, 4, seed=8),    # global bitmap (giant ~all)
     "uniform_1p8m_d1": lambda: workloads.uniform(1_800_000, 1, seed=9),    # label gathers (no giant)
+    # n >= 2^22 with >= 3/4 of the vertices hooked to a near id in round 0: the id-ordered compress
+    # (k_jump_local / k_jump_list) -- a path, a torus (row chains + the column-0 chain), and paths of 4
+    # whose heads hang off far, random heads (more exit targets than the list holds: the fallback)
+    "chain_4p3m": lambda: workloads.chain(4_300_000),
+    "torus_2100": lambda: workloads.grid(2100, 2100, circular=True),
+    "paths4_far_heads_4p2m": lambda: _paths4_far_heads(1 << 20),
 }
+
+
+def _paths4_far_heads(k):
+    rng = np.random.default_rng(11)
+    i = np.arange(k, dtype=np.int64)
+    inner = np.concatenate([np.column_stack([4 * i + j, 4 * i + j + 1]) for j in range(3)])
+    parent = (rng.random(k - 1) * np.arange(1, k)).astype(np.int64)  # head c hangs off head parent[c - 1] < c
+    heads = np.column_stack([4 * np.arange(1, k, dtype=np.int64), 4 * parent])
+    return symmetrize(np.concatenate([inner, heads]), 4 * k)
 
 
 @pytest.mark.parametrize("name", sorted(BIG))
