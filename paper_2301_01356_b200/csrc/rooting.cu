@@ -287,49 +287,138 @@ __device__ __forceinline__ int flag_succ(int s, int sh, int N) {
 // the hash pick one as a splitter, its walker stops there and leaves a
 // detached element on the next level -- unreachable from the head, never
 // read back (k_positions places detached roots from rootidx).
-__global__ void k_link_tour(const int* __restrict__ comp, const int2* __restrict__ fe,
-                            const int* __restrict__ lhead, const int* __restrict__ hsub, const int* __restrict__ nexto,
-                            const unsigned long long* __restrict__ rootidx, const int* __restrict__ flags,
-                            const int* __restrict__ rlist, int n,
-                            int* __restrict__ nxt, int2* __restrict__ own0, const Scalars* sc, int sh0,
-                            const unsigned long long* __restrict__ tile_pre) {
+struct TourArgs {
+  const int* comp;
+  const int2* fe;
+  const int* lhead;
+  const int* hsub;
+  const int* nexto;
+  const unsigned long long* rootidx;
+  const unsigned long long* tile_pre;
+  const int* flags;
+  const int* rlist;
+};
+
+// successor of list element e (-1: end of the list); c = listed roots
+__device__ __forceinline__ int tour_succ(const TourArgs& a, int64_t e, int c) {
+  const int x = (int)(e >> 1);
+  if (__ldg(a.comp + x) == x) {  // enter(x) / exit(x)
+    if (__ldg(a.flags + x) == 2) return -1;
+    if ((e & 1) == 0) {
+      int h = __ldg(a.lhead + x);
+      if (h <= -2) h = hub_next(a.hsub, h, 0);
+      return h >= 0 ? h : (int)e + 1;
+    }
+    const int ri = lo32(root_rank(a.rootidx, a.tile_pre, x));
+    return (ri + 1 < c) ? 2 * __ldg(a.rlist + ri + 1) : -1;
+  }
+  // arc e arrives at t; leave through the out-arc after e^1
+  const int2 uv = __ldg(a.fe + x);
+  const int t = (e & 1) ? uv.x : uv.y;
+  int nx = __ldg(a.nexto + (e ^ 1));
+  if (nx >= 0) return nx;
+  // end of t's list (of a hub's sub-list: the next non-empty one)
+  const int h = __ldg(a.lhead + t);
+  if (h <= -2) nx = hub_next(a.hsub, h, (x & (hub_ways(h) - 1)) + 1);
+  if (nx >= 0) return nx;
+  if (__ldg(a.comp + t) == t) return 2 * t + 1;
+  return h <= -2 ? hub_next(a.hsub, h, 0) : h;
+}
+
+// (small tours: the successors go to their own array, k_walk<false, false> reads them)
+__global__ void k_link_tour(TourArgs a, int n, int* __restrict__ nxt, const Scalars* sc, int sh0) {
   pdl_enter();
   const int c = sc->nlisted;
   const int64_t N = 2 * (int64_t)n;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
-    int x = (int)(e >> 1);
-    int out;
-    if (__ldg(comp + x) == x) {  // enter(x) / exit(x)
-      if (__ldg(flags + x) == 2) {
-        out = -1;
-      } else if ((e & 1) == 0) {
-        int h = __ldg(lhead + x);
-        if (h <= -2) h = hub_next(hsub, h, 0);
-        out = h >= 0 ? h : (int)e + 1;
-      } else {
-        int ri = lo32(root_rank(rootidx, tile_pre, x));
-        out = (ri + 1 < c) ? 2 * __ldg(rlist + ri + 1) : -1;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x)
+    nxt[e] = flag_succ(tour_succ(a, e, c), sh0, (int)N);
+}
+
+// Large tours (level 0 in place): the successor goes into the element's
+// (segment, offset) slot, which the level-0 walker reads and then overwrites
+// (one sector per visited element instead of a successor sector plus a
+// partial write).  The kernel also ranks, in shared memory, every level-0
+// segment that lies inside one 2048-element tile: the tile's successors are
+// staged, each of its 128 splitters walks its segment there (~30 cycles a
+// step instead of an L2 round trip), and a segment that ends inside the tile
+// is written out finished -- (segment, offset) per element, weight and next
+// splitter per segment.  On id-ordered tours (meshes, paths: consecutive tour
+// elements are 16 bytes apart) that is nearly every segment, and k_walk's
+// level-0 pass -- one L2 read and one partial write per step, bound by the L2
+// operation rate (4c: 1.71 ms, lts 63 %) -- is left with the few segments
+// that cross a tile boundary.  A random tour (RMAT) completes none and pays
+// one shared-memory step per splitter.
+constexpr int kLinkTile = 2048;
+constexpr int kNotWalked = (int)0x80000000;  // succ_next[j]: segment j is k_walk's
+
+__global__ void __launch_bounds__(256) k_link_walk(TourArgs a, int n, int2* __restrict__ own0, const Scalars* sc,
+                                                   int sh0, int K1, int* __restrict__ succ_next,
+                                                   int* __restrict__ w_next, int sh_next) {
+  pdl_enter();
+  __shared__ int S[kLinkTile];     // successor of each tile element (flagged)
+  __shared__ int2 R[kLinkTile];    // finished (segment, offset); .x == kNotWalked: not finished
+  const int c = sc->nlisted;
+  const int N = 2 * n;
+  const int t = threadIdx.x;
+  // tile-local ranking only where it pays: Stage 1's round 0 hooked >= 3/4 of
+  // the vertices to a near id, so the forest -- and the tour -- follow the id order
+  const bool ordered = (int64_t)sc->near[0] * 4 >= (int64_t)n * 3;
+  constexpr int kPer = kLinkTile / 256;
+  if (!ordered) {  // a random tour: no segment stays inside a tile -- successors only, every segment is k_walk's
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + t, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = tid; e < N; e += stride) own0[e] = make_int2(flag_succ(tour_succ(a, e, c), sh0, N), 0);
+    for (int64_t j = tid; j < K1; j += stride) succ_next[j] = kNotWalked;
+    return;
+  }
+  for (int64_t base = (int64_t)blockIdx.x * kLinkTile; base < N; base += (int64_t)gridDim.x * kLinkTile) {
+#pragma unroll
+    for (int i = 0; i < kPer; i++) {
+      const int r = i * 256 + t;
+      const int64_t e = base + r;
+      S[r] = e < N ? flag_succ(tour_succ(a, e, c), sh0, N) : -1;
+      R[r].x = kNotWalked;
+    }
+    __syncthreads();
+    // one splitter per window of 1 << sh0 ids: window j's is split_elem(j)
+    const int wins = kLinkTile >> sh0;
+    for (int wi = t; wi < wins; wi += 256) {
+      const int j = (int)(base >> sh0) + wi;
+      if (j >= K1) break;
+      const int e0 = split_elem(j, sh0, N);
+      int e = e0, len = 0, s;
+      bool inside = true;
+      while (true) {  // walk the staged successors, ranking as it goes
+        const int r = e - (int)base;
+        s = S[r];
+        R[r] = make_int2(j, len++);
+        if (s < 0) break;
+        if (s < (int)base || s >= (int)base + kLinkTile) { inside = false; break; }
+        e = s;
       }
-    } else {  // arc e arrives at t; leave through the out-arc after e^1
-      int2 uv = __ldg(fe + x);
-      int t = (e & 1) ? uv.x : uv.y;
-      int nx = __ldg(nexto + (e ^ 1));
-      if (nx >= 0) {
-        out = nx;
-      } else {  // end of t's list (of a hub's sub-list: the next non-empty one)
-        const int h = __ldg(lhead + t);
-        if (h <= -2) nx = hub_next(hsub, h, (x & (hub_ways(h) - 1)) + 1);
-        if (nx >= 0) out = nx;
-        else if (__ldg(comp + t) == t) out = 2 * t + 1;
-        else out = h <= -2 ? hub_next(hsub, h, 0) : h;
+      if (!inside) {  // the segment leaves the tile: undo, k_walk ranks it
+        e = e0;
+        for (int off = 0; off < len; off++) {
+          const int r = e - (int)base;
+          R[r].x = kNotWalked;
+          e = S[r];
+        }
+        succ_next[j] = kNotWalked;
+        continue;
+      }
+      succ_next[j] = (s == -1) ? -1 : flag_succ((~s) >> sh0, sh_next, K1);
+      w_next[j] = len;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPer; i++) {
+      const int r = i * 256 + t;
+      const int64_t e = base + r;
+      if (e < N) {
+        const int2 v = R[r];
+        own0[e] = v.x == kNotWalked ? make_int2(S[r], 0) : v;
       }
     }
-    // in place (nxt == nullptr): the successor goes into the element's
-    // (segment, offset) slot, which the level-0 walker reads and then
-    // overwrites (one sector per visited element instead of a successor
-    // sector plus a partial write -- the win when the walk is DRAM-bound)
-    if (nxt) nxt[e] = flag_succ(out, sh0, (int)N);
-    else own0[e] = make_int2(flag_succ(out, sh0, (int)N), 0);
+    __syncthreads();  // S / R are rewritten by the next tile
   }
 }
 
@@ -342,6 +431,7 @@ __global__ void __launch_bounds__(256) k_walk(int K, int sh, int N, const int* _
                                               int* __restrict__ succ_next, int* __restrict__ w_next, int sh_next) {
   pdl_enter();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K; j += gridDim.x * blockDim.x) {
+    if (kInPlace && succ_next[j] != kNotWalked) continue;  // (k_link_walk finished the segment inside its tile)
     int e = split_elem(j, sh, N);
     int acc = 0;
     int s;
@@ -572,9 +662,13 @@ void rooting_tour(int n, const int* comp, const int2* fe, Rooting& R, int4* AP, 
   // walks gain (config 5 walk0 1.65 -> 0.92 ms), L2-resident ones lose
   // (config 2: the next element often shares the stored sector)
   const bool inplace = (int64_t)N0 * 8 > (64ll << 20) || !R.nxt;
-  launch(k_link_tour, grid_for(N0, B), B, 0, st, comp, fe, R.lhead, R.hsub, R.nexto,
-         (const unsigned long long*)R.rootidx, (const int*)R.flags, R.rlist, n,
-         inplace ? (int*)nullptr : R.nxt, R.own0, sc, shift(R.S[0]), (const unsigned long long*)R.tile_roots);
+  const TourArgs ta{comp, fe, R.lhead, R.hsub, R.nexto, R.rootidx, R.tile_roots, R.flags, R.rlist};
+  if (inplace) {
+    launch(k_link_walk, grid_for(N0, B), B, 0, st, ta, n, R.own0, (const Scalars*)sc,
+           shift(R.S[0]), (int)R.K[1], R.succ[1], R.wgt[1], sh_after(1));
+  } else {
+    launch(k_link_tour, grid_for(N0, B), B, 0, st, ta, n, R.nxt, (const Scalars*)sc, shift(R.S[0]));
+  }
   note(K_LINK_TOUR);
   // ruling-set levels
   launch(inplace ? k_walk<false, true> : k_walk<false, false>, grid_for(R.K[1], B, 64), B, 0, st, (int)R.K[1],
