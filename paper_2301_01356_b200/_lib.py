@@ -30,7 +30,7 @@ EXPORTS = ("fbcc_workspace_bytes", "fbcc_run", "fbcc_run_host", "fbcc_strerror",
            "fbcc_kernel_name", "fbcc_plan_create", "fbcc_plan_run", "fbcc_plan_launch", "fbcc_plan_stats", "fbcc_plan_destroy",
            "fbcc_set_option", "fbcc_get_option")
 
-OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "s0": 3, "sl": 4, "compress_mask": 8, "pdl": 11, "stream_chunks": 12, "skel_parent": 13, "giant_fold": 14, "eb_staged": 15, "max_rounds": 16, "skel_max_rounds": 17, "accept_fold": 18, "detach": 19}
+OPTIONS = {"sample_rounds": 0, "giant_skip": 1, "s0": 3, "sl": 4, "compress_mask": 8, "pdl": 11, "stream_chunks": 12, "skel_parent": 13, "giant_fold": 14, "eb_staged": 15, "max_rounds": 16, "skel_max_rounds": 17, "accept_fold": 18, "detach": 19, "witness": 20}
 
 
 def set_option(name: str, value: int) -> None:

@@ -1,6 +1,7 @@
 // api.cu -- the C ABI (include/fastbcc_b200.h): workspace layout, the
 // six-stage orchestration of fast_bcc (bcc.py:147-196) on one stream, and
 // CUDA-graph plans that replay the whole launch sequence.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -20,7 +21,7 @@ static const char* kKernelNames[K_NUM_KINDS] = {
     "root_flags", "scan", "root_list", "out_lists", "link_tour", "walk0", "walk_level", "final_rank", "expand", "rank0",
     "positions", "firsts", "w_gather", "tile", "table", "fence", "heads", "count_blocks", "ap", "set_edges",
     "edge_blocks", "edge_final", "memset", "export", "widen", "giant_min", "edge_fill", "edge_search", "jump_local",
-    "jump_list", "scan_tiles"};
+    "jump_list", "scan_tiles", "w_sample", "witness_fix", "nlow"};
 
 static int cuda_fail(cudaError_t e, const char* where) {
   snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
@@ -38,7 +39,8 @@ static std::atomic<int> g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*gi
                       /*warp-staged edge-block pass with the giant bitmap*/ 1,
                       /*... plus adaptive rounds up to (skip_round)*/ 3, /*Stage 5 cap (0: same)*/ 0,
                       /*accept folded into the following compress: 2 = auto (n >= 2^22; config 5 -1.3 %, 4b -4.3 %, config 2 +6 % if forced)*/ 2,
-                      /*isolated vertices off the Euler-tour list and the tile pass*/ 1};
+                      /*isolated vertices off the Euler-tour list and the tile pass*/ 1,
+                      /*witness tags: 1 = plans with m >= 8n*/ 1};
 thread_local const Options* t_opt = nullptr;
 
 int option_default(int key) { return g_opt[key].load(std::memory_order_relaxed); }
@@ -58,7 +60,8 @@ constexpr int kMaxStreamChunks = 64;
 struct Layout {
   size_t total = 0;
   size_t sc, sdesc, sdesc_bytes, crow, comp, fe, prop, flags, rootidx, rlist, lhead, hsub, nexto, nxt, own0, rank0, rec, AP, lh1, lh2, table, cnt, uoff,
-      nlow, bmin, w0, cub;
+      nlow, bmin, w0, cub, wfirsts;
+  bool witness = false;  // Stage 3 from the rows' first arcs (tags.cu): m >= 8n (or forced), positions below 2^30
   size_t lsucc[8], lwgt[8], lown[8], loffs[8];
   int nlev = 0;
   int64_t K[8] = {0};
@@ -125,6 +128,9 @@ struct Layout {
     bmin = take(4 * n);
     w0 = take(12 * n);
     cub = take(cub_bytes);
+    const int wopt = o.v[OPT_WITNESS];
+    witness = m > 0 && 2 * n < (1ll << 30) && (wopt == 2 || (wopt == 1 && m >= 8 * n));
+    wfirsts = witness ? take(4 * n) : 0;  // its own compact first[] (the tile pass reuses the shared one)
   }
 };
 
@@ -145,8 +151,10 @@ struct Pipeline {
   int* nlow;
   int* bmin;
   const Side* side = nullptr;  // second stream for Stage 6's independent pieces (plan capture, host path)
+  Witness W;        // witness plan (Layout::witness); off for a run that exports low / high / w
   int* w0;          // [3][n] each row's arc 0-2 targets (Stage 1's round 0 -> the sampling rounds of Stages 1, 5)
   bool w0_valid = false;
+  bool no_witness = false;  // this run exports w1 / w2 / low / high (fbcc_debug)
 
   Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
            const fbcc_outputs* o, const Options& op)
@@ -185,7 +193,7 @@ struct Pipeline {
       R.offs[l] = (int*)at(lay.loffs[l]);
     }
     R.rec = (int4*)at(lay.rec);
-    R.firsts = (int*)at(lay.lh1);  // Stage 3's compact first[] (see stage3_tags)
+    R.firsts = (int*)at(lay.witness ? lay.wfirsts : lay.lh1);  // Stage 3's compact first[] (see stage3_tags)
     R.nlow = (int*)at(lay.nlow);
     R.cub_tmp = at(lay.cub);
     R.cub_bytes = lay.cub_bytes;
@@ -202,6 +210,11 @@ struct Pipeline {
     nlow = (int*)at(lay.nlow);
     bmin = (int*)at(lay.bmin);
     w0 = (int*)at(lay.w0);
+    W.on = lay.witness;
+    W.w0 = w0;
+    W.und_list = R.rlist;  // (the root list is dead once the tour is linked)
+    W.cap = (int)std::min<int64_t>(n, 1 << 20);
+    W.work = (unsigned long long)std::max<int64_t>(4096, std::min<int64_t>(n / 8, 1 << 22));
   }
 
   // Enqueue all six stages.  ev (7 events) brackets the stages when given.
@@ -251,9 +264,12 @@ struct Pipeline {
                     cudaEvent_t heads_done) {
     stage2_rooting_fused(g, comp, fe, R, T.AP, sc, st);
     mk(2);
-    stage3_tags(g, R, T, st, nlow, side, uoff, R.cub_tmp, R.cub_bytes, sc);
+    // (the sampled tags need Stage 1's recorded arcs, and leave low / high inexact: not for debug exports)
+    Witness Wr = W;
+    if (low_out || high_out || !w0_valid || no_witness) Wr.on = false;
+    stage3_tags(g, R, T, st, nlow, side, uoff, R.cub_tmp, R.cub_bytes, sc, &Wr);
     mk(3);
-    stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st);
+    stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st, sc, &Wr);
     mk(4);
     stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st, w0_valid ? w0 : nullptr);
     mk(5);
@@ -444,6 +460,7 @@ int fbcc_run(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m
   log->profile = (flags & FBCC_FLAG_PROFILE) && stats;
   log->start();
   g_log = log;
+  P.no_witness = dbg != nullptr;
   P.enqueue(st, timing ? ev : nullptr, dbg ? dbg->low : nullptr, dbg ? dbg->high : nullptr);
   g_log = nullptr;
   cudaError_t e = cudaGetLastError();

@@ -14,7 +14,7 @@ constexpr int kINF = 0x7FFFFFFF;
 // Device-side scalars shared by the stages (lives at the head of the
 // workspace).  Counts that only the device knows stay here so that no stage
 // needs a host round trip (the whole run is one asynchronous stream).
-struct Scalars {
+struct alignas(8) Scalars {
   int ncomp;       // c: number of components of the first pass (roots)
   int giant;       // sampled most-frequent root (Afforest skip)
   int nbccs;       // number of blocks
@@ -34,7 +34,10 @@ struct Scalars {
   int tour_len;    // list elements = 2 (n - detached roots); detached positions follow
   int near[2];     // round-0 hooks to a vertex within kNear ids (stage 1 / stage 5): id-ordered chains (meshes)
   int jlist_n[2];  // exit targets listed by k_jump_local (same split)
-  int pad[11];
+  int und_n;       // witness tags: vertices whose sampled arcs left their fence bit undecided (k_fence phase A)
+  unsigned long long und_work;  // ... tour positions under all of them (8-byte aligned: 54 ints precede it)
+  int und_big;     // ... one of them with a subtree too large for k_witness_fix
+  int pad[7];
 };
 
 // ---------------------------------------------------------------------------
@@ -46,7 +49,7 @@ enum KernelKind : int {  // one kind per kernel function (names: api.cu kKernelN
   K_ROOT_FLAGS, K_SCAN, K_ROOT_LIST, K_OUT_LISTS, K_LINK_TOUR, K_WALK0, K_WALKL, K_FINAL_RANK, K_EXPAND, K_RANK0,
   K_POSITIONS, K_FIRSTS, K_W_GATHER, K_TILE, K_TABLE, K_FENCE, K_HEADS, K_COUNT_BLOCKS, K_AP, K_SET_EDGES,
   K_EDGE_BLOCKS, K_EDGE_FINAL, K_MEMSET, K_EXPORT, K_WIDEN, K_GIANT_MIN, K_EDGE_FILL, K_EDGE_SEARCH, K_JUMP_LOCAL,
-  K_JUMP_LIST, K_SCAN_TILES, K_NUM_KINDS
+  K_JUMP_LIST, K_SCAN_TILES, K_W_SAMPLE, K_WITNESS_FIX, K_NLOW, K_NUM_KINDS
 };
 
 struct LaunchLog {
@@ -94,8 +97,9 @@ enum Option : int {
   OPT_SKEL_MAX_ROUNDS = 17,  // Stage 5's cap instead (0: OPT_MAX_ROUNDS)
   OPT_ACCEPT_FOLD = 18,   // a sampling round's accept runs inside the compress that follows it (2: auto by size)
   OPT_DETACH = 19,        // isolated vertices stay off the Euler-tour list and out of the tile pass
+  OPT_WITNESS = 20,       // Stage 3 from each row's first three arcs + exact repair (0 off, 1 when m >= 8n, 2 always)
   // (keys 2, 5, 6, 7, 9, 10: retired experiments -- accepted, ignored)
-  OPT_NUM = 20
+  OPT_NUM = 21
 };
 struct Options {
   int v[OPT_NUM];

@@ -144,11 +144,22 @@ struct Side {
   cudaEvent_t ev[4] = {};  // fork scan, join scan, fork ap, join ap
 };
 
+// Witness plans (tags.cu): Stage 3 from each row's first three arcs, the open
+// fence bits repaired exactly; the full gather only if the repair overflows
+struct Witness {
+  bool on = false;
+  const int* w0 = nullptr;        // [3][n] arcs 0-2 of every row (k_chunk_rows)
+  int* und_list = nullptr;        // [cap] vertices to repair (a dead Stage-2 array)
+  int cap = 0;
+  unsigned long long work = 0;    // tour positions the repair may walk in all
+};
+
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow, const Side* side = nullptr,
-                 int* uoff = nullptr, void* cub_tmp = nullptr, size_t cub_bytes = 0, Scalars* sc = nullptr);
-void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
-                  int* bmin,
-                  cudaStream_t st);
+                 int* uoff = nullptr, void* cub_tmp = nullptr, size_t cub_bytes = 0, Scalars* sc = nullptr,
+                 const Witness* W = nullptr);
+void stage4_fence(const Graph& g, const Rooting& R, Tags& T, int* low_out, int* high_out, int* head, int* cnt,
+                  int* bmin, cudaStream_t st, Scalars* sc = nullptr, const Witness* W = nullptr);
+void compute_nlow(const Graph& g, int* nlow, cudaStream_t st);
 // (w0: [3][n] each row's first three arc targets, recorded by k_chunk_rows' round 0; nullptr: read adj)
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
                         cudaStream_t st, const int* w0 = nullptr);

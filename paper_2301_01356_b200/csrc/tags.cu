@@ -80,6 +80,93 @@ __device__ __forceinline__ void w_atomic(int4* AP, int fv, int m1, int m2) {
   atomicMax(&AP[fv].y, m2);
 }
 
+// ---------------------------------------------------------------------------
+// Witness tags.  fence[v] only asks whether some non-tree edge under v leaves
+// the parent's interval, and on a dense graph almost every vertex shows such
+// an edge among its first arcs: RMAT s25 -- of 17.1 M tree edges, the first
+// three arcs of every row (already recorded by Stage 1, w0[3][n]) leave 56
+// fence bits open; uniform 2^20 x 8 leaves 271.  Plans with m >= 8n therefore
+// run Stage 3 on those samples:
+//   1. k_w_sample: (w1, w2) from arcs 0-2 of each row (3 coalesced reads and
+//      3 gathers per vertex instead of a gather per arc), bit 30 of w2 set
+//      when the row has more arcs -- the tile pass's max carries the bit up
+//      every subtree, so "exact" (no row under v was cut short) is known too;
+//   2. the tile pass and k_fence as usual: a bit that comes out 0 has a real
+//      witness edge, one that comes out 1 over an exact subtree (or under a
+//      root) is exact; the others are listed;
+//   3. k_witness_fix: one warp per listed vertex rescans every row under it
+//      (the tour positions first..last name them) and settles the bit.
+// If too many are listed, or one has too large a subtree, the full gather and
+// a second tile / fence pass run instead (their kernels are in the plan and
+// return at once otherwise).  Only the fence bits feed the later stages, and
+// they are exact either way; low/high themselves are exact only in the full
+// form, which debug exports and the stand-alone ops always use.
+// ---------------------------------------------------------------------------
+constexpr int kExactBit = 1 << 30;        // tour positions stay below 2^30 in witness plans
+constexpr int kWitnessListCap = 1 << 20;  // listed vertices (<= n: the list is a dead Stage-2 array)
+constexpr int kWitnessMaxSubtree = 1 << 11;  // tour positions one warp may walk for one vertex
+
+struct WitnessGate {
+  const Scalars* sc;  // nullptr: not a witness plan, always open
+  int cap;
+  unsigned long long work;
+  // after k_fence's phase A: do the full gather / tile / fence kernels have to run?
+  __device__ __forceinline__ bool open() const {
+    return !sc || sc->und_n > cap || sc->und_big != 0 || sc->und_work > work;
+  }
+};
+
+__global__ void k_w_sample(const int64_t* __restrict__ off, int n, const int4* __restrict__ rec,
+                           const int* __restrict__ firsts, const int* __restrict__ w0, int4* AP,
+                           const int* __restrict__ tlen) {
+  pdl_enter();
+  const int N = *tlen;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int4 r = __ldg(rec + v);
+    if (r.x >= N) continue;  // detached root: no tour entry
+    const int64_t deg = __ldg(off + v + 1) - __ldg(off + v);
+    int m1 = r.x, m2 = r.x;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      if (deg > k) {
+        const int w = __ldg(w0 + (int64_t)k * n + v);
+        if (w != r.z) {
+          const int f = __ldg(firsts + w);
+          m1 = min(m1, f);
+          m2 = max(m2, f);
+        }
+      }
+    }
+    __stcs(reinterpret_cast<int2*>(AP + r.x), make_int2(m1, deg > 3 ? (m2 | kExactBit) : m2));
+  }
+}
+
+// nlow[v] = neighbours of v below v (rows sorted): the row's last and first
+// arcs settle most rows (RMAT: nearly every vertex has only smaller
+// neighbours, the hubs mostly larger ones), the rest by binary search
+__global__ void k_nlow(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
+                       int* __restrict__ nlow) {
+  pdl_enter();
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int64_t lo = __ldg(off + v), hi = __ldg(off + v + 1);
+    const int64_t rs = lo;
+    if (hi > lo) {
+      if ((int)__ldg(adj + hi - 1) < v) lo = hi;
+      else if ((int)__ldg(adj + lo) > v) hi = lo;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int)__ldg(adj + mid) < v) lo = mid + 1; else hi = mid;
+      }
+    }
+    nlow[v] = (int)(lo - rs);
+  }
+}
+
+void compute_nlow(const Graph& g, int* nlow, cudaStream_t st) {
+  launch(k_nlow, grid_for(g.n, 256), 256, 0, st, g.off, g.adj, g.n, nlow);
+  note(K_NLOW);
+}
+
 // Arc-balanced like visit_arc_chunks (8 arcs per thread, the chunk's row from
 // crow), but rows that straddle chunk boundaries are combined inside the warp
 // instead of with two atomics per piece: consecutive lanes hold consecutive
@@ -96,16 +183,17 @@ __device__ __forceinline__ void w_atomic(int4* AP, int fv, int m1, int m2) {
 #endif
 constexpr int kWGatherMinBlocks = FBCC_WG_MIN_BLOCKS;
 
-template <bool kExact>
+template <bool kExact, bool kCountLow = !kExact>
 __global__ void __launch_bounds__(256, kWGatherMinBlocks) k_w_gather(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                   const int* __restrict__ crow, int n, int64_t m,
                                                   const int4* __restrict__ rec, const int* __restrict__ firsts,
-                                                  int4* AP, int* __restrict__ nlow) {
+                                                  int4* AP, int* __restrict__ nlow, WitnessGate gate) {
   pdl_enter();
+  if (!gate.open()) return;  // (a witness plan whose sampled tags settled every fence bit)
   // the pipeline variant also counts each row's lower neighbours (w < v) for
   // Stage 6's edge numbering (k_upper_degree's binary searches, folded into
-  // this pass over the same arcs)
-  constexpr bool kCount = !kExact;
+  // this pass over the same arcs; witness plans count them in k_nlow)
+  constexpr bool kCount = kCountLow;
   const int64_t nchunks = (m + kItems - 1) / kItems;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(adj) & 31) == 0);
   const int lane = threadIdx.x & 31;
@@ -307,8 +395,9 @@ __device__ __forceinline__ int64_t list_positions(const int* tlen, int64_t N) { 
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict__ AP,
                                                           int64_t N, int ntile, int2* __restrict__ lh1,
                                                           int2* __restrict__ lh2, int2* __restrict__ table0, Scalars* sc, int tlev,
-                                                          const int* tlen) {
+                                                          const int* tlen, WitnessGate gate) {
   pdl_enter();
+  if (!gate.open()) return;
   N = list_positions(tlen, N);
   const int nt = (int)((N + kTile - 1) / kTile);
   extern __shared__ __align__(128) unsigned char tsm[];
@@ -408,13 +497,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict
 // published to the block by __syncthreads; every level is tiny next to a
 // launch when ntile <= kTableOneCta)
 
-__global__ void __launch_bounds__(1024) k_table_all(int2* table, int ntile, int tlev, const int* tlen) {
+__global__ void __launch_bounds__(1024) k_table_all(int2* table, int ntile, int tlev, const int* tlen,
+                                                    WitnessGate gate) {
   pdl_enter();
+  if (!gate.open()) return;
   table_levels(table, ntile, (int)((list_positions(tlen, (int64_t)ntile * kTile) + kTile - 1) / kTile), tlev);
 }
 
-__global__ void k_table_level(int2* table, int ntile, int k, const int* tlen) {
+__global__ void k_table_level(int2* table, int ntile, int k, const int* tlen, WitnessGate gate) {
   pdl_enter();
+  if (!gate.open()) return;
   const int nt = (int)((list_positions(tlen, (int64_t)ntile * kTile) + kTile - 1) / kTile);
   const int2* prev = table + (int64_t)(k - 1) * ntile;
   int2* cur = table + (int64_t)k * ntile;
@@ -425,14 +517,49 @@ __global__ void k_table_level(int2* table, int ntile, int k, const int* tlen) {
   }
 }
 
+static WitnessGate gate_of(const Witness* W, const Scalars* sc) {
+  return (W && W->on) ? WitnessGate{sc, W->cap, W->work} : WitnessGate{nullptr, 0, 0};
+}
+
+// tile pass + the tile-extreme table (gate: see WitnessGate; an open-ended
+// gate {nullptr} always runs)
+static void tile_pass(const Graph& g, Tags& T, cudaStream_t st, Scalars* sc, WitnessGate gate) {
+  const int B = 256;
+  cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+  // (the table in k_tile's last block when it fits one CTA and a ticket word exists)
+  Scalars* tsc = (sc && T.ntile <= kTableOneCta && T.tlev > 1) ? sc : nullptr;
+  launch(k_tile, T.ntile < kNumSMs ? T.ntile : kNumSMs, kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile,
+         T.lh1, T.lh2, T.table, tsc, T.tlev, T.tour_len, gate);
+  note(K_TILE);
+  if (tsc) {
+  } else if (T.ntile <= kTableOneCta) {
+    if (T.tlev > 1) {
+      launch(k_table_all, 1, 1024, 0, st, T.table, T.ntile, T.tlev, T.tour_len, gate);
+      note(K_TABLE);
+    }
+  } else {
+    for (int k = 1; k < T.tlev; k++) {
+      launch(k_table_level, grid_for(T.ntile, B), B, 0, st, T.table, T.ntile, k, T.tour_len, gate);
+      note(K_TABLE);
+    }
+  }
+}
+
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow, const Side* side, int* uoff,
-                 void* cub_tmp, size_t cub_bytes, Scalars* sc) {
+                 void* cub_tmp, size_t cub_bytes, Scalars* sc, const Witness* W) {
   const int B = 256;
   int64_t nchunks = (g.m + kItems - 1) / kItems;
+  const bool witness = W && W->on;
+  const WitnessGate none{nullptr, 0, 0};
   if (!nlow) {  // stand-alone compute_tags: the reference's exact w2
     if (g.m > 0)
       launch(k_w_gather<true>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, nullptr, T.AP,
-             nullptr);
+             nullptr, none);
+  } else if (witness) {
+    // (compact first[]: its own array, written by k_positions -- the tile pass must not overwrite it)
+    launch(k_w_sample, grid_for(g.n, B), B, 0, st, g.off, g.n, (const int4*)R.rec, (const int*)R.firsts, W->w0, T.AP,
+           T.tour_len);
+    note(K_W_SAMPLE);
   } else {
     // compact first[] lives in lh1 until k_tile overwrites it
     int* firsts = reinterpret_cast<int*>(T.lh1);
@@ -442,45 +569,39 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
     }
     if (g.m > 0)
       launch(k_w_gather<false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, firsts,
-             T.AP, nlow);
+             T.AP, nlow, none);
   }
-  if (g.m > 0) {
+  if (g.m > 0 && !witness) {
     note(K_W_GATHER);
+  }
+  if (nlow && witness && !side) {  // (no second stream: the lower-degree counts here, the scan in Stage 6)
+    compute_nlow(g, nlow, st);
   }
   if (side && nlow) {  // nlow is final: Stage 6's upper-degree scan runs beside Stages 3-5
     cudaEventRecord(side->ev[0], st);
     cudaStreamWaitEvent(side->s, side->ev[0], 0);
+    if (witness) compute_nlow(g, nlow, side->s);  // (the full gather counts them; the sampled one cannot)
     scan_upper_degrees(g.off, nlow, g.n, uoff, cub_tmp, cub_bytes, side->s);
     note(K_SCAN);
     cudaEventRecord(side->ev[1], side->s);
   }
-  cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-  // (the table in k_tile's last block when it fits one CTA and a ticket word exists)
-  Scalars* tsc = (sc && T.ntile <= kTableOneCta && T.tlev > 1) ? sc : nullptr;
-  launch(k_tile, T.ntile < kNumSMs ? T.ntile : kNumSMs, kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile,
-         T.lh1, T.lh2, T.table, tsc, T.tlev, T.tour_len);
-  note(K_TILE);
-  if (tsc) {
-  } else if (T.ntile <= kTableOneCta) {
-    if (T.tlev > 1) {
-      launch(k_table_all, 1, 1024, 0, st, T.table, T.ntile, T.tlev, T.tour_len);
-      note(K_TABLE);
-    }
-  } else {
-    for (int k = 1; k < T.tlev; k++) {
-      launch(k_table_level, grid_for(T.ntile, B), B, 0, st, T.table, T.ntile, k, T.tour_len);
-      note(K_TABLE);
-    }
-  }
+  tile_pass(g, T, st, sc, none);
 }
 
 // ---------------------------------------------------------------------------
 // Stage 4: combine, fence bit
 // ---------------------------------------------------------------------------
+// kPhaseA (witness plans): the tags came from k_w_sample.  A bit that comes
+// out 0 has a witness; one that comes out 1 is exact when no row under v was
+// cut short (bit 30 of the subtree maximum clear) or v hangs off a root (always
+// a fence); the rest -- written 1 for now -- are listed for k_witness_fix.
+template <bool kPhaseA>
 __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const int2* __restrict__ lh2,
                         const int2* __restrict__ table, int ntile, int* low_out, int* high_out,
-                        int* __restrict__ head, int* __restrict__ cnt, int* __restrict__ bmin, const int* tlen) {
+                        int* __restrict__ head, int* __restrict__ cnt, int* __restrict__ bmin, const int* tlen,
+                        WitnessGate gate, int* __restrict__ und_list, Scalars* sc) {
   pdl_enter();
+  if (!kPhaseA && !gate.open()) return;
   const int64_t N = list_positions(tlen, 2 * (int64_t)n);
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
@@ -499,10 +620,22 @@ __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const in
         res = comb(res, comb(table[(int64_t)k * ntile + i], table[(int64_t)k * ntile + j - (1 << k) + 1]));
       }
     }
+    bool cut = false;  // some row under v was sampled, not scanned
+    if (kPhaseA) {
+      cut = (res.y & kExactBit) != 0;
+      res.y &= ~kExactBit;
+    }
     int fence = 0;
     if (r.z >= 0) {
       int4 pr = rec[r.z];
       fence = (res.x >= pr.x && res.y <= pr.y) ? 1 : 0;
+      if (kPhaseA && fence && cut && pr.z >= 0) {  // undecided
+        const int span = r.y - r.x + 1;
+        if (span > kWitnessMaxSubtree) sc->und_big = 1;
+        const int at = atomicAdd(&sc->und_n, 1);
+        if (at < gate.cap) und_list[at] = v;
+        atomicAdd(&sc->und_work, (unsigned long long)span);
+      }
     }
     reinterpret_cast<int*>(rec + v)[3] = fence;
     if (low_out) {
@@ -517,11 +650,96 @@ __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const in
   }
 }
 
-void stage4_fence(const Graph& g, const Rooting& R, const Tags& T, int* low_out, int* high_out, int* head, int* cnt,
-                  int* bmin, cudaStream_t st) {
+// The listed vertices' fence bits from every row under them: one warp per
+// vertex walks its tour interval; an entry position names a vertex of the
+// subtree, whose row the warp scans.  When the gate is open (too many listed,
+// or too much under them) the full gather takes over instead, and this kernel
+// only restores the (first, first) start values it accumulates into.
+__global__ void __launch_bounds__(256) k_witness_fix(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                                     int n, int4* rec, int4* AP, const int* __restrict__ und_list,
+                                                     const int* __restrict__ tlen, WitnessGate gate) {
+  pdl_enter();
+  const int N = *tlen;
+  if (gate.open()) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+      const int f = __ldg(&rec[v].x);
+      if (f < N) *reinterpret_cast<int2*>(AP + f) = make_int2(f, f);
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int cnt = gate.sc->und_n;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += warps) {
+    const int v = und_list[i];
+    const int4 r = rec[v];
+    int lo = r.x, hi = r.x;
+    auto take = [&](int w, int px) {
+      if (w == px) return;  // the tree edge to the parent
+      const int f = __ldcg(&rec[w].x);
+      lo = min(lo, f);
+      hi = max(hi, f);
+    };
+    // 32 tour positions at a time, a lane each; rows over 64 arcs by the whole warp
+    for (int p0 = r.x; p0 <= r.y; p0 += 32) {
+      const int p = p0 + lane;
+      const int x = p <= r.y ? AP[p].z : -1;  // (< 0: an exit position)
+      int px = -1;
+      int64_t rs = 0, re = 0;
+      if (x >= 0) {
+        px = __ldcg(&rec[x].z);
+        rs = __ldg(off + x);
+        re = __ldg(off + x + 1);
+      }
+      const bool big = re - rs > 64;
+      if (!big)
+        for (int64_t a = rs; a < re; a++) take((int)__ldg(adj + a), px);
+      unsigned bm = __ballot_sync(0xffffffffu, big);
+      while (bm) {
+        const int src = __ffs(bm) - 1;
+        bm &= bm - 1;
+        const int bpx = __shfl_sync(0xffffffffu, px, src);
+        const int64_t bs = __shfl_sync(0xffffffffu, rs, src), be = __shfl_sync(0xffffffffu, re, src);
+        for (int64_t a = bs + lane; a < be; a += 32) take((int)__ldg(adj + a), bpx);
+      }
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0) {
+      const int4 pr = rec[r.z];
+      reinterpret_cast<int*>(rec + v)[3] = (lo >= pr.x && hi <= pr.y) ? 1 : 0;
+    }
+  }
+}
+
+void stage4_fence(const Graph& g, const Rooting& R, Tags& T, int* low_out, int* high_out, int* head, int* cnt,
+                  int* bmin, cudaStream_t st, Scalars* sc, const Witness* W) {
   const int B = 256;
-  launch(k_fence, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out, head,
-                                          cnt, bmin, T.tour_len);
+  const WitnessGate gate = gate_of(W, sc);
+  if (!(W && W->on)) {
+    launch(k_fence<false>, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out,
+           head, cnt, bmin, T.tour_len, gate, (int*)nullptr, sc);
+    note(K_FENCE);
+    return;
+  }
+  // witness plan: fence bits from the sampled tags, the open ones repaired;
+  // then the full gather / tile / fence -- which return at once unless the
+  // repair list overflowed (WitnessGate)
+  launch(k_fence<true>, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, (int*)nullptr,
+         (int*)nullptr, head, cnt, bmin, T.tour_len, gate, W->und_list, sc);
+  note(K_FENCE);
+  launch(k_witness_fix, grid_for((int64_t)W->cap * 32, B, 16), B, 0, st, g.off, g.adj, g.n, R.rec, T.AP,
+         (const int*)W->und_list, T.tour_len, gate);
+  note(K_WITNESS_FIX);
+  const int64_t nchunks = (g.m + kItems - 1) / kItems;
+  if (g.m > 0) {
+    launch(k_w_gather<false, false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec,
+           (const int*)R.firsts, T.AP, (int*)nullptr, gate);
+    note(K_W_GATHER);
+  }
+  tile_pass(g, T, st, sc, gate);
+  launch(k_fence<false>, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, (int*)nullptr,
+         (int*)nullptr, head, cnt, bmin, T.tour_len, gate, (int*)nullptr, sc);
   note(K_FENCE);
 }
 

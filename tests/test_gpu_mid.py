@@ -96,7 +96,10 @@ def test_mid_graph_rungs(name, oracle_mod):
 OPTION_VARIANTS = [{"eb_staged": 0}, {"max_rounds": 6}, {"max_rounds": 8, "sample_rounds": 2}, {"pdl": 0},
                    {"sample_rounds": 1}, {"giant_skip": 0}, {"s0": 8, "sl": 4}, {"accept_fold": 1},
                    {"accept_fold": 1, "max_rounds": 5}, {"skel_parent": 131}, {"skel_max_rounds": 4},
-                   {"compress_mask": 0}, {"detach": 0}, {"detach": 0, "s0": 8, "sl": 4}]
+                   {"compress_mask": 0}, {"detach": 0}, {"detach": 0, "s0": 8, "sl": 4},
+                   # Stage 3 from the rows' first three arcs (forced: the meshes overflow the repair list and
+                   # fall back to the full gather inside the same plan) and without it
+                   {"witness": 2}, {"witness": 0}, {"witness": 2, "detach": 0}]
 
 
 @pytest.mark.parametrize("name", ["rmat_s16", "isolated_mix", "star_mid_20k", "uniform_64k_d3", "chain_300k",
@@ -197,3 +200,60 @@ def test_random_graphs_match_oracle(block, oracle_mod):
         for k in ("label", "head", "is_ap", "edge_label"):
             assert np.array_equal(r[k], ref[k]), (seed, k)
         assert r["num_bccs"] == ref["num_bccs"] and r["num_components"] == ref["num_components"], seed
+
+
+def _core_with_blobs(seed):
+    """A dense random core with dense blobs hanging off single cut vertices: the
+    blob's top tree edge is a fence whose subtree holds rows of more than three
+    arcs (one of them a hub over 64), so the sampled tags leave it open and
+    k_witness_fix has to rescan a few hundred rows."""
+    rng = np.random.default_rng(seed)
+    nc = 4096
+    pairs = [rng.integers(0, nc, size=(nc * 8, 2))]
+    n = nc
+    for b in range(6):
+        size = int(rng.integers(40, 700))
+        ids = np.arange(n, n + size)
+        hub = ids[int(rng.integers(0, size))]
+        pairs.append(np.column_stack([np.full(size, hub), ids]))                      # a hub row
+        pairs.append(ids[rng.integers(0, size, size=(size * 3, 2))])                  # dense inside
+        pairs.append(np.array([[int(rng.integers(0, nc)), ids[int(rng.integers(0, size))]]]))  # one cut edge
+        n += size
+    p = np.concatenate(pairs).astype(np.int64)
+    return symmetrize(p[p[:, 0] != p[:, 1]], n)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_witness_repair_paths(seed, oracle_mod):
+    from paper_2301_01356_b200 import _lib
+
+    g = _core_with_blobs(seed)
+    ref = oracle_mod.fast_bcc(g.offsets, g.edges)
+    old = _lib.get_option("witness")
+    try:
+        for w in (2, 1, 0):
+            _lib.set_option("witness", w)
+            r = _run(g, debug=False)
+            for k in ("label", "head", "is_ap", "edge_label"):
+                assert np.array_equal(r[k], ref[k]), (seed, w, k)
+            assert r["num_bccs"] == ref["num_bccs"] and r["num_components"] == ref["num_components"]
+    finally:
+        _lib.set_option("witness", old)
+
+
+def test_random_graphs_witness_forced(oracle_mod):
+    """The seeded random graphs again with the sampled tags forced on."""
+    from paper_2301_01356_b200 import _lib
+
+    old = _lib.get_option("witness")
+    try:
+        _lib.set_option("witness", 2)
+        for seed in range(0, 200, 3):
+            g = _random_graph(seed)
+            ref = oracle_mod.fast_bcc(g.offsets, g.edges)
+            r = _run(g, debug=False)
+            for k in ("label", "head", "is_ap", "edge_label"):
+                assert np.array_equal(r[k], ref[k]), (seed, k)
+            assert r["num_bccs"] == ref["num_bccs"] and r["num_components"] == ref["num_components"], seed
+    finally:
+        _lib.set_option("witness", old)
