@@ -102,6 +102,10 @@ __device__ __forceinline__ void w_atomic(int4* AP, int fv, int m1, int m2) {
 // they are exact either way; low/high themselves are exact only in the full
 // form, which debug exports and the stand-alone ops always use.
 // ---------------------------------------------------------------------------
+#ifndef FBCC_WITNESS_ARCS
+#define FBCC_WITNESS_ARCS 3
+#endif
+constexpr int kWitnessArcs = FBCC_WITNESS_ARCS;  // arcs sampled per row (<= 3: what k_chunk_rows records)
 constexpr int kExactBit = 1 << 30;        // tour positions stay below 2^30 in witness plans
 constexpr int kWitnessListCap = 1 << 20;  // listed vertices (<= n: the list is a dead Stage-2 array)
 constexpr int kWitnessMaxSubtree = 1 << 11;  // tour positions one warp may walk for one vertex
@@ -122,22 +126,26 @@ __global__ void k_w_sample(const int64_t* __restrict__ off, int n, const int4* _
   pdl_enter();
   const int N = *tlen;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const int4 r = __ldg(rec + v);
-    if (r.x >= N) continue;  // detached root: no tour entry
+    // every per-vertex word first (coalesced, independent of one another),
+    // then the gathers together: one vertex is two dependent round trips,
+    // not five (loaded behind its guards the kernel sat at 30 % of DRAM, 1.0 ms)
+    const int fv = __ldg(firsts + v);
+    const int pv = __ldg(&rec[v].z);
     const int64_t deg = __ldg(off + v + 1) - __ldg(off + v);
-    int m1 = r.x, m2 = r.x;
+    int w[kWitnessArcs];
 #pragma unroll
-    for (int k = 0; k < 3; k++) {
-      if (deg > k) {
-        const int w = __ldg(w0 + (int64_t)k * n + v);
-        if (w != r.z) {
-          const int f = __ldg(firsts + w);
-          m1 = min(m1, f);
-          m2 = max(m2, f);
-        }
-      }
+    for (int k = 0; k < kWitnessArcs; k++) w[k] = __ldg(w0 + (int64_t)k * n + v);  // (arc 0 of an empty row: unwritten, unused)
+    if (fv >= N) continue;  // detached root: no tour entry
+    int f[kWitnessArcs];
+#pragma unroll
+    for (int k = 0; k < kWitnessArcs; k++) f[k] = (deg > k && w[k] != pv) ? __ldg(firsts + w[k]) : fv;
+    int m1 = fv, m2 = fv;
+#pragma unroll
+    for (int k = 0; k < kWitnessArcs; k++) {
+      m1 = min(m1, f[k]);
+      m2 = max(m2, f[k]);
     }
-    __stcs(reinterpret_cast<int2*>(AP + r.x), make_int2(m1, deg > 3 ? (m2 | kExactBit) : m2));
+    __stcs(reinterpret_cast<int2*>(AP + fv), make_int2(m1, deg > kWitnessArcs ? (m2 | kExactBit) : m2));
   }
 }
 
