@@ -159,7 +159,7 @@ int fbcc_plan_destroy(fbcc_plan plan);
    tests/test_gpu_mid.py::test_mid_graph_option_paths).  Thread-safe: each
    call (fbcc_run, fbcc_run_host, an op) and each plan snapshots the defaults
    once and runs with its own copy, so a concurrent fbcc_set_option never
-   changes a run in flight.  Keys 3/4 change fbcc_workspace_bytes.  Keys:
+   changes a run in flight.  Keys 3/4/20 change fbcc_workspace_bytes.  Keys:
      0  sampling rounds always run (0..8; default 2)
      1  giant-component skip in the remaining-arc link pass (0/1; 1)
      3  level-0 list-ranking splitter spacing (power of two >= 2; 16)
@@ -178,6 +178,11 @@ int fbcc_plan_destroy(fbcc_plan plan);
         n >= 2^22; 2: configs 4a/4b/4c/5 -1 to -4 %, config 2 would be +6 %)
     19  isolated vertices (but vertex 0) stay off the Euler-tour list and out of
         the tile pass; their tour positions follow the list's (0/1; 1)
+    20  Stage 3 from each row's first three arcs, the fence bits they leave open
+        repaired exactly, the full per-arc gather only if that repair overflows
+        (0 off, 1 plans with m >= 8n, 2 every plan with 2n < 2^30; 1).  Changes
+        fbcc_workspace_bytes (4n more).  Runs that export w1/w2/low/high
+        (fbcc_debug) and fbcc_run_host always use the full gather.
    Keys 2, 5, 6, 7, 9, 10 are retired experiments: accepted and ignored. */
 int fbcc_set_option(int key, int value);
 int fbcc_get_option(int key);
