@@ -34,7 +34,7 @@ static std::atomic<int> g_opt[OPT_NUM] = {/*sample rounds (always run)*/ 2, /*gi
                       /*retired*/ 0, 0, 0, /*compress after rounds mask: 0 = first+last; all rounds: 4b -13%, config 3 -2%*/ 0xFF,
                       /*retired*/ 0, /*retired*/ 0,
                       /*programmatic dependent launch (dependents launch as the previous grid exits)*/ 1,
-                      /*fbcc_run_host edge-copy chunks (at most; one per 2^21 arcs)*/ 4, /*skeleton parent-edge rounds (hook_min + round 1)*/ 3,
+                      /*fbcc_run_host edge-copy chunks (at most; one per 2^21 arcs)*/ 4, /*skeleton parent-edge rounds (bits 0, 1: rounds 0 and 1; 0x80: round 0 on parent edges only, inside Stage 4's pass)*/ 0x83,
                       /*giant pick folded into the last compress*/ 1,
                       /*warp-staged edge-block pass with the giant bitmap*/ 1,
                       /*... plus adaptive rounds up to (skip_round)*/ 3, /*Stage 5 cap (0: same)*/ 0,
@@ -269,9 +269,16 @@ struct Pipeline {
     if (low_out || high_out || !w0_valid || no_witness) Wr.on = false;
     stage3_tags(g, R, T, st, nlow, side, uoff, R.cub_tmp, R.cub_bytes, sc, &Wr);
     mk(3);
-    stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st, sc, &Wr);
+    // Stage 5's round 0 along plain parent edges rides in Stage 4's pass (skel_parent bit 0x80): always
+    // in witness plans (dense graphs), else only where the forest is id-ordered (device-side test;
+    // k_hook_min, which also tries each row's first arc, does better on fragmented meshes and kNN graphs)
+    const bool s5r0 = (opts.v[OPT_SKEL_PARENT] & 0x80) != 0 && opts.v[OPT_SAMPLE_ROUNDS] > 0;
+    const bool s5always = s5r0 && lay.witness;
+    stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st, sc, &Wr, s5r0 ? out.label : nullptr,
+                 s5r0 ? prop : nullptr, s5r0 && !s5always);
     mk(4);
-    stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st, w0_valid ? w0 : nullptr);
+    stage5_skeleton_cc(g, R.rec, out.label, prop, sc, st, w0_valid ? w0 : nullptr, s5always, R.nexto,
+                       s5r0 && !s5always);
     mk(5);
     if (label_done) cudaEventRecord(label_done, st);
     // Stage 2's root list / root ranks / out-list links are dead by Stage 6:

@@ -10,6 +10,12 @@ namespace fbcc {
 
 constexpr int kNumSMs = 148;   // B200
 constexpr int kINF = 0x7FFFFFFF;
+// round 0 hooks a vertex to a smaller neighbour (Stage 5: its plain parent) within
+// this many ids in preference to the minimum one (meshes: connectivity.cu round0_target)
+#ifndef FBCC_NEAR
+#define FBCC_NEAR 64
+#endif
+constexpr int kNear = FBCC_NEAR;
 
 // Device-side scalars shared by the stages (lives at the head of the
 // workspace).  Counts that only the device knows stay here so that no stage
@@ -39,6 +45,12 @@ struct alignas(8) Scalars {
   int und_big;     // ... one of them with a subtree too large for k_witness_fix
   int pad[7];
 };
+
+// Stage 1's round 0 hooked >= 3/4 of the vertices to a near id: the forest, the
+// tour and the plain parent edges follow the id order (tori, paths)
+__device__ __forceinline__ bool id_ordered(const Scalars* sc, int n) {
+  return (long long)sc->near[0] * 4 >= (long long)n * 3;
+}
 
 // ---------------------------------------------------------------------------
 // launch log: counts every launch of ours and, in profile mode, brackets

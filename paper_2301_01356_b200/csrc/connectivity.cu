@@ -153,10 +153,7 @@ __device__ __forceinline__ int link(int u, int w, int* comp, int2* fe) {
 // scatters (k_positions, the w gather's AP stores, the tile pass's partials)
 // become coalesced instead of random.  Random-id graphs (configs 2, 3, 5)
 // almost never have a smaller neighbour within kNear ids and keep the minimum.
-#ifndef FBCC_NEAR
-#define FBCC_NEAR 64
-#endif
-constexpr int kNear = FBCC_NEAR;
+// (kNear: common.cuh)
 
 __device__ __forceinline__ int round0_target(const uint32_t* __restrict__ adj, int v, int64_t rs, int64_t re,
                                              int* first_arc = nullptr) {
@@ -255,8 +252,9 @@ bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, i
 template <int kPred, bool kRecord>
 __global__ void k_hook_min(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int* comp,
                            int2* fe, unsigned long long* __restrict__ prop, PredData pd, bool skel_parent,
-                           bool parent_only) {
+                           bool parent_only, const Scalars* skip_if_ordered) {
   pdl_enter();
+  if (skip_if_ordered && id_ordered(skip_if_ordered, n)) return;  // (Stage 4's k_fence did this round)
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int64_t s = __ldg(off + v);
     int c = v;
@@ -1019,7 +1017,8 @@ __global__ void __launch_bounds__(256) k_jump_list(int* comp, int n, const Scala
 // ri: the final compress also writes Stage 2's root flags / list heads.
 template <int kPred, bool kRecord>
 static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop, PredData pd, Scalars* sc,
-                   int slot, cudaStream_t st, bool round0_done = false, RootInit ri = RootInit{}, int* jlist = nullptr) {
+                   int slot, cudaStream_t st, bool round0_done = false, RootInit ri = RootInit{}, int* jlist = nullptr,
+                   const Scalars* hook_skip = nullptr) {
   const int B = 256;
   const int kBase = opt(OPT_SAMPLE_ROUNDS);
   // adaptive rounds kBase .. kRounds-1 (skip_round); Stage 5 may cap them separately
@@ -1044,7 +1043,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
   } else if (kRounds > 0) {
     const int sp = opt(OPT_SKEL_PARENT);
     launch(k_hook_min<kPred, kRecord>, gv, B, 0, st, g.off, g.adj, g.n, comp, fe, prop, pd, (sp & 1) != 0,
-           (sp & 0x80) != 0);  // round 0
+           (sp & 0x80) != 0 && !hook_skip, hook_skip);  // round 0
     note(K_HOOK_MIN);
   } else {
     launch(k_iota, gv, B, 0, st, comp, g.n, nullptr);
@@ -1203,12 +1202,14 @@ void stage1_forest(const Graph& g, int* comp, int2* fe, unsigned long long* prop
 }
 
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
-                        cudaStream_t st, const int* w0) {
+                        cudaStream_t st, const int* w0, bool round0_done, int* jlist, bool round0_if_ordered) {
   PredData pd{};
   pd.rec = rec;
   pd.w0 = w0;
   pd.warc = w0;  // (rows [n, 3n): arcs 1 and 2; k_chunk_rows recorded all three)
-  run_cc<PRED_SKEL, false>(g, label, nullptr, prop, pd, sc, 8, st);
+  // round0_done: Stage 4's k_fence already hooked every vertex under its plain parent
+  run_cc<PRED_SKEL, false>(g, label, nullptr, prop, pd, sc, 8, st, round0_done, RootInit{},
+                           (round0_done || round0_if_ordered) ? jlist : nullptr, round0_if_ordered ? sc : nullptr);
 }
 
 void masked_cc(const Graph& g, const uint8_t* mask, int* comp, int2* fe, unsigned long long* prop, Scalars* sc,

@@ -157,12 +157,18 @@ struct Witness {
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow, const Side* side = nullptr,
                  int* uoff = nullptr, void* cub_tmp = nullptr, size_t cub_bytes = 0, Scalars* sc = nullptr,
                  const Witness* W = nullptr);
+// (label5 / prop5: also Stage 5's sampling round 0 along plain parent edges -- comp = the parent when the
+// tree edge is no fence and the parent's id is smaller -- and the proposal reset; needs sc)
 void stage4_fence(const Graph& g, const Rooting& R, Tags& T, int* low_out, int* high_out, int* head, int* cnt,
-                  int* bmin, cudaStream_t st, Scalars* sc = nullptr, const Witness* W = nullptr);
+                  int* bmin, cudaStream_t st, Scalars* sc = nullptr, const Witness* W = nullptr, int* label5 = nullptr,
+                  unsigned long long* prop5 = nullptr, bool s5_if_ordered = false);  // (... only on id-ordered forests)
 void compute_nlow(const Graph& g, int* nlow, cudaStream_t st);
 // (w0: [3][n] each row's first three arc targets, recorded by k_chunk_rows' round 0; nullptr: read adj)
+// (round0_done: stage4_fence wrote Stage 5's round 0 -- label5 / prop5 given; jlist: scratch for the
+// id-ordered compress, see stage1_forest)
 void stage5_skeleton_cc(const Graph& g, const int4* rec, int* label, unsigned long long* prop, Scalars* sc,
-                        cudaStream_t st, const int* w0 = nullptr);
+                        cudaStream_t st, const int* w0 = nullptr, bool round0_done = false, int* jlist = nullptr,
+                        bool round0_if_ordered = false);  // (... k_hook_min runs unless the forest is id-ordered)
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, int* heavy, int* sreq, int* spos,
                       void* cub_tmp, size_t cub_bytes, Scalars* sc, cudaStream_t st,

@@ -607,10 +607,13 @@ template <bool kPhaseA>
 __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const int2* __restrict__ lh2,
                         const int2* __restrict__ table, int ntile, int* low_out, int* high_out,
                         int* __restrict__ head, int* __restrict__ cnt, int* __restrict__ bmin, const int* tlen,
-                        WitnessGate gate, int* __restrict__ und_list, Scalars* sc) {
+                        WitnessGate gate, int* __restrict__ und_list, Scalars* sc, int* __restrict__ label5,
+                        unsigned long long* __restrict__ prop5, bool s5_if_ordered) {
   pdl_enter();
   if (!kPhaseA && !gate.open()) return;
+  if (label5 && s5_if_ordered && !id_ordered(sc, n)) label5 = nullptr;  // (k_hook_min runs instead)
   const int64_t N = list_positions(tlen, 2 * (int64_t)n);
+  int near = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     int4 r = rec[v];
     int ta = r.x / kTile, tb = r.y / kTile;
@@ -655,6 +658,20 @@ __global__ void k_fence(int n, int4* rec, const int2* __restrict__ lh1, const in
     head[v] = -1;
     cnt[v] = 0;
     bmin[v] = kINF;
+    // Stage 5's sampling round 0 along plain parent edges (k_hook_min's
+    // parent-only form, one pass and one record gather fewer): the parent
+    // record is already here.  A bit still open in phase A counts as a fence
+    // -- the vertex stays a root, and the link pass covers its tree edge.
+    if (label5) {
+      const bool hook = r.z >= 0 && fence == 0 && r.z < v;
+      label5[v] = hook ? r.z : v;
+      prop5[v] = ~0ull;
+      near += hook && v - r.z <= kNear;
+    }
+  }
+  if (label5) {
+    // (a redo after an overflowed repair counts twice: the count only picks Stage 5's compress variant)
+    block_count_add(&sc->near[1], near);
   }
 }
 
@@ -721,12 +738,13 @@ __global__ void __launch_bounds__(256) k_witness_fix(const int64_t* __restrict__
 }
 
 void stage4_fence(const Graph& g, const Rooting& R, Tags& T, int* low_out, int* high_out, int* head, int* cnt,
-                  int* bmin, cudaStream_t st, Scalars* sc, const Witness* W) {
+                  int* bmin, cudaStream_t st, Scalars* sc, const Witness* W, int* label5, unsigned long long* prop5,
+                  bool s5_if_ordered) {
   const int B = 256;
   const WitnessGate gate = gate_of(W, sc);
   if (!(W && W->on)) {
     launch(k_fence<false>, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, low_out, high_out,
-           head, cnt, bmin, T.tour_len, gate, (int*)nullptr, sc);
+           head, cnt, bmin, T.tour_len, gate, (int*)nullptr, sc, label5, prop5, s5_if_ordered);
     note(K_FENCE);
     return;
   }
@@ -734,7 +752,7 @@ void stage4_fence(const Graph& g, const Rooting& R, Tags& T, int* low_out, int* 
   // then the full gather / tile / fence -- which return at once unless the
   // repair list overflowed (WitnessGate)
   launch(k_fence<true>, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, (int*)nullptr,
-         (int*)nullptr, head, cnt, bmin, T.tour_len, gate, W->und_list, sc);
+         (int*)nullptr, head, cnt, bmin, T.tour_len, gate, W->und_list, sc, label5, prop5, s5_if_ordered);
   note(K_FENCE);
   launch(k_witness_fix, grid_for((int64_t)W->cap * 32, B, 16), B, 0, st, g.off, g.adj, g.n, R.rec, T.AP,
          (const int*)W->und_list, T.tour_len, gate);
@@ -747,7 +765,7 @@ void stage4_fence(const Graph& g, const Rooting& R, Tags& T, int* low_out, int* 
   }
   tile_pass(g, T, st, sc, gate);
   launch(k_fence<false>, grid_for(g.n, B), B, 0, st, g.n, R.rec, T.lh1, T.lh2, T.table, T.ntile, (int*)nullptr,
-         (int*)nullptr, head, cnt, bmin, T.tour_len, gate, (int*)nullptr, sc);
+         (int*)nullptr, head, cnt, bmin, T.tour_len, gate, (int*)nullptr, sc, label5, prop5, s5_if_ordered);
   note(K_FENCE);
 }
 
