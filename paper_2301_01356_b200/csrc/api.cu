@@ -224,7 +224,11 @@ struct Pipeline {
     cudaMemsetAsync(sc, 0, sizeof(Scalars), st);
     note(K_MEMSET);
     mk(0);
-    const bool round0 = build_chunk_rows(g, const_cast<int*>(g.crow), sc, st, comp, fe, prop, nlow, w0);
+    // (a run that takes Stage 3 from the sampled arcs reads the chunk -> row table only if its repair
+    // overflows: not built -- 4 bytes per 8 arcs less to write)
+    const bool wrun = W.on && !no_witness && !low_out && !high_out && opts.v[OPT_SAMPLE_ROUNDS] > 0;
+    W.crow_built = !wrun;
+    const bool round0 = build_chunk_rows(g, wrun ? nullptr : const_cast<int*>(g.crow), sc, st, comp, fe, prop, nlow, w0);
     w0_valid = round0;
     stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args(), round0 ? w0 : nullptr, R.nexto);
     mk(1);

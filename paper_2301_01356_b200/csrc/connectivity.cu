@@ -216,6 +216,7 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
     }
     const bool hub = q1 - q0 > kRowChunks;
     if (hub && (int64_t)(q1 - q0) * kItems >= kHubDeg) sc->has_hubs = 1;
+    if (!crow) continue;  // (a witness plan: no arc-balanced pass reads the table unless its repair overflows)
     if (!hub)
       for (int q = q0; q < q1; q++) crow[q] = v;
     unsigned hb = __ballot_sync(0xffffffffu, hub);

@@ -152,6 +152,7 @@ struct Witness {
   int* und_list = nullptr;        // [cap] vertices to repair (a dead Stage-2 array)
   int cap = 0;
   unsigned long long work = 0;    // tour positions the repair may walk in all
+  bool crow_built = true;         // the chunk -> row table exists (else the overflow redo searches the offsets)
 };
 
 void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int* nlow, const Side* side = nullptr,

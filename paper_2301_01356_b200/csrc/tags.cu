@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256, kWGatherMinBlocks) k_w_gather(const int64
 #pragma unroll
         for (int i = 0; i < kItems; i++) w[i] = (a0 + i < a1) ? __ldg(adj + a0 + i) : 0u;
       }
-      int v = __ldg(crow + q);
+      int v = crow ? __ldg(crow + q) : -1;  // (no table: a witness plan's overflow redo)
       if (v < 0) v = row_of(off, 0, n - 1, a0);
       int rs = (int)__ldg(off + v), re = (int)__ldg(off + v + 1);
       int4 r = __ldg(rec + v);
@@ -759,7 +759,8 @@ void stage4_fence(const Graph& g, const Rooting& R, Tags& T, int* low_out, int* 
   note(K_WITNESS_FIX);
   const int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (g.m > 0) {
-    launch(k_w_gather<false, false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec,
+    launch(k_w_gather<false, false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj,
+           W->crow_built ? g.crow : (const int*)nullptr, g.n, g.m, R.rec,
            (const int*)R.firsts, T.AP, (int*)nullptr, gate);
     note(K_W_GATHER);
   }
