@@ -193,7 +193,7 @@ struct Pipeline {
       R.offs[l] = (int*)at(lay.loffs[l]);
     }
     R.rec = (int4*)at(lay.rec);
-    R.firsts = (int*)at(lay.witness ? lay.wfirsts : lay.lh1);  // Stage 3's compact first[] (see stage3_tags)
+    R.firsts = (int*)at(lay.lh1);  // Stage 3's compact first[] (see stage3_tags)
     R.nlow = (int*)at(lay.nlow);
     R.cub_tmp = at(lay.cub);
     R.cub_bytes = lay.cub_bytes;
@@ -211,6 +211,7 @@ struct Pipeline {
     bmin = (int*)at(lay.bmin);
     w0 = (int*)at(lay.w0);
     W.on = lay.witness;
+    W.firsts = lay.witness ? (int*)at(lay.wfirsts) : nullptr;
     W.w0 = w0;
     W.und_list = R.rlist;  // (the root list is dead once the tour is linked)
     W.cap = (int)std::min<int64_t>(n, 1 << 20);
@@ -228,7 +229,9 @@ struct Pipeline {
     // overflows: not built -- 4 bytes per 8 arcs less to write)
     const bool wrun = W.on && !no_witness && !low_out && !high_out && opts.v[OPT_SAMPLE_ROUNDS] > 0;
     W.crow_built = !wrun;
-    const bool round0 = build_chunk_rows(g, wrun ? nullptr : const_cast<int*>(g.crow), sc, st, comp, fe, prop, nlow, w0);
+    R.firsts = wrun ? nullptr : (int*)((char*)sc + (lay.lh1 - lay.sc));  // (k_positions' compact first[]: the full gather's)
+    const bool round0 = build_chunk_rows(g, wrun ? nullptr : const_cast<int*>(g.crow), sc, st, comp, fe, prop,
+                                         wrun ? nullptr : nlow, w0);
     w0_valid = round0;
     stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args(), round0 ? w0 : nullptr, R.nexto);
     mk(1);

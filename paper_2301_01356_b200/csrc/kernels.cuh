@@ -152,6 +152,7 @@ struct Witness {
   int* und_list = nullptr;        // [cap] vertices to repair (a dead Stage-2 array)
   int cap = 0;
   unsigned long long work = 0;    // tour positions the repair may walk in all
+  int* firsts = nullptr;          // [n] compact first[] of the overflow redo (built only then)
   bool crow_built = true;         // the chunk -> row table exists (else the overflow redo searches the offsets)
 };
 

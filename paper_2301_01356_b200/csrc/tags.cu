@@ -121,24 +121,25 @@ struct WitnessGate {
 };
 
 __global__ void k_w_sample(const int64_t* __restrict__ off, int n, const int4* __restrict__ rec,
-                           const int* __restrict__ firsts, const int* __restrict__ w0, int4* AP,
-                           const int* __restrict__ tlen) {
+                           const int* __restrict__ w0, int4* AP, const int* __restrict__ tlen) {
   pdl_enter();
   const int N = *tlen;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     // every per-vertex word first (coalesced, independent of one another),
-    // then the gathers together: one vertex is two dependent round trips,
-    // not five (loaded behind its guards the kernel sat at 30 % of DRAM, 1.0 ms)
-    const int fv = __ldg(firsts + v);
-    const int pv = __ldg(&rec[v].z);
+    // then the gathers together: one vertex is two dependent round trips.
+    // first[w] comes straight from the 16-byte records: at three gathers per
+    // vertex a compact first[] array is not worth k_positions' scattered
+    // 4-byte store per vertex that would build it.
+    const int4 r = __ldg(rec + v);
     const int64_t deg = __ldg(off + v + 1) - __ldg(off + v);
     int w[kWitnessArcs];
 #pragma unroll
     for (int k = 0; k < kWitnessArcs; k++) w[k] = __ldg(w0 + (int64_t)k * n + v);  // (arc 0 of an empty row: unwritten, unused)
+    const int fv = r.x, pv = r.z;
     if (fv >= N) continue;  // detached root: no tour entry
     int f[kWitnessArcs];
 #pragma unroll
-    for (int k = 0; k < kWitnessArcs; k++) f[k] = (deg > k && w[k] != pv) ? __ldg(firsts + w[k]) : fv;
+    for (int k = 0; k < kWitnessArcs; k++) f[k] = (deg > k && w[k] != pv) ? __ldg(&rec[w[k]].x) : fv;
     int m1 = fv, m2 = fv;
 #pragma unroll
     for (int k = 0; k < kWitnessArcs; k++) {
@@ -291,11 +292,13 @@ __global__ void __launch_bounds__(256, kWGatherMinBlocks) k_w_gather(const int64
 
 // compact first[] for the relaxed gather; zeroes the lower-degree counters
 // the gather accumulates into (rows split across warps add atomically)
-__global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ firsts, int* __restrict__ nlow) {
+__global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ firsts, int* __restrict__ nlow,
+                         WitnessGate gate) {
   pdl_enter();
+  if (!gate.open()) return;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     firsts[v] = __ldg(&rec[v].x);
-    nlow[v] = 0;
+    if (nlow) nlow[v] = 0;
   }
 }
 
@@ -564,15 +567,13 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
       launch(k_w_gather<true>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, nullptr, T.AP,
              nullptr, none);
   } else if (witness) {
-    // (compact first[]: its own array, written by k_positions -- the tile pass must not overwrite it)
-    launch(k_w_sample, grid_for(g.n, B), B, 0, st, g.off, g.n, (const int4*)R.rec, (const int*)R.firsts, W->w0, T.AP,
-           T.tour_len);
+    launch(k_w_sample, grid_for(g.n, B), B, 0, st, g.off, g.n, (const int4*)R.rec, W->w0, T.AP, T.tour_len);
     note(K_W_SAMPLE);
   } else {
     // compact first[] lives in lh1 until k_tile overwrites it
     int* firsts = reinterpret_cast<int*>(T.lh1);
     if (R.firsts != firsts || R.nlow != nlow) {  // (else k_positions wrote both)
-      launch(k_firsts, grid_for(g.n, B), B, 0, st, R.rec, g.n, firsts, nlow);
+      launch(k_firsts, grid_for(g.n, B), B, 0, st, R.rec, g.n, firsts, nlow, none);
       note(K_FIRSTS);
     }
     if (g.m > 0)
@@ -759,9 +760,12 @@ void stage4_fence(const Graph& g, const Rooting& R, Tags& T, int* low_out, int* 
   note(K_WITNESS_FIX);
   const int64_t nchunks = (g.m + kItems - 1) / kItems;
   if (g.m > 0) {
+    // (the redo's compact first[]: built only then, into the witness plan's own array)
+    launch(k_firsts, grid_for(g.n, B), B, 0, st, (const int4*)R.rec, g.n, W->firsts, (int*)nullptr, gate);
+    note(K_FIRSTS);
     launch(k_w_gather<false, false>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj,
            W->crow_built ? g.crow : (const int*)nullptr, g.n, g.m, R.rec,
-           (const int*)R.firsts, T.AP, (int*)nullptr, gate);
+           (const int*)W->firsts, T.AP, (int*)nullptr, gate);
     note(K_W_GATHER);
   }
   tile_pass(g, T, st, sc, gate);
