@@ -182,7 +182,7 @@ int fbcc_plan_destroy(fbcc_plan plan);
         repaired exactly, the full per-arc gather only if that repair overflows
         (0 off, 1 plans with m >= 8n, 2 every plan with 2n < 2^30; 1).  Changes
         fbcc_workspace_bytes (4n more).  Runs that export w1/w2/low/high
-        (fbcc_debug) and fbcc_run_host always use the full gather.
+        (fbcc_debug) always use the full gather.
    Keys 2, 5, 6, 7, 9, 10 are retired experiments: accepted and ignored. */
 int fbcc_set_option(int key, int value);
 int fbcc_get_option(int key);

@@ -345,6 +345,10 @@ struct Pipeline {
       stage1_stream_range(g, qb[c], qb[c + 1], comp, fe, st);
     }
     stage1_stream_finish(g, comp, sc, st, root_init_args());
+    // (the whole edge array is here: the rows' first arcs for Stage 5's sampling rounds and, in
+    // witness plans, Stage 3)
+    record_arcs(g, w0, st);
+    w0_valid = g.m > 0;
     mk(1);
     enqueue_rest(st, mk, nullptr, nullptr, ev_label, ev_heads);
     if (io.label) {

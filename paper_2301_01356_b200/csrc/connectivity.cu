@@ -231,6 +231,24 @@ __global__ void k_chunk_rows(const int64_t* __restrict__ off, int n, int* __rest
   if (comp) block_count_add(&sc->near[0], near);
 }
 
+// w0[k][v] = target of arc k of row v (k = 0..2; -1: the row is shorter) -- what k_chunk_rows' round 0
+// records, for the host path, whose edges arrive after that kernel ran
+__global__ void k_record_arcs(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n,
+                              int* __restrict__ w0) {
+  pdl_enter();
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int64_t rs = __ldg(off + v), deg = __ldg(off + v + 1) - rs;
+#pragma unroll
+    for (int k = 0; k < 3; k++) w0[(int64_t)k * n + v] = deg > k ? (int)__ldg(adj + rs + k) : -1;
+  }
+}
+
+void record_arcs(const Graph& g, int* w0, cudaStream_t st) {
+  if (g.m == 0) return;
+  launch(k_record_arcs, grid_for(g.n, 256), 256, 0, st, g.off, g.adj, g.n, w0);
+  note(K_CHUNK_ROWS);
+}
+
 bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp, int2* fe,
                       unsigned long long* prop, int* nlow, int* w0) {
   if (g.m == 0) {

@@ -24,6 +24,9 @@ void widen_offsets(const int* src, int64_t* dst, int64_t n, cudaStream_t st);
 bool build_chunk_rows(const Graph& g, int* crow, Scalars* sc, cudaStream_t st, int* comp = nullptr,
                       int2* fe = nullptr, unsigned long long* prop = nullptr, int* nlow = nullptr, int* w0 = nullptr);
 
+// (host path: the first three arcs of every row, once the edge array has landed)
+void record_arcs(const Graph& g, int* w0, cudaStream_t st);
+
 // Stage 2 initial state written by Stage 1's final compress (one pass over
 // the vertices instead of a separate k_root_flags): flags[v] = v is a root
 // (flags[n] = 0, the scan's tail), lhead[v] = empty out-list (-1) or the hub
