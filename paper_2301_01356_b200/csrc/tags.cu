@@ -121,7 +121,8 @@ struct WitnessGate {
 };
 
 __global__ void k_w_sample(const int64_t* __restrict__ off, int n, const int4* __restrict__ rec,
-                           const int* __restrict__ w0, int4* AP, const int* __restrict__ tlen) {
+                           const int* __restrict__ w0, int4* AP, const int* __restrict__ tlen,
+                           int2* __restrict__ lh1) {
   pdl_enter();
   const int N = *tlen;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
@@ -146,7 +147,12 @@ __global__ void k_w_sample(const int64_t* __restrict__ off, int n, const int4* _
       m1 = min(m1, f[k]);
       m2 = max(m2, f[k]);
     }
-    __stcs(reinterpret_cast<int2*>(AP + fv), make_int2(m1, deg > kWitnessArcs ? (m2 | kExactBit) : m2));
+    const int2 w12 = make_int2(m1, deg > kWitnessArcs ? (m2 | kExactBit) : m2);
+    __stcs(reinterpret_cast<int2*>(AP + fv), w12);
+    // a leaf of the forest (RMAT: most vertices) is its own subtree: its
+    // low / high are these two words, stored here by vertex (coalesced) -- the
+    // tile pass then skips the leaves' queries and their scattered stores
+    if (r.y == fv + 1) lh1[v] = w12;
   }
 }
 
@@ -314,7 +320,14 @@ __global__ void k_firsts(const int4* __restrict__ rec, int n, int* __restrict__ 
 // its own loads.  The staged record carries both the tile values (w1, w2)
 // and the query (v or ~v, partner position): nothing is read from global
 // memory twice.
-constexpr int kTileThreads = 1024;
+#ifndef FBCC_TILE_THREADS
+#define FBCC_TILE_THREADS 1024
+#endif
+#ifndef FBCC_TILE_CTAS
+#define FBCC_TILE_CTAS 1
+#endif
+constexpr int kTileThreads = FBCC_TILE_THREADS;
+constexpr int kTileCtas = FBCC_TILE_CTAS;  // resident CTAs per SM (shared memory: 200 KB at 4096 positions per tile)
 constexpr int kSub = 32;
 constexpr int kNSub = kTile / kSub;  // 128
 constexpr int kSubLev = 32 - __builtin_clz(kNSub);  // levels 0..log2(kNSub) (8 for 128 sub-blocks)
@@ -403,10 +416,10 @@ __device__ __forceinline__ int64_t list_positions(const int* tlen, int64_t N) { 
 
 // (sc != nullptr: the last block to finish also builds every level of the
 // tile-extreme sparse table -- k_table_all's work, one launch fewer)
-__global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict__ AP,
+__global__ void __launch_bounds__(kTileThreads, kTileCtas) k_tile(const int4* __restrict__ AP,
                                                           int64_t N, int ntile, int2* __restrict__ lh1,
                                                           int2* __restrict__ lh2, int2* __restrict__ table0, Scalars* sc, int tlev,
-                                                          const int* tlen, WitnessGate gate) {
+                                                          const int* tlen, WitnessGate gate, bool skip_leaves) {
   pdl_enter();
   if (!gate.open()) return;
   N = list_positions(tlen, N);
@@ -479,6 +492,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const int4* __restrict
       const int4 ap = T[p];
       const int2 q = make_int2(ap.z, ap.w);
       if (q.x >= 0) {  // entry position of v = q.x; partner = last[v]
+        if (skip_leaves && (int64_t)q.y == gp + 1) continue;  // (k_w_sample stored the leaf's own words)
         const int64_t rel = (int64_t)q.y - base;
         lh1[q.x] = (rel < kTile) ? S.range(p, (int)rel) : S.to_end(p);
       } else if ((int64_t)q.y < base) {  // exit position of ~q.x, entry in an earlier tile
@@ -534,13 +548,13 @@ static WitnessGate gate_of(const Witness* W, const Scalars* sc) {
 
 // tile pass + the tile-extreme table (gate: see WitnessGate; an open-ended
 // gate {nullptr} always runs)
-static void tile_pass(const Graph& g, Tags& T, cudaStream_t st, Scalars* sc, WitnessGate gate) {
+static void tile_pass(const Graph& g, Tags& T, cudaStream_t st, Scalars* sc, WitnessGate gate, bool skip_leaves = false) {
   const int B = 256;
   cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
   // (the table in k_tile's last block when it fits one CTA and a ticket word exists)
   Scalars* tsc = (sc && T.ntile <= kTableOneCta && T.tlev > 1) ? sc : nullptr;
-  launch(k_tile, T.ntile < kNumSMs ? T.ntile : kNumSMs, kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile,
-         T.lh1, T.lh2, T.table, tsc, T.tlev, T.tour_len, gate);
+  launch(k_tile, T.ntile < kNumSMs * kTileCtas ? T.ntile : kNumSMs * kTileCtas, kTileThreads, kTileSmem, st, T.AP, 2 * (int64_t)g.n, T.ntile,
+         T.lh1, T.lh2, T.table, tsc, T.tlev, T.tour_len, gate, skip_leaves);
   note(K_TILE);
   if (tsc) {
   } else if (T.ntile <= kTableOneCta) {
@@ -567,7 +581,7 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
       launch(k_w_gather<true>, grid_for(nchunks, B, 32), B, 0, st, g.off, g.adj, g.crow, g.n, g.m, R.rec, nullptr, T.AP,
              nullptr, none);
   } else if (witness) {
-    launch(k_w_sample, grid_for(g.n, B), B, 0, st, g.off, g.n, (const int4*)R.rec, W->w0, T.AP, T.tour_len);
+    launch(k_w_sample, grid_for(g.n, B), B, 0, st, g.off, g.n, (const int4*)R.rec, W->w0, T.AP, T.tour_len, T.lh1);
     note(K_W_SAMPLE);
   } else {
     // compact first[] lives in lh1 until k_tile overwrites it
@@ -594,7 +608,7 @@ void stage3_tags(const Graph& g, const Rooting& R, Tags& T, cudaStream_t st, int
     note(K_SCAN);
     cudaEventRecord(side->ev[1], side->s);
   }
-  tile_pass(g, T, st, sc, none);
+  tile_pass(g, T, st, sc, none, witness);
 }
 
 // ---------------------------------------------------------------------------
