@@ -154,6 +154,7 @@ struct Pipeline {
   Witness W;        // witness plan (Layout::witness); off for a run that exports low / high / w
   int* w0;          // [3][n] each row's arc 0-2 targets (Stage 1's round 0 -> the sampling rounds of Stages 1, 5)
   bool w0_valid = false;
+  bool s1_round0 = false;   // Stage 1 ran its sampling round 0 (the device path; not the streamed host path)
   bool no_witness = false;  // this run exports w1 / w2 / low / high (fbcc_debug)
 
   Pipeline(const int64_t* offsets, const uint32_t* edges, int64_t n, int64_t m, void* workspace,
@@ -233,6 +234,7 @@ struct Pipeline {
     const bool round0 = build_chunk_rows(g, wrun ? nullptr : const_cast<int*>(g.crow), sc, st, comp, fe, prop,
                                          wrun ? nullptr : nlow, w0);
     w0_valid = round0;
+    s1_round0 = round0;
     stage1_forest(g, comp, fe, prop, sc, st, round0, root_init_args(), round0 ? w0 : nullptr, R.nexto);
     mk(1);
     enqueue_rest(st, mk, low_out, high_out, nullptr, nullptr);
@@ -280,7 +282,9 @@ struct Pipeline {
     // in witness plans (dense graphs), else only where the forest is id-ordered (device-side test;
     // k_hook_min, which also tries each row's first arc, does better on fragmented meshes and kNN graphs)
     const bool s5r0 = (opts.v[OPT_SKEL_PARENT] & 0x80) != 0 && opts.v[OPT_SAMPLE_ROUNDS] > 0;
-    const bool s5always = s5r0 && lay.witness;
+    // (not on the host path: its streamed forest is no min-neighbour star forest, and without
+    // k_hook_min's first-arc hooks Stage 5's sample finds no giant there -- config 2 e2e 2.59 -> 2.79 ms)
+    const bool s5always = s5r0 && lay.witness && s1_round0;
     stage4_fence(g, R, T, low_out, high_out, out.head, cnt, bmin, st, sc, &Wr, s5r0 ? out.label : nullptr,
                  s5r0 ? prop : nullptr, s5r0 && !s5always);
     mk(4);
