@@ -70,7 +70,7 @@ def alg_bytes(kind, n, m, T, E, K1=0):
         "positions": n * (16 + 16 + 8 + 4) + 2 * n * 8 * 2,
         "firsts": 16 * n + 4 * n,
         "w_gather": csr + 4 * m + 16 * n + 12 * n,   # first[w] per arc + row record + (w1, w2) + nlow out
-        "w_sample": n * (4 + 4 + 16 + 12 + 12 + 8),  # first, parent, offsets pair, 3 recorded arcs + 3 gathers, (w1, w2) out
+        "w_sample": n * (16 + 8 + 12 + 12 + 8 + 8),  # own record, degree, 3 recorded arcs + 3 gathers, (w1, w2) by tour + by vertex
         "nlow": 16 * n + 8 * n + 4 * n,              # offsets pair, the row's first / last arc, count out
         "tile": 2 * n * 16 + 16 * n,                 # A + P in, partials out
         "fence": n * (16 + 16 + 16 + 4),

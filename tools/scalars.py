@@ -8,7 +8,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 FIELDS = ["ncomp", "giant", "nbccs", "err", "num_edges"] + [f"nroots{i}" for i in range(16)] + \
          [f"hooks{i}" for i in range(16)] + ["nheavy0", "nheavy1", "has_hubs", "ticket", "giant_cnt",
-                                             "tile_ticket", "elist"]
+                                             "tile_ticket", "eheavy", "nmega0", "nmega1", "emega", "nlisted", "tour_len",
+                                             "near0", "near1", "jlist_n0", "jlist_n1", "und_n", "und_work_lo",
+                                             "und_work_hi", "und_big"]
 
 
 def main():
