@@ -330,8 +330,14 @@ constexpr int kPerRoot = FBCC_PER_ROOT;
 // round 2 is skipped -- 4a -0.47 ms; config 2's round 1 hooks 65k, RMAT's
 // 466k.  A ratio against round 0's roots would count RMAT's 16.5 M isolated
 // vertices and starve its giant.)
-__device__ __forceinline__ bool skip_round(const int* hooks, int round, int rbase, int n) {
+// (hub_sc, Stage 1 only: on a graph with hub rows -- RMAT -- a row's third arc
+// is one more hub already in the giant: round 2 hooked 8.7 k of config 5's
+// 0.97 M remaining roots for 0.21 ms, while the hub-free uniform graph needs
+// it -- config 2 +40 % without.  Stage 5 keeps its rounds: its giant only forms there.)
+__device__ __forceinline__ bool skip_round(const int* hooks, int round, int rbase, int n,
+                                           const Scalars* hub_sc = nullptr) {
   if (round < rbase || round < 2) return false;
+  if (hub_sc && hub_sc->has_hubs) return true;
   const int h1 = hooks[round - 1];
   if ((int64_t)h1 * 8192 < (int64_t)n) return true;
   return round > 2 && (int64_t)h1 * 20 < (int64_t)hooks[round - 2];
@@ -351,9 +357,10 @@ __device__ __forceinline__ int64_t sets_left(const int* nroots, const int* hooks
 template <int kPred>
 __global__ void k_propose(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round,
                           int* comp, unsigned long long* prop, PredData pd, const int* __restrict__ nroots,
-                          const int* __restrict__ hooks, bool flat, bool skel_parent, int rbase) {
+                          const int* __restrict__ hooks, bool flat, bool skel_parent, int rbase,
+                          const Scalars* hub_sc) {
   pdl_enter();
-  if (skip_round(hooks, round, rbase, n)) return;
+  if (skip_round(hooks, round, rbase, n, hub_sc)) return;
   // participate iff hash < thr / 2^24, thr = min(1, kPerRoot * roots / n);
   // roots at round start = roots counted after round 0 minus later hooks
   uint32_t thr = 1u << 24;
@@ -416,9 +423,9 @@ __device__ __forceinline__ int sampled_arc(const int64_t* __restrict__ off, cons
 template <bool kRecord>
 __global__ void k_accept(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj, int n, int round, int* comp,
                          unsigned long long* prop, int2* fe, int* hooks, int rbase, const int* __restrict__ warc,
-                         const int* __restrict__ nroots) {
+                         const int* __restrict__ nroots, const Scalars* hub_sc) {
   pdl_enter();
-  if (skip_round(hooks, round, rbase, n) || sets_left(nroots, hooks, round) <= 1) return;
+  if (skip_round(hooks, round, rbase, n, hub_sc) || sets_left(nroots, hooks, round) <= 1) return;
   int hooked = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     unsigned long long key = prop[v];
@@ -509,13 +516,14 @@ __global__ void __launch_bounds__(256, kScan ? kCBlocksScan : kCBlocks) k_compre
                                                   const uint32_t* __restrict__ adj = nullptr,
                                                   const int* __restrict__ warc = nullptr,
                                                   const int* __restrict__ roots0 = nullptr,
-                                                  const int* __restrict__ hooks0 = nullptr) {
+                                                  const int* __restrict__ hooks0 = nullptr,
+                                                  const Scalars* hub_sc = nullptr) {
   pdl_enter();
   int roots = 0;
   int hooked = 0;
   // (roots0: the compress after sampling round `round` >= 1 -- nothing was
   // proposed when a single set was left, see sets_left)
-  const int n_work = ((hooks && skip_round(hooks, round, rbase, n)) ||
+  const int n_work = ((hooks && skip_round(hooks, round, rbase, n, hub_sc)) ||
                       (roots0 && sets_left(roots0, hooks0, round) <= 1)) ? 0 : n;
   const int64_t* hoff = (ri.flags && ri.off && ri.sc->has_hubs) ? ri.off : nullptr;
   if (ri.flags && blockIdx.x == 0 && threadIdx.x == 0) ri.flags[n] = 0;
@@ -1074,15 +1082,16 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
     // 1 always, 2 = auto: graphs of >= 2^22 vertices -- configs 4a/4b/4c/5
     // -1 to -4 %, while config 2 gains +6 % from the two-level trees a folded
     // accept can leave)
+    const Scalars* hub_sc = (kPred == PRED_NONE && slot == 0) ? (const Scalars*)sc : nullptr;  // (skip_round's hub rule)
     const int af = opt(OPT_ACCEPT_FOLD);
     const bool fold = r > 0 && ((cmask >> r) & 1) && (af == 1 || (af == 2 && g.n >= (1 << 22)));
     if (r > 0) {
       launch(k_propose<kPred>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, pd, nroots, hooks, flat,
-             ((opt(OPT_SKEL_PARENT) >> r) & 1) != 0, kBase);
+             ((opt(OPT_SKEL_PARENT) >> r) & 1) != 0, kBase, hub_sc);
       note(K_PROPOSE);
       if (!fold) {
         launch(k_accept<kRecord>, gv, B, 0, st, g.off, g.adj, g.n, r, comp, prop, fe, hooks, kBase, pd.warc,
-               (const int*)nroots);
+               (const int*)nroots, hub_sc);
         note(K_ACCEPT);
       }
     }
@@ -1093,7 +1102,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
       if (fold) {
         launch(k_compress<false, true, kRecord>, gres, B, 0, st, comp, g.n, (int*)nullptr, last_round ? sc : nullptr,
                opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase, prop, hooks + r, fe, g.off, g.adj,
-               pd.warc, (const int*)nroots, (const int*)hooks);
+               pd.warc, (const int*)nroots, (const int*)hooks, hub_sc);
       } else {
         if (r == 0 && jlist && g.n >= kJumpListMinN) {  // id-ordered chains (see k_jump_local)
           launch(k_jump_local, grid_for((g.n + kJumpTile - 1) / kJumpTile, 1, 8), 256, 0, st, comp, g.n, sc, slot ? 1 : 0,
@@ -1107,7 +1116,7 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
                last_round ? sc : nullptr, opt(OPT_GIANT_SKIP) != 0, RootInit{}, skip_hooks, r, kBase,
                (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
                (const uint32_t*)nullptr, (const int*)nullptr, r > 0 ? (const int*)nroots : (const int*)nullptr,
-               (const int*)hooks);
+               (const int*)hooks, hub_sc);
       }
       note(K_COMPRESS);
     }
@@ -1134,8 +1143,8 @@ static void run_cc(const Graph& g, int* comp, int2* fe, unsigned long long* prop
          ri.rootidx ? grid_for((g.n + kCPer - 1) / kCPer, B, kCBlocksScan) : gres, B, 0, st, comp, g.n, nroots + 7,
          nullptr, false, ri, (const int*)nullptr, 0, 0,
          (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr, (const int64_t*)nullptr,
-         (const uint32_t*)nullptr, (const int*)nullptr, (const int*)nullptr,
-         (const int*)nullptr);  // final root count (= components)
+         (const uint32_t*)nullptr, (const int*)nullptr, (const int*)nullptr, (const int*)nullptr,
+         (const Scalars*)nullptr);  // final root count (= components)
   note(K_COMPRESS);
 }
 
@@ -1198,7 +1207,7 @@ void stage1_stream_finish(const Graph& g, int* comp, Scalars* sc, cudaStream_t s
          B, 0, st, comp, g.n, sc->nroots + 7, nullptr, false, ri,
          (const int*)nullptr, 0, 0, (unsigned long long*)nullptr, (int*)nullptr, (int2*)nullptr,
          (const int64_t*)nullptr, (const uint32_t*)nullptr, (const int*)nullptr, (const int*)nullptr,
-         (const int*)nullptr);
+         (const int*)nullptr, (const Scalars*)nullptr);
   note(K_COMPRESS);
 }
 
