@@ -101,28 +101,72 @@ __device__ __forceinline__ void publish_roots(const unsigned long long* rootidx,
   sc->tour_len = 2 * (n - hi32(t));
 }
 
-struct UpperDegree {
-  const int64_t* off;
-  const int* nlow;
-  int n;
-  __host__ __device__ int operator()(int v) const {
-    return v < n ? (int)(off[v + 1] - off[v]) - nlow[v] : 0;
-  }
-};
-using UpperIt = cub::TransformInputIterator<int, UpperDegree, cub::CountingInputIterator<int>>;
+// Edge numbering: uoff[v] = upper arcs (u -> w, u < w) of the rows before v,
+// v in [0, n]; uoff[n] = E.  Two levels like the root scan, no library call:
+// k_updeg_local writes each vertex's prefix inside its 1024-vertex tile and
+// the tile's sum, k_scan_tiles (one CTA) the tile prefixes, k_add_tile_prefix
+// adds them in.  (Off the critical path: the pipeline runs it on its side
+// stream beside Stages 3-5.)
+constexpr int kUpTile = 1024;  // 256 threads x 4 consecutive vertices
+__global__ void k_scan_tiles(unsigned long long* __restrict__ tiles, int ntiles,
+                             unsigned long long* __restrict__ total_out, int n, Scalars* sc);
 
-size_t scan_upper_temp_bytes(int n) {
-  size_t bytes = 0;
-  UpperIt it(cub::CountingInputIterator<int>(0), UpperDegree{nullptr, nullptr, n});
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (int*)nullptr, n + 1);
-  return bytes;
+__global__ void __launch_bounds__(256) k_updeg_local(const int64_t* __restrict__ off, const int* __restrict__ nlow,
+                                                     int n, int* __restrict__ uoff,
+                                                     unsigned long long* __restrict__ tsum) {
+  pdl_enter();
+  __shared__ int wtot[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * kUpTile; base < n; base += (int64_t)gridDim.x * kUpTile) {
+    const int v0 = (int)base + 4 * t;
+    int u[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      u[i] = v0 + i < n ? (int)(__ldg(off + v0 + i + 1) - __ldg(off + v0 + i)) - __ldg(nlow + v0 + i) : 0;
+    const int sum = u[0] + u[1] + u[2] + u[3];
+    int incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+      const int x = wtot[w];
+      if (w < warp) before += x;
+      total += x;
+    }
+    int run = before + incl - sum;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      if (v0 + i < n) {
+        uoff[v0 + i] = run;
+        run += u[i];
+      }
+    if (t == 0) tsum[base / kUpTile] = (unsigned long long)total;
+    __syncthreads();  // wtot is rewritten by the next tile
+  }
 }
+
+__global__ void k_add_tile_prefix(int* __restrict__ uoff, const unsigned long long* __restrict__ tpre, int n,
+                                  int ntiles) {
+  pdl_enter();
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x)
+    uoff[v] = v < n ? uoff[v] + (int)__ldg(tpre + v / kUpTile) : (int)__ldg(tpre + ntiles);  // (tpre[ntiles]: the total, E)
+}
+
+size_t scan_upper_temp_bytes(int n) { return 8 * ((size_t)n / kUpTile + 2); }
 
 void scan_upper_degrees(const int64_t* off, const int* nlow, int n, int* uoff, void* tmp, size_t tmp_bytes,
                         cudaStream_t st) {
-  size_t bytes = tmp_bytes;
-  UpperIt it(cub::CountingInputIterator<int>(0), UpperDegree{off, nlow, n});
-  cub::DeviceScan::ExclusiveSum(tmp, bytes, it, uoff, n + 1, st);
+  (void)tmp_bytes;
+  unsigned long long* tsum = reinterpret_cast<unsigned long long*>(tmp);
+  const int ntiles = (n + kUpTile - 1) / kUpTile;
+  launch(k_updeg_local, grid_for(ntiles, 1, 8), 256, 0, st, off, nlow, n, uoff, tsum);
+  launch(k_scan_tiles, 1, 1024, 0, st, tsum, ntiles, tsum + ntiles, n, (Scalars*)nullptr);
+  launch(k_add_tile_prefix, grid_for(n + 1, 256), 256, 0, st, uoff, (const unsigned long long*)tsum, n, ntiles);
 }
 
 // ---------------------------------------------------------------------------
@@ -176,8 +220,10 @@ __global__ void k_root_list(const int* __restrict__ comp, const unsigned long lo
 // k_compress<kScan>): tile root counts -> exclusive prefixes, in place, by
 // one CTA (n / 1024 entries: 33 k on config 5, 98 k at n = 1e8); also the
 // totals (rootidx[n]) and the counts derived from them.
+// (sc != nullptr: the root scan -- total_out is rootidx + n, and the counts derived
+// from the totals are published; nullptr: the upper-degree scan, total only)
 __global__ void __launch_bounds__(1024) k_scan_tiles(unsigned long long* __restrict__ tiles, int ntiles,
-                                                     unsigned long long* __restrict__ rootidx, int n, Scalars* sc) {
+                                                     unsigned long long* __restrict__ total_out, int n, Scalars* sc) {
   pdl_enter();
   __shared__ unsigned long long wtot[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -201,8 +247,8 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(unsigned long long* __restr
     }
     wtot[lane] = w - x;
     if (lane == 31) {
-      rootidx[n] = w;
-      publish_roots(rootidx, n, sc);
+      *total_out = w;
+      if (sc) publish_roots(total_out - n, n, sc);
     }
   }
   __syncthreads();
@@ -637,7 +683,7 @@ void stage2_rooting_fused(const Graph& g, const int* comp, const int2* fe, Rooti
   // R.flags / R.lhead / R.hsub were written by Stage 1's final compress --
   // and the roots' ranks, when the scan ran inside it
   if (R.tile_roots) {
-    launch(k_scan_tiles, 1, 1024, 0, st, R.tile_roots, (g.n + kRootTile - 1) / kRootTile, R.rootidx, g.n, sc);
+    launch(k_scan_tiles, 1, 1024, 0, st, R.tile_roots, (g.n + kRootTile - 1) / kRootTile, R.rootidx + g.n, g.n, sc);
     note(K_SCAN_TILES);
   } else {
     scan_roots(R.flags, R.rootidx, g.n + 1, R.cub_tmp, R.cub_bytes, st);
