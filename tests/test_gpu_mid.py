@@ -237,6 +237,13 @@ def test_witness_repair_paths(seed, oracle_mod):
             for k in ("label", "head", "is_ap", "edge_label"):
                 assert np.array_equal(r[k], ref[k]), (seed, w, k)
             assert r["num_bccs"] == ref["num_bccs"] and r["num_components"] == ref["num_components"]
+            if w:  # the host path records the rows' first arcs itself (k_record_arcs) before sampling them
+                from paper_2301_01356_b200 import Graph, fast_bcc
+
+                lab = fast_bcc(Graph(g.offsets, g.edges).pin())
+                for k in ("label", "head", "is_ap", "edge_label"):
+                    assert np.array_equal(np.asarray(getattr(lab, k)).astype(ref[k].dtype), ref[k]), (seed, w, "host", k)
+                assert lab.num_bccs == ref["num_bccs"]
     finally:
         _lib.set_option("witness", old)
 
