@@ -131,8 +131,9 @@ __global__ void k_w_sample(const int64_t* __restrict__ off, int n, const int4* _
     // first[w] comes straight from the 16-byte records: at three gathers per
     // vertex a compact first[] array is not worth k_positions' scattered
     // 4-byte store per vertex that would build it.
-    const int4 r = __ldg(rec + v);
     const int64_t deg = __ldg(off + v + 1) - __ldg(off + v);
+    if (deg == 0) continue;  // (RMAT: half the vertices -- no record, no arcs to read; its tour slot, if any, keeps (first, first))
+    const int4 r = __ldg(rec + v);
     int w[kWitnessArcs];
 #pragma unroll
     for (int k = 0; k < kWitnessArcs; k++) w[k] = __ldg(w0 + (int64_t)k * n + v);  // (arc 0 of an empty row: unwritten, unused)
