@@ -251,12 +251,14 @@ struct EdgeFix {
 // any adjacency -- on RMAT that is all but ~4 M of the 33.5 M rows.  Rows of
 // <= 32 arcs are handled by their own lane, longer ones by the whole warp,
 // rows over kEdgeSuperRow arcs are deferred to k_edge_search (whole grid).
-// sreq[v] (every v written): v's lower-arc fix is k_edge_search's.
+// sreq bit v (one 32-bit word per warp step, every word written): v's
+// lower-arc fix is k_edge_search's.  (A bitmap: 4 bytes per 32 rows to write
+// here and to read in the two passes that follow, not 4 per row.)
 __global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                   int n, const int* __restrict__ label, const int* __restrict__ head,
                                                   const int* __restrict__ uoff, const int* __restrict__ nlow,
                                                   int* edge_label, int* bmin, LongRows heavy,
-                                                  int* __restrict__ sreq, Scalars* sc) {
+                                                  unsigned* __restrict__ sreq, Scalars* sc) {
   pdl_enter();
   EdgeFix f;
   f.init(off, adj, label, head, uoff, nlow, edge_label, bmin, sc);
@@ -300,7 +302,8 @@ __global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ of
       r = __any_sync(0xffffffffu, r);
       if (lane == src) req = r;
     }
-    if (v < n) sreq[v] = req;
+    const unsigned rb = __ballot_sync(0xffffffffu, req);
+    if (lane == 0) sreq[base >> 5] = rb;
   }
   f.flush();
 }
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(256) k_edge_search(const int64_t* __restrict__
                                                      const int* __restrict__ label, const int* __restrict__ head,
                                                      const int* __restrict__ uoff, const int* __restrict__ nlow,
                                                      int* edge_label, int* bmin, LongRows heavy,
-                                                     int* sreq, int* spos, Scalars* sc) {
+                                                     unsigned* sreq, int* spos, Scalars* sc) {
   pdl_enter();
   EdgeFix f;
   f.init(off, adj, label, head, uoff, nlow, edge_label, bmin, sc);
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(256) k_edge_search(const int64_t* __restrict__
       [&](int v, int64_t a) {
         if (f.arc(v, lu, hl, row_u0, ebase, a, (int)__ldg(adj + a))) {
           spos[v] = f.fix_lower(v, lu, hl);  // (k_edge_final maps it; a repeat below is idempotent)
-          sreq[v] = 1;
+          atomicOr(sreq + (v >> 5), 1u << (v & 31));
         }
       });
   f.flush();
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(256) k_edge_search(const int64_t* __restrict__
   const int64_t warps = stride >> 5;
   for (int64_t base = (tid >> 5) * 32; base < n; base += warps * 32) {
     const int64_t v = base + lane;
-    const bool r = v < n && sreq[v];  // (plain load: the deferred rows above set theirs)
+    const bool r = v < n && ((sreq[base >> 5] >> lane) & 1u);  // (plain load: the deferred rows above set theirs)
     const unsigned b = __ballot_sync(0xffffffffu, r);
     if (r) wq[cnt + __popc(b & ((1u << lane) - 1))] = (int)v;
     cnt += __popc(b);
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ 
                                                     const int* __restrict__ label, const int* __restrict__ uoff,
                                                     const int* __restrict__ nlow, int* edge_label,
                                                     const int* __restrict__ bmin, LongRows heavy,
-                                                    const int* __restrict__ sreq, const int* __restrict__ spos,
+                                                    const unsigned* __restrict__ sreq, const int* __restrict__ spos,
                                                     const Scalars* sc) {
   pdl_enter();
   const int E = __ldg(uoff + n);
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ 
           e1 = __ldg(uoff + v + 1);
           if (__ldg(off + v + 1) - __ldg(off + v) > kEdgeSuperRow) e1 = e0;  // deferred row: below
         }
-        if (__ldg(sreq + v)) edge_map(edge_label, bmin, __ldg(spos + v));
+        if ((__ldg(sreq + (base >> 5)) >> lane) & 1u) edge_map(edge_label, bmin, __ldg(spos + v));
       }
       const bool coop = e1 - e0 > 32;
       if (!coop)
@@ -481,13 +484,13 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
     note(K_EDGE_FILL);
     LongRows hv{heavy, n, &sc->eheavy, &sc->emega};  // (a dead n-int Stage-2 array, see api.cu)
     launch(k_edge_fix, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin, hv,
-           sreq, sc);
+           reinterpret_cast<unsigned*>(sreq), sc);
     note(K_EDGE_BLOCKS);
     launch(k_edge_search, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin,
-           hv, sreq, spos, sc);
+           hv, reinterpret_cast<unsigned*>(sreq), spos, sc);
     note(K_EDGE_SEARCH);
     launch(k_edge_final, grid_for(n, B, 32), B, 0, st, g.off, n, label, uoff, nlow, edge_label, bmin, hv,
-           (const int*)sreq, (const int*)spos, (const Scalars*)sc);
+           (const unsigned*)sreq, (const int*)spos, (const Scalars*)sc);
     note(K_EDGE_FINAL);
   }
   if (side) cudaStreamWaitEvent(st, side->ev[3], 0);  // join the articulation flags
