@@ -165,7 +165,7 @@ inline void launch(void (*kernel)(KArgs...), int grid, int block, size_t smem, c
 inline void note(KernelKind k) {
   LaunchLog* L = g_log;
   if (!L) return;
-  if (k != K_MEMSET) L->count += (k == K_SCAN) ? 3 : 1;  // the upper-degree scan: tile-local prefixes, tile scan, add
+  if (k != K_MEMSET) L->count += (k == K_SCAN) ? 2 : 1;  // the upper-degree scan: tile-local prefixes, tile scan
   if (L->profile && L->nrec < LaunchLog::kMax) {
     L->record(L->nrec + 1);
     L->kind[L->nrec++] = k;

@@ -182,6 +182,19 @@ void export_debug(const Graph& g, const int2* fe, const int4* rec, const int4* A
                   int* parent, int* first, int* last, int* w1, int* w2, uint8_t* fence,
                   cudaStream_t st, const int* tour_len = nullptr);
 
+// Edge ids.  scan_upper_degrees leaves each vertex's prefix inside its kUpTile-vertex tile in uoff and
+// the tile prefixes (then the total, E) in its scratch buffer; Stage 6 adds the two as it reads them
+// (UpOff::at) -- no pass over the vertices to add them in.
+constexpr int kUpTile = 1024;
+struct UpOff {
+  const int* loc;                   // [n] prefix inside the tile
+  const unsigned long long* tpre;  // [tiles + 1] tile prefixes, then the total
+  int n, ntiles;
+  __device__ __forceinline__ int at(int v) const {  // upper arcs of the rows before v; v == n: E
+    return v < n ? __ldg(loc + v) + (int)__ldg(tpre + v / kUpTile) : (int)__ldg(tpre + ntiles);
+  }
+};
+
 size_t scan_temp_bytes(int64_t items);
 // uoff[v] = sum over u < v of (deg(u) - nlow[u]), v in [0, n] (uoff[n] = E)
 size_t scan_upper_temp_bytes(int n);

@@ -111,7 +111,7 @@ __device__ __forceinline__ int big_giant(const int* label, const Scalars* sc) {
 // edge id of upper arc a of row u: uoff[u] + (a - first upper arc)
 __global__ void k_giant_min(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                             const int* __restrict__ label, const int* __restrict__ head,
-                            const int* __restrict__ uoff, const int* __restrict__ nlow, int* bmin, const Scalars* sc) {
+                            UpOff uoff, const int* __restrict__ nlow, int* bmin, const Scalars* sc) {
   pdl_enter();
   const int G = big_giant(label, sc);
   if (G < 0) return;
@@ -130,16 +130,16 @@ __global__ void k_giant_min(const int64_t* __restrict__ off, const uint32_t* __r
     }
     const unsigned b = __ballot_sync(0xffffffffu, hit);
     if (b) {
-      if (lane == __ffs(b) - 1) bmin[G] = __ldg(uoff + u0) + (int)(a - a0);
+      if (lane == __ffs(b) - 1) bmin[G] = uoff.at(u0) + (int)(a - a0);
       return;
     }
   }
 }
 
-__global__ void k_edge_fill(int n, const int* __restrict__ label, const int* __restrict__ uoff,
+__global__ void k_edge_fill(int n, const int* __restrict__ label, UpOff uoff,
                             const int* __restrict__ bmin, int* __restrict__ edge_label, Scalars* sc) {
   pdl_enter();
-  const int E = __ldg(uoff + n);
+  const int E = uoff.at(n);
   if (blockIdx.x == 0 && threadIdx.x == 0) sc->num_edges = E;
   const int G = big_giant(label, sc);
   if (G < 0) return;
@@ -163,7 +163,7 @@ struct EdgeFix {
   const uint32_t* adj;
   const int* label;
   const int* head;
-  const int* uoff;
+  UpOff uoff;
   const int* nlow;
   int* edge_label;
   int* bmin;
@@ -171,7 +171,7 @@ struct EdgeFix {
   int run_blk, run_min;
 
   __device__ __forceinline__ void init(const int64_t* o, const uint32_t* a, const int* lb, const int* hd,
-                                       const int* uo, const int* nl, int* el, int* bm, const Scalars* sc) {
+                                       UpOff uo, const int* nl, int* el, int* bm, const Scalars* sc) {
     off = o;
     adj = a;
     label = lb;
@@ -200,7 +200,7 @@ struct EdgeFix {
     hl = __ldg(head + lu);
     const int hv = v == lu ? hl : -1;  // head[v] >= 0 only at label vertices
     row_u0 = hv >= 0 && v < hv;
-    ebase = __ldg(uoff + v) - (int)(rs + __ldg(nlow + v));
+    ebase = uoff.at(v) - (int)(rs + __ldg(nlow + v));
   }
   // one arc of non-giant row v; returns true for the lower arc to the head of
   // v's block when that head is in G (the edge sits in the head's G row)
@@ -239,7 +239,7 @@ struct EdgeFix {
       const int64_t mid = (lo + hi) >> 1;
       if ((int)__ldg(adj + mid) < v) lo = mid + 1; else hi = mid;
     }
-    const int e = __ldg(uoff + x) + (int)(lo - ub);
+    const int e = uoff.at(x) + (int)(lo - ub);
     mark(e, lu);
     if (x < lu) atomicMin(bmin + lu, e);
     return e;
@@ -256,7 +256,7 @@ struct EdgeFix {
 // here and to read in the two passes that follow, not 4 per row.)
 __global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                   int n, const int* __restrict__ label, const int* __restrict__ head,
-                                                  const int* __restrict__ uoff, const int* __restrict__ nlow,
+                                                  UpOff uoff, const int* __restrict__ nlow,
                                                   int* edge_label, int* bmin, LongRows heavy,
                                                   unsigned* __restrict__ sreq, Scalars* sc) {
   pdl_enter();
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(256) k_edge_fix(const int64_t* __restrict__ of
 __global__ void __launch_bounds__(256) k_edge_search(const int64_t* __restrict__ off,
                                                      const uint32_t* __restrict__ adj, int n,
                                                      const int* __restrict__ label, const int* __restrict__ head,
-                                                     const int* __restrict__ uoff, const int* __restrict__ nlow,
+                                                     UpOff uoff, const int* __restrict__ nlow,
                                                      int* edge_label, int* bmin, LongRows heavy,
                                                      unsigned* sreq, int* spos, Scalars* sc) {
   pdl_enter();
@@ -379,13 +379,13 @@ __device__ __forceinline__ void edge_map(int* edge_label, const int* bmin, int e
 // searched positions and the deferred rows; otherwise every edge (16-byte
 // streaming loads and stores).
 __global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ off, int n,
-                                                    const int* __restrict__ label, const int* __restrict__ uoff,
+                                                    const int* __restrict__ label, UpOff uoff,
                                                     const int* __restrict__ nlow, int* edge_label,
                                                     const int* __restrict__ bmin, LongRows heavy,
                                                     const unsigned* __restrict__ sreq, const int* __restrict__ spos,
                                                     const Scalars* sc) {
   pdl_enter();
-  const int E = __ldg(uoff + n);
+  const int E = uoff.at(n);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int G = big_giant(label, sc);
@@ -397,8 +397,8 @@ __global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ 
       int e0 = 0, e1 = 0;
       if (v < n) {
         if (__ldg(label + v) != G) {
-          e0 = __ldg(uoff + v);
-          e1 = __ldg(uoff + v + 1);
+          e0 = uoff.at(v);
+          e1 = uoff.at(v + 1);
           if (__ldg(off + v + 1) - __ldg(off + v) > kEdgeSuperRow) e1 = e0;  // deferred row: below
         }
         if ((__ldg(sreq + (base >> 5)) >> lane) & 1u) edge_map(edge_label, bmin, __ldg(spos + v));
@@ -416,10 +416,10 @@ __global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ 
     }
     int eb = 0;  // (the deferred rows' upper arcs: edge ids eb + a)
     heavy.visit(
-        off, [&](int v, int64_t rs) { eb = __ldg(uoff + v) - (int)(rs + __ldg(nlow + v)); },
+        off, [&](int v, int64_t rs) { eb = uoff.at(v) - (int)(rs + __ldg(nlow + v)); },
         [&](int v, int64_t a) {
           const int e = eb + (int)a;
-          if (e >= __ldg(uoff + v)) edge_map(edge_label, bmin, e);
+          if (e >= uoff.at(v)) edge_map(edge_label, bmin, e);
         });
     return;
   }
@@ -440,8 +440,8 @@ __global__ void __launch_bounds__(256) k_edge_final(const int64_t* __restrict__ 
   }
 }
 
-__global__ void k_set_edges(const int* __restrict__ uoff, int n, Scalars* sc) {
-  pdl_enter(); sc->num_edges = uoff[n]; }
+__global__ void k_set_edges(UpOff uoff, int n, Scalars* sc) {
+  pdl_enter(); sc->num_edges = uoff.at(n); }
 
 void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* head, uint8_t* is_ap,
                       int* edge_label, int* cnt, int* uoff, int* nlow, int* bmin, int* heavy, int* sreq, int* spos,
@@ -474,22 +474,24 @@ void stage6_labelling(const Graph& g, const int4* rec, const int* label, int* he
     scan_upper_degrees(g.off, nlow, n, uoff, cub_tmp, cub_bytes, st);
     note(K_SCAN);
   }
+  // (edge ids: the tile-local prefixes in uoff plus the tile prefixes scan_upper_degrees left in cub_tmp)
+  const UpOff up{uoff, reinterpret_cast<const unsigned long long*>(cub_tmp), n, (n + kUpTile - 1) / kUpTile};
   if (!edge_label || g.m == 0) {
-    launch(k_set_edges, 1, 1, 0, st, uoff, n, sc);
+    launch(k_set_edges, 1, 1, 0, st, up, n, sc);
     note(K_SET_EDGES);
   } else {
-    launch(k_giant_min, 1, 32, 0, st, g.off, g.adj, label, head, uoff, nlow, bmin, (const Scalars*)sc);
+    launch(k_giant_min, 1, 32, 0, st, g.off, g.adj, label, head, up, (const int*)nlow, bmin, (const Scalars*)sc);
     note(K_GIANT_MIN);
-    launch(k_edge_fill, grid_for(g.m / 8 + 1, B), B, 0, st, n, label, uoff, bmin, edge_label, sc);
+    launch(k_edge_fill, grid_for(g.m / 8 + 1, B), B, 0, st, n, label, up, (const int*)bmin, edge_label, sc);
     note(K_EDGE_FILL);
     LongRows hv{heavy, n, &sc->eheavy, &sc->emega};  // (a dead n-int Stage-2 array, see api.cu)
-    launch(k_edge_fix, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin, hv,
+    launch(k_edge_fix, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, (const int*)head, up, (const int*)nlow, edge_label, bmin, hv,
            reinterpret_cast<unsigned*>(sreq), sc);
     note(K_EDGE_BLOCKS);
-    launch(k_edge_search, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, head, uoff, nlow, edge_label, bmin,
+    launch(k_edge_search, grid_for(n, B, 32), B, 0, st, g.off, g.adj, n, label, (const int*)head, up, (const int*)nlow, edge_label, bmin,
            hv, reinterpret_cast<unsigned*>(sreq), spos, sc);
     note(K_EDGE_SEARCH);
-    launch(k_edge_final, grid_for(n, B, 32), B, 0, st, g.off, n, label, uoff, nlow, edge_label, bmin, hv,
+    launch(k_edge_final, grid_for(n, B, 32), B, 0, st, g.off, n, label, up, (const int*)nlow, edge_label, (const int*)bmin, hv,
            (const unsigned*)sreq, (const int*)spos, (const Scalars*)sc);
     note(K_EDGE_FINAL);
   }

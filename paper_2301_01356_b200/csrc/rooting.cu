@@ -104,10 +104,10 @@ __device__ __forceinline__ void publish_roots(const unsigned long long* rootidx,
 // Edge numbering: uoff[v] = upper arcs (u -> w, u < w) of the rows before v,
 // v in [0, n]; uoff[n] = E.  Two levels like the root scan, no library call:
 // k_updeg_local writes each vertex's prefix inside its 1024-vertex tile and
-// the tile's sum, k_scan_tiles (one CTA) the tile prefixes, k_add_tile_prefix
-// adds them in.  (Off the critical path: the pipeline runs it on its side
+// the tile's sum, k_scan_tiles (one CTA) the tile prefixes; Stage 6 adds the
+// two as it reads them (UpOff, kernels.cuh).  (Off the critical path: the pipeline runs it on its side
 // stream beside Stages 3-5.)
-constexpr int kUpTile = 1024;  // 256 threads x 4 consecutive vertices
+// (kUpTile = 1024, kernels.cuh: 256 threads x 4 consecutive vertices)
 __global__ void k_scan_tiles(unsigned long long* __restrict__ tiles, int ntiles,
                              unsigned long long* __restrict__ total_out, int n, Scalars* sc);
 
@@ -150,13 +150,6 @@ __global__ void __launch_bounds__(256) k_updeg_local(const int64_t* __restrict__
   }
 }
 
-__global__ void k_add_tile_prefix(int* __restrict__ uoff, const unsigned long long* __restrict__ tpre, int n,
-                                  int ntiles) {
-  pdl_enter();
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x)
-    uoff[v] = v < n ? uoff[v] + (int)__ldg(tpre + v / kUpTile) : (int)__ldg(tpre + ntiles);  // (tpre[ntiles]: the total, E)
-}
-
 size_t scan_upper_temp_bytes(int n) { return 8 * ((size_t)n / kUpTile + 2); }
 
 void scan_upper_degrees(const int64_t* off, const int* nlow, int n, int* uoff, void* tmp, size_t tmp_bytes,
@@ -166,7 +159,6 @@ void scan_upper_degrees(const int64_t* off, const int* nlow, int n, int* uoff, v
   const int ntiles = (n + kUpTile - 1) / kUpTile;
   launch(k_updeg_local, grid_for(ntiles, 1, 8), 256, 0, st, off, nlow, n, uoff, tsum);
   launch(k_scan_tiles, 1, 1024, 0, st, tsum, ntiles, tsum + ntiles, n, (Scalars*)nullptr);
-  launch(k_add_tile_prefix, grid_for(n + 1, 256), 256, 0, st, uoff, (const unsigned long long*)tsum, n, ntiles);
 }
 
 // ---------------------------------------------------------------------------
