@@ -353,6 +353,10 @@ struct Pipeline {
     // witness plans, Stage 3)
     record_arcs(g, w0, st);
     w0_valid = g.m > 0;
+    // (the streamed forest is no min-neighbour forest: the samples leave more fence bits open and
+    // the repair walks bigger subtrees -- worth it from a few million vertices up: config 5 Stages 3-4
+    // 5.5 -> 3.0 ms, but config 2 0.16 -> 0.28 ms)
+    if (g.n < (1 << 22)) no_witness = true;
     mk(1);
     enqueue_rest(st, mk, nullptr, nullptr, ev_label, ev_heads);
     if (io.label) {

@@ -81,6 +81,19 @@ def test_large_config(name):
     assert _sha(res["is_ap"]) == meta["is_ap_sha256"], "is_ap"
     assert _sha(res["edge_label"]) == meta["edge_label_sha256"], "edge_label"
 
+    if name == "5":  # the host path at this size too: streamed upload, the rows' first arcs recorded on the
+        # device after it, sampled tags with the repair on the streamed forest (plans of n >= 2^22, m >= 8n)
+        from paper_2301_01356_b200 import Graph, fast_bcc
+
+        lab = fast_bcc(Graph(offsets.astype(np.int64, copy=False), edges).pin())
+        assert lab.num_bccs == meta["num_bccs"] and lab.num_components == meta["num_components"]
+        assert _sha(np.asarray(lab.label)) == meta["label_sha256"], "host path: label"
+        assert _sha(np.asarray(lab.head)) == meta["head_sha256"], "host path: head"
+        assert _sha(np.asarray(lab.edge_label)) == meta["edge_label_sha256"], "host path: edge_label"
+        assert _sha(np.asarray(lab.is_ap).astype(np.uint8)) == meta["is_ap_sha256"], "host path: is_ap"
+        del lab
+        torch.cuda.empty_cache()
+
     oracle_s = None
     if os.environ.get("FBCC_LARGE") == "1":  # element-wise against the C oracle too
         import oracle
